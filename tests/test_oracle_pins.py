@@ -1,0 +1,438 @@
+"""Pins of the CPU oracle against things other than itself (-m "not gpu").
+
+Every oracle function is checked against worked examples printed in SPEC.md
+(tests/golden/spec_examples.json, each cited), closed forms, brute force on
+tiny inputs, or invariants the paper states.
+"""
+import json
+import os
+from fractions import Fraction
+import itertools
+
+import numpy as np
+import pytest
+
+import workload as WL
+from oracle import cluster as C
+from oracle import pipeline as P
+from oracle import prf, routing as R, step as S
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ----------------------------------------------------------------------------- prf
+def test_splitmix64_reference_vectors():
+    for x, y in GOLD["splitmix64"]["cases"]:
+        x = int(x, 16) if isinstance(x, str) else x
+        got = int(prf.splitmix64(np.array([x], dtype=np.uint64))[0])
+        assert got == int(y, 16)
+
+
+def test_init_rows_deterministic_and_seeded():
+    keys = np.array([3, 7, (2 << 40) | 11], dtype=np.int64)
+    a = prf.init_rows(1, keys, 16)
+    assert np.array_equal(a, prf.init_rows(1, keys, 16))
+    assert not np.array_equal(a, prf.init_rows(2, keys, 16))
+    # a row depends only on (seed, key, j): order/batching independent
+    assert np.array_equal(prf.init_rows(1, keys[::-1], 16), a[::-1])
+
+
+def test_init_rows_range_and_moments():
+    d = 16
+    v = prf.init_rows(5, np.arange(10000), d).astype(np.float64).ravel()
+    lim = 1 / np.sqrt(d)
+    assert v.min() >= -lim - 1e-7 and v.max() < lim
+    # uniform on [-lim, lim): mean 0, var lim^2/3; 3-sigma Monte Carlo
+    n = len(v)
+    assert abs(v.mean()) < 3 * lim / np.sqrt(3 * n)
+    assert abs(v.var() - lim ** 2 / 3) < 0.02 * lim ** 2
+
+
+def test_init_rows_single_rounding_exact():
+    """v must be the correctly rounded value of lo + scale*u (what fmaf gives),
+    checked with exact rational arithmetic."""
+    d = 128
+    keys = np.arange(50)
+    h = prf.prf_words(9, keys, d)
+    v = prf.init_rows(9, keys, d)
+    lo = Fraction(float(np.float32(-1.0 / np.sqrt(d))))
+    sc = Fraction(float(np.float32(2.0 / np.sqrt(d))))
+    for i in range(0, 50, 7):
+        for j in range(0, d, 13):
+            u = Fraction(int(h[i, j]) >> 40, 1 << 24)
+            exact = lo + sc * u
+            # round-to-nearest fp32 of the exact rational
+            f = np.float32(float(exact))
+            cands = [np.nextafter(f, np.float32(-1)), f, np.nextafter(f, np.float32(1))]
+            best = min(cands, key=lambda c: abs(Fraction(float(c)) - exact))
+            assert v[i, j] == best
+
+
+def test_init_rows_dyadic_values():
+    v = prf.init_rows(3, np.arange(4000), 8, "dyadic").ravel() * 256
+    assert np.array_equal(v, np.round(v)) and v.min() == -8 and v.max() == 7
+    counts = np.bincount((v + 8).astype(int), minlength=16)
+    assert counts.min() > 0.8 * len(v) / 16
+
+
+# ----------------------------------------------------------------------------- routing
+def test_spec_dedup_and_shard_examples():
+    for c in GOLD["dedup"]["cases"]:
+        u, inv = R.dedup(np.array(c["keys"], dtype=np.int64))
+        assert u.tolist() == c["unique"] and inv.tolist() == c["inverse"]
+    for k, W, o in GOLD["shard_of"]["cases"]:
+        assert int(R.shard_of(np.array([k]), W)[0]) == o
+    for a, b in GOLD["canonical_key_order"]["cases"]:
+        assert R.dedup(np.array(a, dtype=np.int64))[0].tolist() == b
+
+
+def test_spec_all_to_all_example():
+    g = GOLD["all_to_all"]
+    assert R.all_to_all(g["payloads"]) == g["expect"]
+    with pytest.raises(ValueError):
+        R.all_to_all([[1], [2, 3]])
+
+
+def test_spec_stage_key_routing_example():
+    g = GOLD["stage_key_routing"]
+    batches = [(np.array(k, dtype=np.int64), np.array([0, len(k)], np.int32)) for k in g["worker_keys"]]
+    _, own = R.route_all(batches, g["W"])
+    assert [o.owner_keys.tolist() for o in own] == g["owner_requests"]
+
+
+def _brute_route(keys, W, mb_occ, N):
+    keys = [int(k) for k in keys]
+    uniq = sorted(set(keys), key=lambda k: ((k & R.ROW_MASK) % W, k))
+    inverse = [uniq.index(k) for k in keys]
+    counts = [sum(1 for k in uniq if (k & R.ROW_MASK) % W == o) for o in range(W)]
+    mask = [0] * len(uniq)
+    for j, k in enumerate(keys):
+        mask[uniq.index(k)] |= 1 << int(mb_occ[j])
+    return uniq, inverse, counts, mask
+
+
+@pytest.mark.parametrize("W,N,seed", [(1, 1, 0), (2, 2, 1), (3, 4, 2), (4, 3, 3)])
+def test_route_source_brute_force(W, N, seed):
+    cfg = WL.CONFIGS["tiny"]
+    keys, offs = WL.gen_batch(cfg, seed, 0, 0, batch=24)
+    perm, mbo = C.cluster_sequential(24, N) if 24 % N == 0 else C.cluster_sequential(24, 1)
+    Nn = len(mbo) - 1
+    mb = R.mb_of_occurrence(offs, cfg.num_features, perm, mbo)
+    rs = R.route_source(keys, W, mb, Nn)
+    uniq, inverse, counts, mask = _brute_route(keys, W, mb, Nn)
+    assert rs.uniq.tolist() == uniq
+    assert rs.inverse.tolist() == inverse
+    assert rs.send_counts.tolist() == counts
+    assert rs.send_offsets.tolist() == [0] + list(np.cumsum(counts))
+    assert rs.mask.tolist() == mask
+    # invariants named by BASELINE north_star: counts sum to unique keys and
+    # every key lands on owner = row mod W
+    assert rs.send_counts.sum() == len(set(keys.tolist()))
+    for o in range(W):
+        seg = rs.uniq[rs.send_offsets[o]:rs.send_offsets[o + 1]]
+        assert ((seg & R.ROW_MASK) % W == o).all()
+        assert (np.diff(seg) > 0).all()
+    assert np.array_equal(rs.uniq[rs.inverse], keys)
+    for i in range(Nn):
+        has = [(m >> i) & 1 for m in mask]
+        # pos_i = rank among mask-bit-i keys (brute force)
+        for u in range(len(uniq)):
+            if has[u]:
+                assert rs.pos[i][u] == sum(has[:u])
+        assert rs.mb_counts[i].sum() == sum(has)
+
+
+def test_route_owner_conservation_and_dedup():
+    cfg = WL.CONFIGS["tiny"]
+    W, N = 3, 2
+    batches = [WL.gen_batch(cfg, 7, 0, r, batch=16) for r in range(W)]
+    mbs = [R.mb_of_occurrence(b[1], 4, *C.cluster_sequential(16, N)) for b in batches]
+    src, own = R.route_all(batches, W, mbs, N)
+    assert sum(s.send_counts.sum() for s in src) == sum(len(o.recv_keys) for o in own)
+    for o, ow in enumerate(own):
+        union = set()
+        for s in range(W):
+            union |= set(src[s].uniq[src[s].send_offsets[o]:src[s].send_offsets[o + 1]].tolist())
+        assert ow.owner_keys.tolist() == sorted(union)              # P:347 second dedup
+        assert np.array_equal(ow.owner_keys[ow.owner_inv], ow.recv_keys)
+        for i in range(N):
+            for s in range(W):
+                lst = ow.send_lists[i][s]
+                expect = [k for k in src[s].uniq[src[s].send_offsets[o]:src[s].send_offsets[o + 1]]
+                          if (src[s].mask[np.searchsorted(src[s].uniq[src[s].send_offsets[o]:src[s].send_offsets[o+1]], k) + src[s].send_offsets[o]] >> i) & 1]
+                assert ow.recv_keys[lst].tolist() == [int(k) for k in expect]
+
+
+def test_microbatch_routing_resends():
+    """keys repeated across micro-batches are re-sent; sum_i |K(M_i)| >= |K(B)|."""
+    keys = np.array([5, 1, 5, 2], dtype=np.int64)
+    offs = np.array([0, 2, 4], dtype=np.int32)          # sample0 {5,1}, sample1 {5,2}
+    mb = R.mb_of_occurrence(offs, 1, np.array([0, 1]), np.array([0, 1, 2]))
+    rs = R.route_source(keys, 1, mb, 2)
+    assert rs.mb_counts[:, 0].tolist() == [2, 2]
+    assert rs.mb_counts.sum() >= len(rs.uniq)
+
+
+# ----------------------------------------------------------------------------- step
+def test_spec_pool_examples():
+    for c in GOLD["pool"]["cases"]:
+        rows = np.array(c["rows"], dtype=np.float32)
+        out = S.pool_sum(rows, np.array([0, len(rows)]))
+        assert out[0].tolist() == c["expect"]
+    # empty bag -> zero vector (reading Q5)
+    assert S.pool_sum(np.zeros((0, 3), np.float32), np.array([0, 0])).tolist() == [[0, 0, 0]]
+
+
+def test_spec_apply_sparse_grads_examples():
+    c0, c1 = GOLD["apply_sparse_grads"]["cases"]
+    out = S.sgd_rows(np.array([c0["e"]], np.float32), np.array([c0["sum"]]),
+                     np.float32(c0["eta"] / c0["B"]))
+    assert np.allclose(out[0], c0["expect"], rtol=1e-6)
+    g = np.sum(np.array(c1["contribs"], dtype=np.float64), axis=0)
+    out = S.sgd_rows(np.array([c1["e"]], np.float32), g[None], c1["eta"] / c1["B"])
+    assert out[0].tolist() == c1["expect"]
+
+
+def _brute_step(batches, douts, seed, d, mode, lr):
+    """Plain per-key loops over the global batch (tiny inputs only)."""
+    table = {}
+
+    def get(k):
+        if k not in table:
+            table[k] = prf.init_rows(seed, np.array([k]), d, mode)[0].astype(np.float64)
+        return table[k]
+    pooled_all, grads = [], {}
+    for (keys, offs), dout in zip(batches, douts):
+        pooled = []
+        for b in range(len(offs) - 1):
+            acc = np.zeros(d)
+            for j in range(offs[b], offs[b + 1]):
+                acc = acc + get(int(keys[j]))
+            pooled.append(acc.astype(np.float32))
+            for j in range(offs[b], offs[b + 1]):
+                k = int(keys[j])
+                grads[k] = grads.get(k, np.zeros(d)) + dout[b].astype(np.float64)
+        pooled_all.append(np.array(pooled))
+    s = float(np.float32(lr))
+    new = {k: (get(k) - s * g).astype(np.float32) for k, g in grads.items()}
+    return pooled_all, new
+
+
+@pytest.mark.parametrize("mode", ["dyadic", "uniform"])
+def test_sync_step_brute_force(mode):
+    cfg = WL.CONFIGS["tiny"]
+    batches = [WL.gen_batch(cfg, 11, 0, r, batch=8) for r in range(2)]
+    douts = [WL.gen_dout(11, 0, r, 8 * 4, 16, "dyadic" if mode == "dyadic" else "realistic")
+             for r in range(2)]
+    tab = S.LazyTable(4, 16, mode)
+    res = S.sync_step(tab, batches, douts, 2.0 ** -10)
+    pooled_bf, new_bf = _brute_step(batches, douts, 4, 16, mode, 2.0 ** -10)
+    for a, b in zip(res.pooled, pooled_bf):
+        if mode == "dyadic":
+            assert np.array_equal(a, b)
+        else:
+            assert np.allclose(a, b, rtol=1e-6, atol=1e-7)
+    for k, row in new_bf.items():
+        got = tab.get(np.array([k]))[0]
+        if mode == "dyadic":
+            assert np.array_equal(got, row)
+        else:
+            assert np.allclose(got, row, rtol=1e-6, atol=1e-7)
+
+
+def test_sync_step_closed_forms():
+    # dpooled == 1 => G[k] = number of occurrences (exact, order free)
+    cfg = WL.CONFIGS["tiny"]
+    batches = [WL.gen_batch(cfg, 3, 0, r, batch=16) for r in range(2)]
+    douts = [np.ones((16 * 4, 5), np.float32) for _ in range(2)]
+    g = S.key_grads(batches, douts)
+    allk = np.concatenate([b[0] for b in batches])
+    for k, row, c in zip(g.keys, g.grad, g.count):
+        n = int((allk == k).sum())
+        assert c == n and (row == n).all()
+    # constant rows c => pooled = bag length * c
+    rows = np.full((int(batches[0][1][-1]), 5), 0.25, np.float32)
+    pooled = S.pool_sum(rows, batches[0][1])
+    assert np.array_equal(pooled[:, 0], np.diff(batches[0][1]) * 0.25)
+
+
+def test_sync_step_only_touched_keys_change():
+    """Eq. 2 first case: e_k unchanged for k not in K(B_t)."""
+    cfg = WL.CONFIGS["tiny"]
+    tab = S.LazyTable(0, 16)
+    probe = np.array([(3 << 40) | 999, (0 << 40) | 998], dtype=np.int64)
+    before = tab.get(probe).copy()
+    batches = [WL.gen_batch(cfg, 0, 0, 0, batch=8)]
+    assert not np.isin(probe, batches[0][0]).any()
+    S.sync_step(tab, batches, [WL.gen_dout(0, 0, 0, 32, 16)], 0.5)
+    assert np.array_equal(tab.get(probe), before)
+
+
+# ----------------------------------------------------------------------------- cluster
+def test_spec_cluster_example():
+    g = GOLD["cluster_samples"]
+    ks = [np.array(k) for k in g["keysets"]]
+    for fn in (C.cluster_rounds, C.cluster_spec_greedy):
+        perm, mbo = fn(ks, g["N"])
+        groups = [sorted(perm[mbo[i]:mbo[i + 1]].tolist()) for i in range(g["N"])]
+        assert sorted(groups) == g["groups"]
+        assert C.partition_cost(ks, perm, mbo) == g["cost"]
+    assert C.brute_force_best(ks, 2) == g["cost"]
+    assert C.partition_cost(ks, np.array([0, 2, 1, 3]), np.array([0, 2, 4])) == g["random_pair_cost"]
+
+
+def test_cluster_n1_and_ties_and_validity():
+    ks = [np.array([1, 2])] * 6
+    for fn in (C.cluster_rounds, C.cluster_spec_greedy):
+        perm, mbo = fn(ks, 1)
+        assert perm.tolist() == list(range(6))
+        perm, mbo = fn(ks, 3)
+        # identical sets: deterministic, lowest-id tie break
+        assert np.array_equal(perm, fn(ks, 3)[0])
+        assert sorted(perm.tolist()) == list(range(6))
+    with pytest.raises(ValueError):
+        C.cluster_rounds(ks, 4)
+
+
+def test_admission_schedule():
+    g = C.admission_sizes(10 ** 9)
+    assert [next(g) for _ in range(7)] == [1, 1, 1, 2, 3, 3, 4]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_cluster_rounds_small_brute_force(seed):
+    rng = np.random.default_rng(seed)
+    ks = [np.unique(rng.integers(0, 8, size=rng.integers(1, 4))) for _ in range(6)]
+    perm, mbo = C.cluster_rounds(ks, 2)
+    assert sorted(perm.tolist()) == list(range(6))
+    assert all(mbo[i + 1] - mbo[i] == 3 for i in range(2))
+    cost = C.partition_cost(ks, perm, mbo)
+    best = C.brute_force_best(ks, 2)
+    seq = C.partition_cost(ks, *C.cluster_sequential(6, 2))
+    assert best <= cost
+
+
+def test_cluster_payload_dominance_correlated():
+    """S:586 / A6: mean clustered sum_i |K(M_i)| <= mean random."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(2000,) * 4)
+    tot_c = tot_r = 0
+    for seed in range(6):
+        keys, offs = WL.gen_correlated_batch(cfg, seed, 0, 0, groups=8, rho=0.8, batch=64)
+        ks = C.sample_keysets(keys, offs, 4)
+        tot_c += C.partition_cost(ks, *C.cluster_rounds(ks, 4))
+        rp = np.random.default_rng(seed).permutation(64)
+        tot_r += C.partition_cost(ks, rp, np.arange(5) * 16)
+    assert tot_c < tot_r
+
+
+# ----------------------------------------------------------------------------- pipeline
+def test_spec_dual_buffer_sync_example():
+    g = GOLD["dual_buffer_sync"]
+    mk = lambda d: P.Buffer(0, np.array(sorted(int(k) for k in d)),
+                            np.array([d[str(k)] for k in sorted(int(k) for k in d)], np.float32))
+    a, p = mk(g["active"]), mk(g["prefetch"])
+    P.dual_buffer_sync(a, p)
+    assert {int(k): r.tolist() for k, r in zip(p.keys, p.rows)} == \
+        {int(k): np.float32(v).tolist() for k, v in g["expect"].items()}
+    # disjoint -> unchanged; identical -> copy
+    q = mk({"9": [4.0]})
+    P.dual_buffer_sync(a, q)
+    assert q.rows.tolist() == [[4.0]]
+    r = mk({"5": [0.0], "7": [0.0]})
+    P.dual_buffer_sync(a, r)
+    assert np.array_equal(r.rows, a.rows)
+
+
+def _tiny_traj(W, T=6, seed=0, batch=8, dyadic=True):
+    cfg = WL.CONFIGS["tiny"]
+    batches = [[WL.gen_batch(cfg, seed, t, r, batch=batch) for r in range(W)] for t in range(T)]
+    douts = [[WL.gen_dout(seed, t, r, batch * 4, 16, "dyadic" if dyadic else "realistic")
+              for r in range(W)] for t in range(T)]
+    return batches, douts
+
+
+@pytest.mark.parametrize("W,N,cl,grad", [(1, 1, "sequential", "lin"), (2, 2, "clustered", "lin"),
+                                         (4, 4, "clustered", "quad"), (2, 4, "sequential", "quad"),
+                                         (3, 2, "clustered", "lin")])
+def test_corollary1_pipelined_equals_sync_bitwise(W, N, cl, grad):
+    """Corollary 1 in parity regime P1: DBP+FWP tables == Eq. 1."""
+    batches, douts = _tiny_traj(W)
+    lr = 2.0 ** -10
+    ref = P.sync_train(S.LazyTable(1, 16, "dyadic"), batches, douts, lr, grad_mode=grad)
+    tr = P.nestpipe_train(S.LazyTable(1, 16, "dyadic"), batches, douts,
+                          P.PipeConfig(W=W, N=N, cluster=cl, F=4, lr_over_B=lr, grad_mode=grad))
+    assert P.first_divergence(ref, [t.table for t in tr]) is None
+    # forward rows: pooled of every micro-batch equals the sync forward
+    tab = S.LazyTable(1, 16, "dyadic")
+    res = S.sync_step(tab, batches[0], douts[0], lr, grad_mode=grad)
+    for r in range(W):
+        for i in range(N):
+            perm, mbo = tr[0].perm[r], tr[0].mb_offsets[r]
+            bags = P._mb_bags(perm, mbo, i, 4)
+            assert np.array_equal(tr[0].pooled[r][i], res.pooled[r][bags])
+
+
+def test_negative_control_six_stage_diverges_at_step2():
+    """P:436-440 / S:473, S:732 (A3): skipping the dual-buffer sync gives a
+    one-step-stale read; divergence first appears at step 2 (1-based)."""
+    W = 2
+    cfg = WL.CONFIGS["tiny"]
+    hot = np.int64(7)
+    batches, douts = _tiny_traj(W)
+    # adversarial: one hot key in every batch of every rank
+    batches = [[(np.concatenate([[hot], k[1:]]), o) for (k, o) in st] for st in batches]
+    lr = 2.0 ** -6
+    ref = P.sync_train(S.LazyTable(1, 16, "dyadic"), batches, douts, lr, grad_mode="quad")
+    safe = P.nestpipe_train(S.LazyTable(1, 16, "dyadic"), batches, douts,
+                            P.PipeConfig(W=W, N=2, F=4, lr_over_B=lr, grad_mode="quad"))
+    bad = P.nestpipe_train(S.LazyTable(1, 16, "dyadic"), batches, douts,
+                           P.PipeConfig(W=W, N=2, F=4, lr_over_B=lr, grad_mode="quad",
+                                        unsafe_six_stage=True))
+    assert P.first_divergence(ref, [t.table for t in safe]) is None
+    assert P.first_divergence(ref, [t.table for t in bad], tol=1e-6) == 2
+    # tau = 1: the stale row the unsafe run used at step 2 is the oracle's step-0 init value
+    rows0 = S.LazyTable(1, 16, "dyadic").get(np.array([hot]))[0]
+    assert not np.array_equal(ref[0][int(hot)], rows0)
+
+
+def test_pipeline_depth_and_n_independence():
+    """S:496 depth independence + Prop. 2: N and clustering do not
+    change the tables (P1, bitwise)."""
+    batches, douts = _tiny_traj(2)
+    runs = []
+    for pipelined, N, cl in [(False, 1, "sequential"), (True, 1, "sequential"),
+                             (True, 2, "clustered"), (True, 4, "sequential")]:
+        tr = P.nestpipe_train(S.LazyTable(2, 16, "dyadic"), batches, douts,
+                              P.PipeConfig(W=2, N=N, cluster=cl, F=4, pipelined=pipelined))
+        runs.append([t.table for t in tr])
+    for r in runs[1:]:
+        assert P.first_divergence(runs[0], r) is None
+
+
+def test_realistic_regime_pipelined_close_to_sync():
+    batches, douts = _tiny_traj(2, dyadic=False)
+    ref = P.sync_train(S.LazyTable(1, 16), batches, douts, 0.05)
+    tr = P.nestpipe_train(S.LazyTable(1, 16), batches, douts,
+                          P.PipeConfig(W=2, N=2, cluster="clustered", F=4, lr_over_B=0.05))
+    assert P.first_divergence(ref, [t.table for t in tr], tol=1e-6) is None
+
+
+# ----------------------------------------------------------------------------- workload
+def test_workload_deterministic_and_skewed():
+    cfg = WL.CONFIGS["tiny"]
+    a = WL.gen_batch(cfg, 1, 2, 0)
+    b = WL.gen_batch(cfg, 1, 2, 0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    keys, offs = a
+    assert len(offs) == 32 * 4 + 1 and (np.diff(offs) >= 1).all() and (np.diff(offs) <= 3).all()
+    tab, row = WL.unpack_keys(keys)
+    F = 4
+    bag_tab = np.repeat(np.arange(32 * F) % F, np.diff(offs))
+    assert np.array_equal(tab, bag_tab) and (row < 1000).all()
+    # no repeats within a bag
+    for bg in range(32 * F):
+        seg = keys[offs[bg]:offs[bg + 1]]
+        assert len(np.unique(seg)) == len(seg)
+    r = WL.zipf_ranks(np.random.default_rng(0), 1.2, 10 ** 4, 10 ** 5)
+    cnt = np.bincount(r, minlength=10 ** 4)
+    assert cnt[0] > cnt[99] > 0
