@@ -1,0 +1,233 @@
+/*
+ * nest.h -- C ABI of libnest.so, the B200 (sm_100a) hot path of NestPipe
+ * (arXiv 2604.06956): the synchronous row-sharded embedding step, forward and
+ * backward, with Dual-Buffer Pipelining (DBP) and Frozen-Window Pipelining
+ * (FWP).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (the reference's
+ * documents), SURVEY = /root/repo/SURVEY.md section.  Every entry point states
+ * the passage that defines the operation it performs.
+ *
+ * Conventions (apply to every call unless stated otherwise)
+ * -----------------------------------------------------------------------
+ * Keys      int64 packed (table << 40) | row, row < table_rows[table]
+ *           (SURVEY Q2).  Owner of a key = row mod world, local row inside
+ *           the owner's shard of that table = row div world (Q1).
+ * Batches   CSR, sample-major: bag (b, f) = b*F + f holds the keys sample b
+ *           has for feature f; bag_offsets is int32[B*F+1].
+ * Shard     the rank's slice of every table, rows (table, local row)
+ *           concatenated table by table, fp32 [shard_rows, dim], in the
+ *           caller-owned `table_mem` (tables row-sharded, the HBM
+ *           shard plays the role of the host store written back to).
+ * Memory    every device byte is owned by the caller: query sizes with
+ *           nest_workspace_bytes, pass device pointers (e.g. torch tensors).
+ *           The library owns only NCCL communicators, CUDA events and small
+ *           pinned host mirrors.  Pointers are device pointers unless marked
+ *           "host".  Inputs are read-only.
+ * Streams   `void*` arguments named *stream / compute / comm are cudaStream_t
+ *           (NULL = the legacy default stream).  All calls are
+ *           stream-asynchronous except nest_route (one host sync for the
+ *           All2All sizes), nest_create and nest_destroy.
+ * Slots     two pipeline slots (0/1) hold the per-batch state: routing
+ *           results and one HBM buffer each; their roles (active/prefetch)
+ *           alternate every step.
+ * Errors    host-detectable errors return immediately and leave the context
+ *           unchanged.  Device-detected errors (key out of range, foreign key
+ *           at an owner) are raised at the next nest_route sync, become
+ *           sticky, and every later call returns that code (CUDA-style).
+ *           Calls never abort or throw.  nest_last_error gives a message.
+ *           Collective consistency: the count exchange carries every rank's
+ *           error flags and counts to every rank, so all ranks take the same
+ *           error decision at the same call.
+ */
+#ifndef NEST_H_
+#define NEST_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NEST_API __attribute__((visibility("default")))
+#else
+#define NEST_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NEST_OK = 0,
+  NEST_ERR_INVALID = 1,       /* bad argument / shape / config (SPEC exit 2) */
+  NEST_ERR_CUDA = 2,          /* a CUDA runtime call failed */
+  NEST_ERR_NCCL = 3,          /* an NCCL call failed */
+  NEST_ERR_CAPACITY = 4,      /* counts exceed a preallocated capacity */
+  NEST_ERR_KEY_RANGE = 5,     /* table >= num_tables or row >= table_rows */
+  NEST_ERR_SHARD = 6,         /* owner received a key it does not own */
+  NEST_ERR_ORDER = 7,         /* call out of order: e.g. lookup before route */
+  NEST_ERR_DIVISIBILITY = 8   /* B mod N != 0 */
+} nest_status_t;
+
+typedef struct nest_ctx nest_ctx_t;   /* opaque; one per rank */
+
+enum { NEST_POOL_SUM = 0, NEST_POOL_NONE = 1 };
+enum { NEST_INIT_UNIFORM = 0, NEST_INIT_DYADIC = 1, NEST_INIT_ZERO = 2 };
+enum { NEST_SCHED_SEQUENTIAL = 0, NEST_SCHED_CLUSTERED = 1 };
+enum { NEST_MAX_WORLD = 64, NEST_MAX_MICRO_BATCHES = 8, NEST_MAX_TABLES = 1024 };
+
+/* Static configuration of one rank.  Capacities bound every per-batch count;
+ * 0 selects the documented default. */
+typedef struct {
+  int32_t world;              /* W >= 1 ranks (one per GPU) */
+  int32_t rank;               /* 0 <= rank < W */
+  int32_t num_tables;         /* T <= NEST_MAX_TABLES */
+  int32_t dim;                /* d in {16, 32, 64, 128, 256} (fp32 rows) */
+  const int64_t* table_rows;  /* host [T]: rows of every table */
+  int32_t pooling;            /* NEST_POOL_SUM or NEST_POOL_NONE (expand) */
+  int32_t num_features;       /* F >= 1 bags per sample */
+  int64_t max_keys;           /* K cap: key occurrences per rank per batch (< 2^28) */
+  int64_t max_batch;          /* B cap: samples per rank per batch */
+  int32_t max_micro_batches;  /* N cap, 1..NEST_MAX_MICRO_BATCHES */
+  int64_t max_recv_keys;      /* R_o cap: keys an owner receives per batch (default 2*max_keys, clamped to shard rows*W) */
+  int64_t max_owner_keys;     /* U_o cap: owner-unique keys (default min(max_recv_keys, shard rows)) */
+  int64_t max_mb_rows;        /* cap of sum_i U_{s,i} (rows a source receives over all micro-batches; default max_keys) */
+  int64_t max_owner_mb_rows;  /* cap of sum_i R_{o,i} (rows an owner sends over all micro-batches; default max_recv_keys*N clamped) */
+  uint64_t seed;              /* PRF seed of the table initialisation */
+  int32_t init_mode;          /* NEST_INIT_UNIFORM (+-1/sqrt(d)), _DYADIC (parity regime P1), _ZERO */
+  int32_t tower_layers;       /* stand-in dense tower depth L (0 = no tower) */
+  int32_t tower_hidden;       /* tower width (bf16 GEMMs) */
+} nest_config_t;
+
+/* Host-known counts of one slot after nest_route (all per this rank). */
+typedef struct {
+  int32_t valid;              /* 1 after a successful nest_route on the slot */
+  int32_t num_micro_batches;  /* N of the routed batch */
+  int32_t batch;              /* B */
+  int64_t nnz;                /* K key occurrences */
+  int64_t uniq;               /* U_s source-unique keys (sum of send counts) */
+  int64_t recv;               /* R_o keys received as owner */
+  int64_t mb_uniq[NEST_MAX_MICRO_BATCHES];   /* U_{s,i}: rows received in mb i */
+  int64_t mb_recv[NEST_MAX_MICRO_BATCHES];   /* R_{o,i}: rows sent as owner in mb i */
+  int64_t mb_nnz[NEST_MAX_MICRO_BATCHES];    /* K_i occurrences in mb i */
+  int64_t mb_out_rows[NEST_MAX_MICRO_BATCHES]; /* rows of `out`/`dout` for mb i */
+} nest_slot_info_t;
+
+/* Device pointers into a slot's routing results (for parity checks). */
+typedef struct {
+  const int64_t* uniq;        /* [U_s] unique keys, (owner, key) ascending */
+  const int32_t* inverse;     /* [K] uniq[inverse[j]] == keys[j] */
+  const uint32_t* mask;       /* [U_s] bit i set iff the key occurs in micro-batch i */
+  const int32_t* pos;         /* [N][U_s+1] index of u among mask-bit-i keys */
+  const int32_t* send_counts; /* [W][N+2] per owner: {U, U_1..U_N, err} */
+  const int32_t* all_counts;  /* [W][W][N+2] every rank's send_counts (count exchange) */
+  const int64_t* recv_keys;   /* [R_o] received keys | mask << 56, sources concatenated */
+  const int32_t* owner_rows;  /* [U_o] shard row of every owner-unique key, ascending */
+  const int32_t* owner_inv;   /* [R_o] owner-unique index of every received key */
+  const int32_t* n_owner;     /* [1] U_o */
+  const float* buffer;        /* [U_o][d] the slot's HBM buffer (active or prefetch) */
+} nest_route_view_t;
+
+/* Library version string. */
+NEST_API const char* nest_version(void);
+
+/* Writes a 128-byte NCCL unique id into uid_out (host memory).  Call on rank 0
+ * twice (main + aux communicator) and broadcast the bytes to all ranks. */
+NEST_API nest_status_t nest_get_unique_id(void* uid_out);
+
+/* Bytes of table memory (the shard, fp32 [shard_rows, dim]) and of workspace
+ * this configuration needs.  Pure host computation. */
+NEST_API nest_status_t nest_workspace_bytes(const nest_config_t* cfg, size_t* table_bytes,
+                                   size_t* work_bytes);
+
+/* Number of shard rows this rank stores: sum_t |{row < rows_t : row mod W = rank}|. */
+NEST_API int64_t nest_shard_rows(const nest_config_t* cfg);
+
+/* Creates a context.  nccl_uids: host, 2 x 128 bytes (main and aux
+ * communicator) from nest_get_unique_id on rank 0, or NULL when world == 1.
+ * Collective over all ranks (ncclCommInitRank).  table_mem / work_mem: device
+ * buffers of at least the queried sizes, 256-byte aligned. */
+NEST_API nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids,
+                          void* table_mem, void* work_mem, void* stream,
+                          nest_ctx_t** out);
+NEST_API nest_status_t nest_destroy(nest_ctx_t* ctx);
+
+/* PRF initialisation of the whole shard: row of key k gets init_row(seed, k,
+ * d). */
+NEST_API nest_status_t nest_init_tables(nest_ctx_t* ctx, void* stream);
+
+/* FWP partition of the local batch into N equal micro-batches (
+ * S:544-552; SURVEY §8(c) clustering spec).  mode NEST_SCHED_SEQUENTIAL slices
+ * by sample id; NEST_SCHED_CLUSTERED runs the round-based key-centric greedy.
+ * Outputs: perm_out int32[B] (samples of micro-batch i are
+ * perm_out[mb_offsets_out[i] .. mb_offsets_out[i+1]), ascending id inside a
+ * micro-batch), mb_offsets_out int32[N+1].  B mod N != 0 -> NEST_ERR_DIVISIBILITY. */
+NEST_API nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys,
+                                const int32_t* bag_offsets, int32_t B, int32_t N,
+                                int32_t mode, int32_t* perm_out,
+                                int32_t* mb_offsets_out, void* stream);
+
+/* Key Routing + Embedding Retrieval of DBP for one
+ * batch into `slot`: source dedup and owner bucketing, exchange of counts (one
+ * host sync), key All2All, owner dedup, gather of the owned rows from the
+ * shard into the slot's HBM buffer.  keys/bag_offsets: the local batch (nnz
+ * occurrences, B samples).  perm/mb_offsets from nest_fwp_schedule (NULL =
+ * one micro-batch, N must be 1).  The gather is ordered after the previous
+ * update's write-back (events inside the library, reading Q8). */
+NEST_API nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys,
+                         const int32_t* bag_offsets, int64_t nnz, int32_t B,
+                         const int32_t* perm, const int32_t* mb_offsets, int32_t N,
+                         void* stream);
+
+/* Dual-buffer synchronization: for every key k in both
+ * the active slot's and the prefetch slot's owner key sets, copy the active
+ * (already updated) row over the prefetch row.  Waits inside for the active
+ * slot's update and the prefetch slot's gather. */
+NEST_API nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot,
+                               int32_t prefetch_slot, void* stream);
+
+/* Forward of micro-batch mb: owners gather the
+ * requested rows of the frozen buffer, All2All them back to the requesters
+ * (on `comm`), and the source pools them per bag (sum) or expands
+ * them per occurrence (pooling NONE) into out (on `compute`).
+ * out: fp32 [mb_out_rows, d]; pooled row p*F+f is bag (perm[mb_off+p], f). */
+NEST_API nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out,
+                              void* compute, void* comm);
+
+/* Backward of micro-batch mb: per unique
+ * key of the micro-batch, deterministic segment-sum of the gradients dout of
+ * the bags (pooled) or occurrences (unpooled) it occurs in, gradient All2All
+ * to the owners.  After the last micro-batch (mb == N-1) every owner sums its
+ * received gradients in (micro-batch, source) order and applies the
+ * sparse SGD update e <- e - lr_over_B * g (Eq. 2),
+ * writing the updated rows to the slot buffer and back to the shard
+ * (write-back).  dout: fp32 [mb_out_rows, d] in out's layout.
+ * lr_over_B = eta / |B_global|. */
+NEST_API nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb,
+                                   const float* dout, float lr_over_B,
+                                   void* compute, void* comm);
+
+/* Stand-in dense tower (the FWP overlap partner, not the product):
+ * fixed bf16 MLP forward + backward on `stream` via cuBLAS, input = the pooled
+ * rows of a micro-batch viewed as [rows/F, F*d]; writes its input gradient
+ * into dout (fp32, same layout).  Requires tower_layers > 0. */
+NEST_API nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t rows,
+                                 float* dout, void* stream);
+
+/* Host-known counts of a slot (valid after nest_route). */
+NEST_API nest_status_t nest_slot_info(const nest_ctx_t* ctx, int32_t slot, nest_slot_info_t* info);
+
+/* Device pointers to a slot's routing results (parity checks). */
+NEST_API nest_status_t nest_route_view(const nest_ctx_t* ctx, int32_t slot, nest_route_view_t* view);
+
+/* out[i] = shard row of keys[i] (device, n keys, all owned by this rank;
+ * foreign / out-of-range keys give a zero row and raise the sticky error). */
+NEST_API nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out,
+                             void* stream);
+
+/* Message of the last error of ctx (or of the last failed nest_create when ctx is NULL). */
+NEST_API const char* nest_last_error(const nest_ctx_t* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEST_H_ */

@@ -1,0 +1,208 @@
+"""NestPipe (arXiv 2604.06956) sharded-embedding hot path on B200.
+
+Thin Python binding over libnest.so (include/nest.h): every step of the path
+runs in the library's sm_100a kernels and NCCL calls; this module only
+allocates device memory with torch, marshals pointers and streams, and raises
+on error.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+from . import _lib as L
+from ._lib import NestError  # noqa: F401
+
+__all__ = ["NestContext", "NestError", "unique_ids"]
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(s) -> Optional[int]:
+    if s is None:
+        import torch
+        s = torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def unique_ids() -> bytes:
+    """Two NCCL unique ids (main + aux communicator), 256 bytes; call on rank 0."""
+    lib = L.load()
+    buf = C.create_string_buffer(256)
+    L.check(lib.nest_get_unique_id(C.byref(buf, 0)))
+    L.check(lib.nest_get_unique_id(C.byref(buf, 128)))
+    return buf.raw
+
+
+class NestContext:
+    """One rank's context: shard + workspace (torch-allocated) + libnest ctx."""
+
+    def __init__(self, table_rows: Sequence[int], dim: int, *, world: int = 1, rank: int = 0,
+                 pooling: str = "sum", num_features: Optional[int] = None, max_keys: int,
+                 max_batch: int, max_micro_batches: int = 1, max_recv_keys: int = 0,
+                 max_mb_rows: int = 0, max_owner_mb_rows: int = 0, seed: int = 0,
+                 init_mode: str = "uniform", tower_layers: int = 0, tower_hidden: int = 1024,
+                 nccl_uids: Optional[bytes] = None, device=None, init_tables: bool = True):
+        import torch
+        self.lib = L.load()
+        self.torch = torch
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._rows = (C.c_int64 * len(table_rows))(*[int(r) for r in table_rows])
+        self.cfg = L.Config(
+            world=world, rank=rank, num_tables=len(table_rows), dim=dim, table_rows=self._rows,
+            pooling={"sum": L.POOL_SUM, "none": L.POOL_NONE}[pooling],
+            num_features=num_features if num_features is not None else len(table_rows),
+            max_keys=max_keys, max_batch=max_batch, max_micro_batches=max_micro_batches,
+            max_recv_keys=max_recv_keys, max_owner_keys=0, max_mb_rows=max_mb_rows,
+            max_owner_mb_rows=max_owner_mb_rows, seed=seed,
+            init_mode={"uniform": L.INIT_UNIFORM, "dyadic": L.INIT_DYADIC, "zero": L.INIT_ZERO}[init_mode],
+            tower_layers=tower_layers, tower_hidden=tower_hidden)
+        self.world, self.rank, self.dim = world, rank, dim
+        self.F = self.cfg.num_features
+        tb, wb = C.c_size_t(), C.c_size_t()
+        L.check(self.lib.nest_workspace_bytes(C.byref(self.cfg), C.byref(tb), C.byref(wb)))
+        self.table_bytes, self.work_bytes = tb.value, wb.value
+        self.shard_rows = self.lib.nest_shard_rows(C.byref(self.cfg))
+        with torch.cuda.device(self.device):
+            self.table_mem = torch.empty(self.table_bytes, dtype=torch.uint8, device=self.device)
+            self.work_mem = torch.empty(self.work_bytes, dtype=torch.uint8, device=self.device)
+            self.shard = self.table_mem.view(torch.float32)[: self.shard_rows * dim].view(self.shard_rows, dim)
+            ctx = C.c_void_p()
+            uid = None
+            if world > 1:
+                if nccl_uids is None or len(nccl_uids) != 256:
+                    raise ValueError("world > 1 needs the 256-byte nccl_uids from rank 0")
+                uid = C.create_string_buffer(nccl_uids, 256)
+            st = torch.cuda.current_stream(self.device)
+            L.check(self.lib.nest_create(C.byref(self.cfg), uid, _ptr(self.table_mem), _ptr(self.work_mem),
+                                         st.cuda_stream, C.byref(ctx)))
+            self.ctx = ctx
+            if init_tables:
+                self.init_tables(st)
+
+    # -- lifecycle -----------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "ctx", None):
+            self.lib.nest_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, code: int) -> None:
+        L.check(code, self.ctx)
+
+    # -- calls (1:1 with include/nest.h) -------------------------------------
+    def init_tables(self, stream=None) -> None:
+        self._check(self.lib.nest_init_tables(self.ctx, _stream(stream)))
+
+    def fwp_schedule(self, keys, bag_offsets, B: int, N: int, mode: str = "sequential", stream=None):
+        torch = self.torch
+        perm = torch.empty(B, dtype=torch.int32, device=self.device)
+        mbo = torch.empty(N + 1, dtype=torch.int32, device=self.device)
+        m = {"sequential": L.SCHED_SEQUENTIAL, "clustered": L.SCHED_CLUSTERED}[mode]
+        self._check(self.lib.nest_fwp_schedule(self.ctx, _ptr(keys), _ptr(bag_offsets), B, N, m,
+                                               _ptr(perm), _ptr(mbo), _stream(stream)))
+        return perm, mbo
+
+    def route(self, slot: int, keys, bag_offsets, B: int, perm=None, mb_offsets=None, N: int = 1,
+              stream=None) -> None:
+        self._check(self.lib.nest_route(self.ctx, slot, _ptr(keys), _ptr(bag_offsets), int(keys.numel()),
+                                        B, _ptr(perm), _ptr(mb_offsets), N, _stream(stream)))
+
+    def dbp_refresh(self, active: int, prefetch: int, stream=None) -> None:
+        self._check(self.lib.nest_dbp_refresh(self.ctx, active, prefetch, _stream(stream)))
+
+    def lookup_fwd(self, slot: int, mb: int, out, compute=None, comm=None) -> None:
+        self._check(self.lib.nest_lookup_fwd(self.ctx, slot, mb, _ptr(out), _stream(compute),
+                                             _stream(comm if comm is not None else compute)))
+
+    def grad_bwd_update(self, slot: int, mb: int, dout, lr_over_B: float, compute=None, comm=None) -> None:
+        self._check(self.lib.nest_grad_bwd_update(self.ctx, slot, mb, _ptr(dout), float(lr_over_B),
+                                                  _stream(compute),
+                                                  _stream(comm if comm is not None else compute)))
+
+    def tower_fwd_bwd(self, pooled, dout, stream=None) -> None:
+        self._check(self.lib.nest_tower_fwd_bwd(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout),
+                                                _stream(stream)))
+
+    def slot_info(self, slot: int) -> L.SlotInfo:
+        info = L.SlotInfo()
+        self._check(self.lib.nest_slot_info(self.ctx, slot, C.byref(info)))
+        return info
+
+    def out_rows(self, slot: int, mb: int) -> int:
+        return int(self.slot_info(slot).mb_out_rows[mb])
+
+    def read_rows(self, keys, stream=None):
+        torch = self.torch
+        out = torch.empty((int(keys.numel()), self.dim), dtype=torch.float32, device=self.device)
+        self._check(self.lib.nest_read_rows(self.ctx, _ptr(keys), int(keys.numel()), _ptr(out),
+                                            _stream(stream)))
+        return out
+
+    def route_view(self, slot: int) -> dict:
+        """Copies of a slot's routing results (host numpy) for parity checks."""
+        torch = self.torch
+        import numpy as np
+        v = L.RouteView()
+        self._check(self.lib.nest_route_view(self.ctx, slot, C.byref(v)))
+        info = self.slot_info(slot)
+        torch.cuda.synchronize(self.device)
+        N, W = info.num_micro_batches, self.world
+        Nc = self.cfg.max_micro_batches + 2
+        K = int(self.cfg.max_keys)
+
+        def fetch(addr, n, dtype):
+            n = int(n)
+            if n == 0 or not addr:
+                return np.zeros(0, dtype=dtype)
+            out = np.empty(n, dtype=dtype)
+            _memcpy_d2h(out.ctypes.data, addr, out.nbytes)
+            return out
+
+        U = int(info.uniq)
+        n_owner = int(fetch(v.n_owner, 1, np.int32)[0])
+        out = {
+            "uniq": fetch(v.uniq, U, np.int64),
+            "inverse": fetch(v.inverse, info.nnz, np.int32),
+            "mask": fetch(v.mask, U, np.uint32),
+            "pos": np.stack([fetch(v.pos + 4 * i * (K + 1), U, np.int32) for i in range(N)]) if N else None,
+            "send_counts": fetch(v.send_counts, W * Nc, np.int32).reshape(W, Nc),
+            "all_counts": fetch(v.all_counts, W * W * Nc, np.int32).reshape(W, W, Nc),
+            "owner_rows": fetch(v.owner_rows, n_owner, np.int32),
+            "n_owner": n_owner,
+            "buffer": fetch(v.buffer, n_owner * self.dim, np.float32).reshape(n_owner, self.dim),
+            "info": info,
+        }
+        if W > 1:
+            out["recv_keys"] = fetch(v.recv_keys, info.recv, np.int64)
+            out["owner_inv"] = fetch(v.owner_inv, info.recv, np.int32)
+        return out
+
+
+_cudart = None
+
+
+def _memcpy_d2h(dst: int, src: int, nbytes: int) -> None:
+    """Synchronous device->host copy through the CUDA runtime torch loaded."""
+    global _cudart
+    if _cudart is None:
+        import os
+        import torch  # noqa: F401  (loads libcudart.so.12 into the process)
+        try:
+            _cudart = C.CDLL("libcudart.so.12")
+        except OSError:
+            import nvidia.cuda_runtime as cr
+            _cudart = C.CDLL(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so.12"))
+        _cudart.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+        _cudart.cudaMemcpy.restype = C.c_int
+    rc = _cudart.cudaMemcpy(dst, src, nbytes, 2)  # cudaMemcpyDeviceToHost
+    if rc != 0:
+        raise NestError(2, f"cudaMemcpy failed ({rc})")

@@ -1,0 +1,502 @@
+// C ABI entry points of libnest.so (include/nest.h) and the per-rank runtime:
+// configuration checks, workspace carving, NCCL communicators, pipeline-slot
+// events, and the stream/event choreography of DBP + FWP (P:363-380,
+// P:457-467).
+#include <cmath>
+#include <cstring>
+#include <exception>
+
+#include "nest_internal.cuh"
+
+namespace nest {
+
+static thread_local std::string g_create_error;
+
+// ---------------------------------------------------------------------------
+// configuration
+// ---------------------------------------------------------------------------
+static void derive(Ctx& c, const nest_config_t* cfg) {
+  NEST_CHECK(cfg != nullptr, NEST_ERR_INVALID, "null config");
+  c.cfg = *cfg;
+  c.W = cfg->world;
+  c.rank = cfg->rank;
+  c.T = cfg->num_tables;
+  c.D = cfg->dim;
+  c.F = cfg->num_features;
+  c.Nmax = cfg->max_micro_batches;
+  NEST_CHECK(c.W >= 1 && c.W <= NEST_MAX_WORLD, NEST_ERR_INVALID, "world out of range");
+  NEST_CHECK(c.rank >= 0 && c.rank < c.W, NEST_ERR_INVALID, "rank out of range");
+  NEST_CHECK(c.T >= 1 && c.T <= NEST_MAX_TABLES, NEST_ERR_INVALID, "num_tables out of range");
+  NEST_CHECK(c.D == 16 || c.D == 32 || c.D == 64 || c.D == 128 || c.D == 256, NEST_ERR_INVALID,
+             "dim must be one of 16, 32, 64, 128, 256");
+  NEST_CHECK(cfg->table_rows != nullptr, NEST_ERR_INVALID, "table_rows is null");
+  NEST_CHECK(cfg->pooling == NEST_POOL_SUM || cfg->pooling == NEST_POOL_NONE, NEST_ERR_INVALID,
+             "bad pooling");
+  NEST_CHECK(c.F >= 1, NEST_ERR_INVALID, "num_features < 1");
+  NEST_CHECK(cfg->max_keys >= 1 && cfg->max_keys < (int64_t(1) << kMbShift), NEST_ERR_INVALID,
+             "max_keys must be in [1, 2^28)");
+  NEST_CHECK(cfg->max_batch >= 1 && cfg->max_batch * c.F < (int64_t(1) << 31), NEST_ERR_INVALID,
+             "max_batch out of range");
+  NEST_CHECK(c.Nmax >= 1 && c.Nmax <= NEST_MAX_MICRO_BATCHES, NEST_ERR_INVALID,
+             "max_micro_batches must be in [1, 8]");
+  NEST_CHECK(cfg->init_mode >= 0 && cfg->init_mode <= 2, NEST_ERR_INVALID, "bad init_mode");
+  c.rows.assign(cfg->table_rows, cfg->table_rows + c.T);
+  for (int t = 0; t < c.T; ++t)
+    NEST_CHECK(c.rows[t] >= 1 && c.rows[t] <= int64_t(kRowMask), NEST_ERR_INVALID, "bad table_rows");
+  // owner-major domain: segment (o, t) holds the rows of table t owned by o
+  c.seg_base.assign(size_t(c.W) * c.T + 1, 0);
+  int64_t acc = 0;
+  for (int o = 0; o < c.W; ++o)
+    for (int t = 0; t < c.T; ++t) {
+      c.seg_base[size_t(o) * c.T + t] = acc;
+      acc += c.rows[t] > o ? (c.rows[t] - o + c.W - 1) / c.W : 0;
+    }
+  c.seg_base[size_t(c.W) * c.T] = acc;
+  c.V = acc;
+  NEST_CHECK(c.V < (int64_t(1) << 31) - 64, NEST_ERR_INVALID, "total rows must be < 2^31");
+  c.lbase.assign(c.T + 1, 0);
+  const int64_t r0 = c.seg_base[size_t(c.rank) * c.T];
+  for (int t = 0; t <= c.T; ++t) c.lbase[t] = c.seg_base[size_t(c.rank) * c.T + t] - r0;
+  c.Vo = c.lbase[c.T];
+  c.words = (c.V + 31) / 32;
+  c.owords = (c.Vo + 31) / 32;
+  c.Kcap = cfg->max_keys;
+  c.Bcap = cfg->max_batch;
+  if (c.W == 1) {
+    c.Rcap = c.Kcap;
+  } else {
+    c.Rcap = cfg->max_recv_keys > 0 ? cfg->max_recv_keys : std::min<int64_t>(2 * c.Kcap, c.W * c.Kcap);
+  }
+  NEST_CHECK(c.Rcap < (int64_t(1) << 31) - 64, NEST_ERR_INVALID, "max_recv_keys too large");
+  c.Uocap = std::max<int64_t>(1, std::min<int64_t>(c.Rcap, c.Vo));
+  c.MBcap = cfg->max_mb_rows > 0 ? cfg->max_mb_rows : c.Kcap;
+  if (c.W == 1)
+    c.OMBcap = c.MBcap;
+  else
+    c.OMBcap = cfg->max_owner_mb_rows > 0 ? cfg->max_owner_mb_rows
+                                          : (c.Nmax > 1 ? 2 * c.Rcap : c.Rcap);
+  c.Pcap = 2 * c.Kcap / 32 + 64;
+}
+
+size_t tower_workspace_bytes(const Ctx& c);
+void tower_bind(Ctx& c, char* mem);
+
+static size_t layout(Ctx& c, char* base) {
+  Carver w{base};
+  const int64_t K = c.Kcap, B = c.Bcap, R = c.Rcap, Uo = c.Uocap, D = c.D, W = c.W, Nm = c.Nmax;
+  const int Nc = c.Nmax + 2;
+  int64_t maxn = std::max<int64_t>({c.words + 2, c.owords + 2, K + 2, R + 2, B + 2,
+                                    int64_t(256) * radix_blocks(K) + 2});
+  const int64_t scan_bytes = (scan_blocks(maxn) + 4) * int64_t(sizeof(I2));
+  c.d_rows = w.take<int64_t>(c.T);
+  c.d_seg_base = w.take<int64_t>(W * c.T + 1);
+  c.d_lbase = w.take<int64_t>(c.T + 1);
+  c.sbm = w.take<uint32_t>(c.words + 2);
+  c.swr = w.take<int32_t>(c.words + 2);
+  c.occ_dom = w.take<uint32_t>(K);
+  c.occ_mbrow = w.take<int32_t>(K);
+  for (int i = 0; i < 2; ++i) {
+    c.tkey[i] = w.take<uint32_t>(K);
+    c.tval[i] = w.take<int32_t>(K);
+  }
+  c.hist = w.take<uint32_t>(int64_t(256) * radix_blocks(K) + 2);
+  c.scan_tmp = w.take<char>(scan_bytes);
+  c.scan_tmp_win = w.take<char>(scan_bytes);
+  c.samp_scratch = w.take<int32_t>(B + 2);
+  c.packed = w.take<int64_t>(W > 1 ? K : 1);
+  c.r_ldom = w.take<uint32_t>(W > 1 ? R : 1);
+  c.seg_start = w.take<int32_t>(K + 2);
+  c.seg_aux = w.take<int32_t>(K + 2);
+  c.hot_list = w.take<int32_t>(K + 1);
+  c.seg_tot = w.take<int32_t>(4);
+  c.partial = w.take<float>(c.Pcap * D);
+  c.src_rows = w.take<float>(c.MBcap * D);
+  c.own_rows = W > 1 ? w.take<float>(c.OMBcap * D) : c.src_rows;
+  c.d_err = w.take<int32_t>(4);
+  c.d_cnt_scratch = w.take<int32_t>(W * Nm + 1);
+  c.n_refreshed = w.take<int32_t>(4);
+  for (int si = 0; si < 2; ++si) {
+    Slot& s = c.slot[si];
+    s.uniq = w.take<int64_t>(K);
+    s.inverse = w.take<int32_t>(K);
+    s.mask = w.take<uint32_t>(K);
+    s.pos = w.take<int32_t>(Nm * (K + 1));
+    s.skey = w.take<uint32_t>(K);
+    s.sval = w.take<int32_t>(K);
+    s.perm = w.take<int32_t>(B);
+    s.bag_off = w.take<int32_t>(B * c.F + 1);
+    s.samp_base = w.take<int32_t>(B);
+    s.mb_of = w.take<int32_t>(B);
+    s.off = w.take<int32_t>(W + 1);
+    s.xfer = w.take<int32_t>(W * W * Nc + Nm + 1);
+    const int64_t ow = W > 1 ? c.owords : c.words;
+    s.obm = w.take<uint32_t>(ow + 2);
+    s.owr = w.take<int32_t>(ow + 2);
+    s.owner_rows = w.take<int32_t>(Uo);
+    s.n_owner = w.take<int32_t>(1);
+    if (W > 1) {
+      s.recv = w.take<int64_t>(R);
+      s.owner_inv = w.take<int32_t>(R);
+      s.src_tab = w.take<int32_t>(Uo * W);
+      s.sendpos = w.take<int32_t>(Nm * (R + 1));
+    }
+    s.buffer = w.take<float>(Uo * D);
+  }
+  const size_t tw = tower_workspace_bytes(c);
+  char* tmem = w.take<char>(int64_t(tw));
+  if (base) tower_bind(c, tw ? tmem : nullptr);
+  return w.off + 256;
+}
+
+// ---------------------------------------------------------------------------
+// guard: exceptions -> status codes, sticky device/comm errors
+// ---------------------------------------------------------------------------
+template <class Fn>
+static nest_status_t guard(Ctx* c, Fn&& fn) {
+  if (c && c->sticky != NEST_OK) return c->sticky;
+  try {
+    fn();
+    return NEST_OK;
+  } catch (const Error& e) {
+    if (c) {
+      c->last_error = e.msg;
+      if (e.code == NEST_ERR_CUDA || e.code == NEST_ERR_NCCL || e.code == NEST_ERR_KEY_RANGE ||
+          e.code == NEST_ERR_SHARD)
+        c->sticky = e.code;
+    } else {
+      g_create_error = e.msg;
+    }
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what(); else g_create_error = e.what();
+    return NEST_ERR_INVALID;
+  }
+}
+
+static cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+static Slot& slot_of(Ctx& c, int32_t slot) {
+  NEST_CHECK(slot == 0 || slot == 1, NEST_ERR_INVALID, "slot must be 0 or 1");
+  return c.slot[slot];
+}
+
+// grouped send/recv All2Allv of fp32 rows
+static void a2a_rows(Ctx& c, const float* send, const std::vector<int64_t>& scnt, float* recv,
+                     const std::vector<int64_t>& rcnt, cudaStream_t st) {
+  const int W = c.W;
+  int64_t so = 0, ro = 0;
+  NEST_NCCL(ncclGroupStart());
+  for (int p = 0; p < W; ++p) {
+    NEST_NCCL(ncclSend(send + so * c.D, size_t(scnt[p] * c.D), ncclFloat32, p, c.comm, st));
+    NEST_NCCL(ncclRecv(recv + ro * c.D, size_t(rcnt[p] * c.D), ncclFloat32, p, c.comm, st));
+    so += scnt[p];
+    ro += rcnt[p];
+  }
+  NEST_NCCL(ncclGroupEnd());
+}
+
+}  // namespace nest
+
+using namespace nest;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* nest_version(void) { return "nestpipe-b200 0.1 (sm_100a)"; }
+
+nest_status_t nest_get_unique_id(void* uid_out) {
+  if (!uid_out) return NEST_ERR_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return NEST_ERR_NCCL;
+  std::memcpy(uid_out, &id, sizeof(id));
+  return NEST_OK;
+}
+
+nest_status_t nest_workspace_bytes(const nest_config_t* cfg, size_t* table_bytes, size_t* work_bytes) {
+  return guard(nullptr, [&] {
+    NEST_CHECK(table_bytes && work_bytes, NEST_ERR_INVALID, "null output");
+    Ctx c;
+    derive(c, cfg);
+    *table_bytes = size_t(std::max<int64_t>(c.Vo, 1)) * c.D * sizeof(float);
+    *work_bytes = layout(c, nullptr);
+  });
+}
+
+int64_t nest_shard_rows(const nest_config_t* cfg) {
+  Ctx c;
+  try {
+    derive(c, cfg);
+  } catch (...) {
+    return -1;
+  }
+  return c.Vo;
+}
+
+nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void* table_mem,
+                          void* work_mem, void* stream, nest_ctx_t** out) {
+  if (!out) return NEST_ERR_INVALID;
+  *out = nullptr;
+  Ctx* c = new Ctx();
+  nest_status_t st = guard(nullptr, [&] {
+    derive(*c, cfg);
+    NEST_CHECK(table_mem && work_mem, NEST_ERR_INVALID, "null table_mem / work_mem");
+    NEST_CHECK((reinterpret_cast<uintptr_t>(table_mem) & 255) == 0 &&
+                   (reinterpret_cast<uintptr_t>(work_mem) & 255) == 0,
+               NEST_ERR_INVALID, "memory must be 256-byte aligned");
+    c->shard = reinterpret_cast<float*>(table_mem);
+    layout(*c, reinterpret_cast<char*>(work_mem));
+    cudaStream_t st0 = S(stream);
+    NEST_CUDA(cudaMemcpyAsync(c->d_rows, c->rows.data(), sizeof(int64_t) * c->T, cudaMemcpyHostToDevice, st0));
+    NEST_CUDA(cudaMemcpyAsync(c->d_seg_base, c->seg_base.data(), sizeof(int64_t) * c->seg_base.size(),
+                              cudaMemcpyHostToDevice, st0));
+    NEST_CUDA(cudaMemcpyAsync(c->d_lbase, c->lbase.data(), sizeof(int64_t) * c->lbase.size(),
+                              cudaMemcpyHostToDevice, st0));
+    NEST_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int32_t) * 4, st0));
+    const int Nc = c->Nmax + 2;
+    for (int si = 0; si < 2; ++si) {
+      Slot& s = c->slot[si];
+      NEST_CUDA(cudaMallocHost(&s.h_xfer, sizeof(int32_t) * (int64_t(c->W) * c->W * Nc + c->Nmax + 1)));
+      NEST_CUDA(cudaMemsetAsync(s.n_owner, 0, sizeof(int32_t), st0));
+      NEST_CUDA(cudaMemsetAsync(s.off, 0, sizeof(int32_t) * (c->W + 1), st0));
+      cudaEvent_t* evs[] = {&s.ev_gather, &s.ev_update, &s.ev_free, &s.ev_ready, &s.ev_sync};
+      for (auto* e : evs) NEST_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      for (int i = 0; i < NEST_MAX_MICRO_BATCHES; ++i) {
+        NEST_CUDA(cudaEventCreateWithFlags(&s.ev_emb[i], cudaEventDisableTiming));
+        NEST_CUDA(cudaEventCreateWithFlags(&s.ev_grad[i], cudaEventDisableTiming));
+      }
+    }
+    NEST_CUDA(cudaStreamSynchronize(st0));
+    if (c->W > 1) {
+      NEST_CHECK(nccl_uids != nullptr, NEST_ERR_INVALID, "world > 1 needs NCCL unique ids");
+      ncclUniqueId id0, id1;
+      std::memcpy(&id0, nccl_uids, sizeof(id0));
+      std::memcpy(&id1, reinterpret_cast<const char*>(nccl_uids) + sizeof(id0), sizeof(id1));
+      NEST_NCCL(ncclCommInitRank(&c->comm, c->W, id0, c->rank));
+      NEST_NCCL(ncclCommInitRank(&c->comm_aux, c->W, id1, c->rank));
+    }
+    if (c->cfg.tower_layers > 0) tower_create(*c);
+  });
+  if (st != NEST_OK) {
+    delete c;
+    return st;
+  }
+  *out = reinterpret_cast<nest_ctx_t*>(c);
+  return NEST_OK;
+}
+
+nest_status_t nest_destroy(nest_ctx_t* ctx) {
+  if (!ctx) return NEST_OK;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  cudaDeviceSynchronize();
+  if (c->tower) tower_destroy(*c);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm_aux) ncclCommDestroy(c->comm_aux);
+  for (auto& s : c->slot) {
+    if (s.h_xfer) cudaFreeHost(s.h_xfer);
+    cudaEvent_t evs[] = {s.ev_gather, s.ev_update, s.ev_free, s.ev_ready, s.ev_sync};
+    for (auto e : evs)
+      if (e) cudaEventDestroy(e);
+    for (int i = 0; i < NEST_MAX_MICRO_BATCHES; ++i) {
+      if (s.ev_emb[i]) cudaEventDestroy(s.ev_emb[i]);
+      if (s.ev_grad[i]) cudaEventDestroy(s.ev_grad[i]);
+    }
+  }
+  delete c;
+  return NEST_OK;
+}
+
+nest_status_t nest_init_tables(nest_ctx_t* ctx, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { launch_init_tables(*c, S(stream)); });
+}
+
+nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int32_t* bag_offsets,
+                                int32_t B, int32_t N, int32_t mode, int32_t* perm_out,
+                                int32_t* mb_offsets_out, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CHECK(N >= 1 && N <= c->Nmax, NEST_ERR_INVALID, "N out of range");
+    NEST_CHECK(B >= 0 && B <= c->Bcap, NEST_ERR_INVALID, "B out of range");
+    NEST_CHECK(B % N == 0, NEST_ERR_DIVISIBILITY, "B mod N != 0");
+    NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || mode == NEST_SCHED_CLUSTERED, NEST_ERR_INVALID, "bad mode");
+    NEST_CHECK(perm_out && mb_offsets_out, NEST_ERR_INVALID, "null output");
+    NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || (keys && bag_offsets), NEST_ERR_INVALID, "null batch");
+    launch_schedule(*c, keys, bag_offsets, B, N, mode, perm_out, mb_offsets_out, S(stream));
+  });
+}
+
+nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, const int32_t* bag_offsets,
+                         int64_t nnz, int32_t B, const int32_t* perm, const int32_t* mb_offsets,
+                         int32_t N, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    Slot& s = slot_of(*c, slot);
+    NEST_CHECK(N >= 1 && N <= c->Nmax, NEST_ERR_INVALID, "N out of range");
+    NEST_CHECK(B >= 1 && B <= c->Bcap, NEST_ERR_INVALID, "B out of range");
+    NEST_CHECK(nnz >= 0 && nnz <= c->Kcap, NEST_ERR_CAPACITY, "nnz exceeds max_keys");
+    NEST_CHECK(B % N == 0, NEST_ERR_DIVISIBILITY, "B mod N != 0");
+    NEST_CHECK(perm != nullptr || N == 1, NEST_ERR_INVALID, "N > 1 needs perm from nest_fwp_schedule");
+    NEST_CHECK(bag_offsets != nullptr && (keys != nullptr || nnz == 0), NEST_ERR_INVALID, "null batch");
+    (void)mb_offsets;  // micro-batches are equal: mb_offsets[i] = i * B / N
+    cudaStream_t st = S(stream);
+    s.routed = false;
+    // the slot's previous batch must be fully consumed (window + refresh), and
+    // its write-back done before this gather reads the shard (reading Q8)
+    NEST_CUDA(cudaStreamWaitEvent(st, s.ev_update, 0));
+    NEST_CUDA(cudaStreamWaitEvent(st, s.ev_free, 0));
+    route_phase_a(*c, s, keys, bag_offsets, nnz, B, perm, N, st);
+    NEST_CUDA(cudaEventSynchronize(s.ev_sync));  // the one host sync (All2All sizes)
+    route_phase_b(*c, s, st);
+    NEST_CUDA(cudaEventRecord(s.ev_gather, st));
+    s.routed = true;
+    s.updated = false;
+  });
+}
+
+nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t prefetch_slot, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CHECK(active_slot != prefetch_slot, NEST_ERR_INVALID, "slots must differ");
+    Slot& a = slot_of(*c, active_slot);
+    Slot& p = slot_of(*c, prefetch_slot);
+    NEST_CHECK(a.routed && p.routed, NEST_ERR_ORDER, "refresh needs both slots routed");
+    NEST_CHECK(a.updated, NEST_ERR_ORDER, "refresh before the active slot's update (S:276)");
+    cudaStream_t st = S(stream);
+    NEST_CUDA(cudaStreamWaitEvent(st, a.ev_update, 0));
+    NEST_CUDA(cudaStreamWaitEvent(st, p.ev_gather, 0));
+    launch_refresh(*c, a, p, st);
+    NEST_CUDA(cudaEventRecord(a.ev_free, st));
+  });
+}
+
+nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out, void* compute,
+                              void* comm) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    Slot& s = slot_of(*c, slot);
+    NEST_CHECK(s.routed, NEST_ERR_ORDER, "lookup before route");
+    NEST_CHECK(!s.updated, NEST_ERR_ORDER, "lookup after the window closed (S:568)");
+    NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
+    NEST_CHECK(out != nullptr, NEST_ERR_INVALID, "null out");
+    cudaStream_t cs = S(compute), ms = S(comm);
+    if (c->W > 1) {
+      if (mb == 0) {
+        // the window starts after everything queued on compute (refresh) and
+        // the slot's gather; later micro-batches only follow the comm chain
+        NEST_CUDA(cudaEventRecord(s.ev_ready, cs));
+        NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_ready, 0));
+        NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_gather, 0));
+      }
+      launch_send_gather(*c, s, mb, ms);
+      std::vector<int64_t> scnt(c->W), rcnt(c->W);
+      const int Nc = c->Nmax + 2;
+      for (int p = 0; p < c->W; ++p) {
+        scnt[p] = s.all[(size_t(p) * c->W + c->rank) * Nc + 1 + mb];  // owner -> requester p
+        rcnt[p] = s.all[(size_t(c->rank) * c->W + p) * Nc + 1 + mb];  // from owner p
+      }
+      a2a_rows(*c, c->own_rows + s.own_base[mb] * c->D, scnt, c->src_rows + s.src_base[mb] * c->D, rcnt, ms);
+      NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
+      NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_emb[mb], 0));
+    } else if (mb == 0) {
+      NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));
+    }
+    launch_pool(*c, s, mb, out, cs);
+  });
+}
+
+nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, const float* dout,
+                                   float lr_over_B, void* compute, void* comm) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    Slot& s = slot_of(*c, slot);
+    NEST_CHECK(s.routed && !s.updated, NEST_ERR_ORDER, "backward outside the window");
+    NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
+    NEST_CHECK(dout != nullptr || s.info.mb_out_rows[mb] == 0, NEST_ERR_INVALID, "null dout");
+    cudaStream_t cs = S(compute), ms = S(comm);
+    Slot& other = c->slot[1 - slot];
+    launch_segsum(*c, s, mb, dout, cs);
+    if (c->W > 1) {
+      NEST_CUDA(cudaEventRecord(s.ev_grad[mb], cs));
+      NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_grad[mb], 0));
+      std::vector<int64_t> scnt(c->W), rcnt(c->W);
+      const int Nc = c->Nmax + 2;
+      for (int p = 0; p < c->W; ++p) {
+        scnt[p] = s.all[(size_t(c->rank) * c->W + p) * Nc + 1 + mb];  // requester -> owner p
+        rcnt[p] = s.all[(size_t(p) * c->W + c->rank) * Nc + 1 + mb];  // from requester p
+      }
+      a2a_rows(*c, c->src_rows + s.src_base[mb] * c->D, scnt, c->own_rows + s.own_base[mb] * c->D, rcnt, ms);
+      if (mb == s.N - 1) {
+        NEST_CUDA(cudaStreamWaitEvent(ms, other.ev_gather, 0));
+        launch_reduce_sgd(*c, s, lr_over_B, ms);
+        NEST_CUDA(cudaEventRecord(s.ev_update, ms));
+        NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
+      }
+    } else if (mb == s.N - 1) {
+      NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
+      launch_reduce_sgd(*c, s, lr_over_B, cs);
+      NEST_CUDA(cudaEventRecord(s.ev_update, cs));
+    }
+    if (mb == s.N - 1) s.updated = true;
+  });
+}
+
+nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t rows, float* dout,
+                                 void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CHECK(c->tower != nullptr, NEST_ERR_INVALID, "tower_layers == 0");
+    NEST_CHECK(rows % c->F == 0, NEST_ERR_INVALID, "rows must be a multiple of F");
+    tower_run(*c, pooled, rows, dout, S(stream));
+  });
+}
+
+nest_status_t nest_slot_info(const nest_ctx_t* ctx, int32_t slot, nest_slot_info_t* info) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !info || (slot != 0 && slot != 1)) return NEST_ERR_INVALID;
+  *info = c->slot[slot].info;
+  info->valid = c->slot[slot].routed ? 1 : 0;
+  return NEST_OK;
+}
+
+nest_status_t nest_route_view(const nest_ctx_t* ctx, int32_t slot, nest_route_view_t* v) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !v || (slot != 0 && slot != 1)) return NEST_ERR_INVALID;
+  const Slot& s = c->slot[slot];
+  v->uniq = s.uniq;
+  v->inverse = s.inverse;
+  v->mask = s.mask;
+  v->pos = s.pos;
+  v->send_counts = s.xfer + int64_t(c->rank) * c->W * (c->Nmax + 2);
+  v->all_counts = s.xfer;
+  v->recv_keys = s.recv;
+  v->owner_rows = s.owner_rows;
+  v->owner_inv = s.owner_inv;
+  v->n_owner = s.n_owner;
+  v->buffer = s.buffer;
+  return NEST_OK;
+}
+
+nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CHECK(n >= 0 && (n == 0 || (keys && out)), NEST_ERR_INVALID, "bad arguments");
+    launch_read_rows(*c, keys, n, out, S(stream));
+  });
+}
+
+const char* nest_last_error(const nest_ctx_t* ctx) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  return c ? c->last_error.c_str() : g_create_error.c_str();
+}
+
+}  // extern "C"

@@ -1,0 +1,393 @@
+// Internal header of libnest.so: context layout, device helpers, and the two
+// generic building blocks every stage uses -- a 3-phase exclusive scan and a
+// stable LSD radix sort of (uint32 key, int32 value) pairs.
+//
+// Design notes: every hot-path stage is HBM-bound; no
+// stage is a dense contraction, so no tensor cores are used here.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "nest.h"
+
+namespace nest {
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+struct Error {
+  nest_status_t code;
+  std::string msg;
+};
+
+#define NEST_CUDA(call)                                                           \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      throw ::nest::Error{NEST_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+#define NEST_NCCL(call)                                                           \
+  do {                                                                            \
+    ncclResult_t r_ = (call);                                                     \
+    if (r_ != ncclSuccess)                                                        \
+      throw ::nest::Error{NEST_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+#define NEST_CHECK(cond, code, text)                                              \
+  do {                                                                            \
+    if (!(cond)) throw ::nest::Error{code, text};                                 \
+  } while (0)
+
+#define NEST_LAUNCH_CHECK() NEST_CUDA(cudaGetLastError())
+
+// device error bits (OR-ed into ctx->d_err)
+enum : int32_t { kErrKeyRange = 1, kErrShard = 2 };
+
+constexpr int kRowBits = 40;
+constexpr uint64_t kRowMask = (uint64_t(1) << kRowBits) - 1;
+constexpr uint64_t kKeyMask56 = (uint64_t(1) << 56) - 1;
+constexpr int kMbShift = 28;                      // occ_mbrow = mb << 28 | row
+constexpr uint32_t kRowFieldMask = (1u << kMbShift) - 1;
+
+// ----------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------
+struct Slot {
+  // source side (this rank as requester)
+  int64_t* uniq = nullptr;         // [Kcap]
+  int32_t* inverse = nullptr;      // [Kcap]
+  uint32_t* mask = nullptr;        // [Kcap]
+  int32_t* pos = nullptr;          // [Nmax][Kcap+1]
+  uint32_t* skey = nullptr;        // [Kcap] sorted (mb << ubits | u)
+  int32_t* sval = nullptr;         // [Kcap] sorted dout row of the occurrence
+  int32_t* perm = nullptr;         // [Bcap]
+  int32_t* bag_off = nullptr;      // [Bcap*F+1]
+  int32_t* samp_base = nullptr;    // [Bcap] output row base of each sample in its mb
+  int32_t* mb_of = nullptr;        // [Bcap]
+  int32_t* off = nullptr;          // [W+1] per-owner offsets into uniq (device)
+  int32_t* xfer = nullptr;         // device: all_counts [W][W][Nmax+2] | mbnnz [Nmax] | err [1]
+  int32_t* h_xfer = nullptr;       // pinned mirror
+  // owner side
+  int64_t* recv = nullptr;         // [Rcap] received key | mask << 56 (W>1)
+  uint32_t* obm = nullptr;         // owner bitmap over the local domain [owords+1]
+  int32_t* owr = nullptr;          // per-word rank [owords+1]
+  int32_t* owner_rows = nullptr;   // [Uocap] shard row of each owner-unique key
+  int32_t* owner_inv = nullptr;    // [Rcap]
+  int32_t* src_tab = nullptr;      // [Uocap][W] received position per source, -1 if none
+  int32_t* sendpos = nullptr;      // [Nmax][Rcap+1]
+  int32_t* n_owner = nullptr;      // [1] U_o
+  float* buffer = nullptr;         // [Uocap][d] HBM buffer (active / prefetch)
+  // host-known plan
+  nest_slot_info_t info{};
+  int N = 0, B = 0, cap = 0;
+  std::vector<int64_t> all;        // [W][W][N+2]
+  std::vector<int64_t> src_base, own_base, q0;   // per mb: row bases / sorted-occurrence starts
+  std::vector<int64_t> key_soff, key_roff;       // key All2All offsets
+  int ubits = 0;
+  bool routed = false, updated = false;
+  cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
+              ev_grad[NEST_MAX_MICRO_BATCHES] = {}, ev_ready = nullptr, ev_sync = nullptr;
+};
+
+struct Ctx {
+  nest_config_t cfg{};
+  std::vector<int64_t> rows;       // [T]
+  int W = 1, rank = 0, T = 0, D = 0, F = 1, Nmax = 1;
+  int64_t Kcap = 0, Bcap = 0, Rcap = 0, Uocap = 0, MBcap = 0, OMBcap = 0, Pcap = 0;
+  int64_t V = 0, Vo = 0;           // global / owner domain sizes (rows)
+  int64_t words = 0, owords = 0;   // bitmap words
+  std::vector<int64_t> seg_base;   // [W*T+1] host copy
+  std::vector<int64_t> lbase;      // [T+1]
+  // device constants
+  int64_t* d_rows = nullptr;       // [T]
+  int64_t* d_seg_base = nullptr;   // [W*T+1]
+  int64_t* d_lbase = nullptr;      // [T+1]
+  float* shard = nullptr;          // [Vo][d]
+  // shared transient workspace
+  uint32_t* sbm = nullptr;         // source bitmap [words+1] (W>1; W==1 uses slot obm)
+  int32_t* swr = nullptr;          // [words+1]
+  uint32_t* occ_dom = nullptr;     // [Kcap]
+  int32_t* occ_mbrow = nullptr;    // [Kcap]
+  uint32_t* tkey[2] = {nullptr, nullptr};  // radix ping-pong [Kcap]
+  int32_t* tval[2] = {nullptr, nullptr};
+  uint32_t* hist = nullptr;        // [256 * radix blocks + 1]
+  void* scan_tmp = nullptr;        // scan block sums, route-side streams (bytes)
+  void* scan_tmp_win = nullptr;    // scan block sums, window-side streams
+  int32_t* samp_scratch = nullptr; // [Bcap+1] unpooled sample prefix (route)
+  int64_t* packed = nullptr;       // [Kcap] key | mask << 56 (W>1 send buffer)
+  uint32_t* r_ldom = nullptr;      // [Rcap]
+  int32_t* seg_start = nullptr;    // [Kcap+1]
+  int32_t* seg_aux = nullptr;      // [2*(Kcap+1)] hot offsets
+  int32_t* hot_list = nullptr;     // [Kcap]
+  int32_t* seg_tot = nullptr;      // [4]
+  float* partial = nullptr;        // [Pcap][d]
+  float* src_rows = nullptr;       // [MBcap][d]
+  float* own_rows = nullptr;       // [OMBcap][d] (== src_rows when W == 1)
+  int32_t* d_err = nullptr;        // [1]
+  int32_t* d_cnt_scratch = nullptr; // [W*(Nmax)] mb counts scratch
+  int32_t* n_refreshed = nullptr;  // [1] rows copied by the last refresh
+  Slot slot[2];
+  ncclComm_t comm = nullptr, comm_aux = nullptr;
+  nest_status_t sticky = NEST_OK;
+  std::string last_error;
+  // tower (cuBLAS), see tower.cu
+  void* tower = nullptr;
+};
+
+// bump allocator over a caller-owned buffer (base == nullptr: size only)
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(int64_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += size_t(std::max<int64_t>(n, 1)) * sizeof(T);
+    return p;
+  }
+};
+
+// ----------------------------------------------------------------------------
+// small device helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// rank of bit x in a bitmap with per-word exclusive popcount prefix `wr`
+__device__ __forceinline__ int32_t bit_rank(const uint32_t* __restrict__ bm,
+                                            const int32_t* __restrict__ wr, uint32_t x) {
+  const uint32_t w = x >> 5, b = x & 31u;
+  return wr[w] + __popc(bm[w] & ((1u << b) - 1u));
+}
+__device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ bm, uint32_t x) {
+  return (bm[x >> 5] >> (x & 31u)) & 1u;
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 ldg_f4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ float4 ld_f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st_f4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+// streaming store (evict-first) for write-once outputs
+__device__ __forceinline__ void st_f4_cs(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// Row geometry for fp32 rows of D floats processed by groups of L lanes, each
+// lane owning VPL consecutive float4 chunks strided by L*4 floats.
+template <int D>
+struct RowGeom {
+  static_assert(D % 4 == 0, "dim must be a multiple of 4");
+  static constexpr int kVec = D / 4;                       // float4 per row
+  static constexpr int L = kVec < 32 ? kVec : 32;          // lanes per row
+  static constexpr int VPL = kVec / L;                     // float4 per lane
+  static constexpr int GPW = 32 / L;                       // groups (rows) per warp
+  static_assert(kVec % L == 0, "row must split evenly over lanes");
+};
+
+// ----------------------------------------------------------------------------
+// generic exclusive scan (3 phases) over n values produced by a functor
+// ----------------------------------------------------------------------------
+struct I2 {
+  int32_t a, b;
+  I2() = default;
+  __host__ __device__ I2(int32_t x, int32_t y) : a(x), b(y) {}
+  __host__ __device__ I2 operator+(const I2& o) const { return I2(a + o.a, b + o.b); }
+};
+__device__ __forceinline__ int32_t shfl_up_t(int32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ uint32_t shfl_up_t(uint32_t v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ long long shfl_up_t(long long v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ I2 shfl_up_t(I2 v, int d) {
+  return I2(__shfl_up_sync(0xffffffffu, v.a, d), __shfl_up_sync(0xffffffffu, v.b, d));
+}
+__device__ __forceinline__ int32_t shfl_down_t(int32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ uint32_t shfl_down_t(uint32_t v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ long long shfl_down_t(long long v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ I2 shfl_down_t(I2 v, int d) {
+  return I2(__shfl_down_sync(0xffffffffu, v.a, d), __shfl_down_sync(0xffffffffu, v.b, d));
+}
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <typename T>
+__device__ __forceinline__ T warp_reduce_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = v + shfl_down_t(v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = shfl_up_t(v, o);
+    if (lane >= o) v = v + n;
+  }
+  return v;
+}
+
+template <typename T, typename In>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(In in, int64_t n, T* block_sums) {
+  __shared__ T ws[kScanThreads / 32];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile;
+  T acc = T();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanThreads + threadIdx.x;
+    if (i < n) acc = acc + in(i);
+  }
+  acc = warp_reduce_sum(acc);
+  if (lane_id() == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T v = threadIdx.x < kScanThreads / 32 ? ws[threadIdx.x] : T();
+    v = warp_reduce_sum(v);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
+  }
+}
+
+// single block: in-place exclusive scan of sums[0..nb), total into sums[nb]
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_block_sums(T* sums, int nb) {
+  __shared__ T ws[32];
+  __shared__ T carry_s, total_s;
+  if (threadIdx.x == 0) carry_s = T();
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    T v = i < nb ? sums[i] : T();
+    T inc = warp_incl_scan(v);
+    T exc = shfl_up_t(inc, 1);
+    if (lane == 0) exc = T();
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      T w = ws[lane];
+      T wi = warp_incl_scan(w);
+      T we = shfl_up_t(wi, 1);
+      if (lane == 0) we = T();
+      ws[lane] = we;
+      if (lane == 31) total_s = wi;
+    }
+    __syncthreads();
+    const T carry = carry_s;
+    if (i < nb) sums[i] = carry + ws[warp] + exc;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + total_s;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[nb] = carry_s;
+}
+
+template <typename T, typename In, typename Out>
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(In in, int64_t n, const T* offsets,
+                                                            int nb, Out out) {
+  __shared__ T tile[kScanTile];
+  __shared__ T ws[kScanThreads / 32];
+  const int64_t base = int64_t(blockIdx.x) * kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanThreads + threadIdx.x;
+    tile[k * kScanThreads + threadIdx.x] = i < n ? in(i) : T();
+  }
+  __syncthreads();
+  T loc[kScanItems];
+  T s = T();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    loc[k] = s;
+    s = s + tile[threadIdx.x * kScanItems + k];
+  }
+  T inc = warp_incl_scan(s);
+  T exc = shfl_up_t(inc, 1);
+  if (lane_id() == 0) exc = T();
+  if (lane_id() == 31) ws[threadIdx.x >> 5] = inc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T v = threadIdx.x < kScanThreads / 32 ? ws[threadIdx.x] : T();
+    T vi = warp_incl_scan(v);
+    T ve = shfl_up_t(vi, 1);
+    if (threadIdx.x == 0) ve = T();
+    if (threadIdx.x < kScanThreads / 32) ws[threadIdx.x] = ve;
+  }
+  __syncthreads();
+  const T off = offsets[blockIdx.x] + ws[threadIdx.x >> 5] + exc;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) tile[threadIdx.x * kScanItems + k] = off + loc[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t i = base + k * kScanThreads + threadIdx.x;
+    if (i < n) out(i, tile[k * kScanThreads + threadIdx.x]);
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out(n, offsets[nb]);
+}
+
+inline int scan_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kScanTile - 1) / kScanTile); }
+
+// exclusive scan: out(i, prefix_i) for i in [0, n), out(n, total).
+// temp must hold scan_blocks(n) + 1 values of T.
+template <typename T, typename In, typename Out>
+void scan_exclusive(In in, int64_t n, Out out, void* temp, cudaStream_t st) {
+  const int nb = scan_blocks(n);
+  T* sums = reinterpret_cast<T*>(temp);
+  k_scan_reduce<T, In><<<nb, kScanThreads, 0, st>>>(in, n, sums);
+  k_scan_block_sums<T><<<1, 1024, 0, st>>>(sums, nb);
+  k_scan_down<T, In, Out><<<nb, kScanThreads, 0, st>>>(in, n, sums, nb, out);
+  NEST_LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------------------------------
+// stable LSD radix sort of (uint32 key, int32 value), 8-bit digits
+// ----------------------------------------------------------------------------
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;   // 4096
+constexpr int kRadixWarps = kRadixThreads / 32;
+
+inline int radix_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kRadixTile - 1) / kRadixTile); }
+
+void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+                      int32_t* vout, int64_t n, int bits, cudaStream_t st);
+
+// ----------------------------------------------------------------------------
+// stage launchers (route.cu / rows.cu / schedule.cu / tower.cu)
+// ----------------------------------------------------------------------------
+void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz,
+                   int B, const int32_t* perm, int N, cudaStream_t st);
+void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
+void launch_init_tables(Ctx& c, cudaStream_t st);
+void launch_gather(Ctx& c, Slot& s, cudaStream_t st);
+void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st);
+void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st);
+void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st);
+void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st);
+void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
+void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int B, int N, int mode,
+                     int32_t* perm, int32_t* mb_offsets, cudaStream_t st);
+void tower_create(Ctx& c);
+void tower_destroy(Ctx& c);
+void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st);
+
+}  // namespace nest

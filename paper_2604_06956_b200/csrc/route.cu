@@ -1,0 +1,615 @@
+// DBP Key Routing + Embedding Retrieval.
+//
+// Source side (R1): keys -> owner-major domain index dom(key) =
+//   seg_base[owner*T + table] + row div W, owner = row mod W.
+// Dedup is a presence bitmap over the domain (a counting sort with 1-bit
+// buckets): mark -> per-word popcount prefix -> set bits in ascending order ARE
+// the unique keys sorted by (owner, key); the rank of a bit is the inverse.
+// This replaces a comparison/radix sort of the K key occurrences by two
+// coalesced passes over them plus a pass over a V-bit bitmap that lives in L2
+// (13 MB for the DLRM config).  See DESIGN.md "R1 route".
+// Owner side (R3): the same on the owner's local domain (= shard row index).
+#include "nest_internal.cuh"
+
+namespace nest {
+
+// ---------------------------------------------------------------------------
+// radix sort (stable LSD, 8-bit digits): histogram -> scan -> ranked scatter
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys,
+                                                              int64_t n, int shift,
+                                                              uint32_t* __restrict__ hist, int nb) {
+  __shared__ uint32_t cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = int64_t(blockIdx.x) * kRadixTile;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll 4
+  for (int k = 0; k < kRadixItems; ++k) {
+    const int64_t i = base + k * kRadixThreads + threadIdx.x;
+    const bool v = i < n;
+    const uint32_t d = v ? (keys[i] >> shift) & 255u : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (v && (peers & lt) == 0) atomicAdd(&cnt[d], __popc(peers));
+  }
+  __syncthreads();
+  hist[int64_t(threadIdx.x) * nb + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
+    const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, int64_t n, int shift,
+    const uint32_t* __restrict__ offs, int nb, uint32_t* __restrict__ kout,
+    int32_t* __restrict__ vout) {
+  __shared__ uint32_t wcnt[kRadixWarps][256];
+  __shared__ uint32_t dstart[256];
+  __shared__ uint32_t gbase[256];
+  __shared__ uint32_t skeys[kRadixTile];
+  __shared__ int32_t svals[kRadixTile];
+  __shared__ uint32_t wsum[kRadixWarps];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+#pragma unroll
+  for (int w = 0; w < kRadixWarps; ++w) wcnt[w][threadIdx.x] = 0;
+  gbase[threadIdx.x] = offs[int64_t(threadIdx.x) * nb + blockIdx.x];
+  __syncthreads();
+  // warp w owns the contiguous items [w*512, w*512+512) of the tile, visited
+  // in rounds of 32: (warp, round, lane) order == input order -> stable
+  const int64_t base = int64_t(blockIdx.x) * kRadixTile + warp * (32 * kRadixItems);
+  const uint32_t lt = lanemask_lt();
+  uint32_t key[kRadixItems];
+  int32_t val[kRadixItems];
+  uint32_t lr[kRadixItems];
+#pragma unroll
+  for (int k = 0; k < kRadixItems; ++k) {
+    const int64_t i = base + k * 32 + lane;
+    const bool v = i < n;
+    key[k] = v ? kin[i] : 0xffffffffu;
+    val[k] = v ? vin[i] : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kRadixItems; ++k) {
+    const bool v = base + k * 32 + lane < n;
+    const uint32_t d = v ? (key[k] >> shift) & 255u : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t before = v ? wcnt[warp][d] : 0u;
+    __syncwarp();
+    if (v && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
+    __syncwarp();
+    lr[k] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kRadixWarps; ++w) {
+      const uint32_t cc = wcnt[w][d];
+      wcnt[w][d] = run;
+      run += cc;
+    }
+    const uint32_t inc = warp_incl_scan(run);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = lane < kRadixWarps ? wsum[lane] : 0u;
+      const uint32_t xi = warp_incl_scan(x);
+      if (lane < kRadixWarps) wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    dstart[d] = wsum[warp] + inc - run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kRadixItems; ++k) {
+    if (base + k * 32 + lane < n) {
+      const uint32_t d = (key[k] >> shift) & 255u;
+      const uint32_t s = dstart[d] + wcnt[warp][d] + lr[k];
+      skeys[s] = key[k];
+      svals[s] = val[k];
+    }
+  }
+  __syncthreads();
+  const int64_t tb = int64_t(blockIdx.x) * kRadixTile;
+  const int nvalid = n - tb < kRadixTile ? int(n - tb) : kRadixTile;
+  for (int s = threadIdx.x; s < nvalid; s += kRadixThreads) {
+    const uint32_t k2 = skeys[s];
+    const uint32_t d = (k2 >> shift) & 255u;
+    const uint32_t p = gbase[d] + (uint32_t(s) - dstart[d]);
+    kout[p] = k2;
+    vout[p] = svals[s];
+  }
+}
+
+void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+                      int32_t* vout, int64_t n, int bits, cudaStream_t st) {
+  if (n <= 0) return;
+  const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
+  const int nb = radix_blocks(n);
+  const uint32_t* sk = kin;
+  const int32_t* sv = vin;
+  for (int p = 0; p < passes; ++p) {
+    uint32_t* dk;
+    int32_t* dv;
+    if (p == passes - 1) {
+      dk = kout;
+      dv = vout;
+    } else {
+      const int t = (sk == c.tkey[0]) ? 1 : 0;
+      dk = c.tkey[t];
+      dv = c.tval[t];
+    }
+    k_radix_hist<<<nb, kRadixThreads, 0, st>>>(sk, n, 8 * p, c.hist, nb);
+    uint32_t* h = c.hist;
+    scan_exclusive<uint32_t>([=] __device__(int64_t i) { return h[i]; }, int64_t(256) * nb,
+                             [=] __device__(int64_t i, uint32_t v) { h[i] = v; }, c.scan_tmp, st);
+    k_radix_scatter<<<nb, kRadixThreads, 0, st>>>(sk, sv, n, 8 * p, c.hist, nb, dk, dv);
+    NEST_LAUNCH_CHECK();
+    sk = dk;
+    sv = dv;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase A kernels
+// ---------------------------------------------------------------------------
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return int(b);
+}
+
+// per sample of the batch (position q in micro-batch order)
+__global__ void k_sched_prep(int B, int cap, int F, int pooled, const int32_t* __restrict__ perm,
+                             const int32_t* __restrict__ bag_off, int32_t* __restrict__ perm_out,
+                             int32_t* __restrict__ mb_of, int32_t* __restrict__ samp_base,
+                             int32_t* __restrict__ mbnnz) {
+  __shared__ int32_t acc[NEST_MAX_MICRO_BATCHES];
+  if (threadIdx.x < NEST_MAX_MICRO_BATCHES) acc[threadIdx.x] = 0;
+  __syncthreads();
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x) {
+    const int b = perm ? perm[q] : q;
+    const int i = q / cap;
+    perm_out[q] = b;
+    mb_of[b] = i;
+    if (pooled) samp_base[b] = (q - i * cap) * F;
+    const int len = bag_off[int64_t(b + 1) * F] - bag_off[int64_t(b) * F];
+    atomicAdd(&acc[i], len);
+  }
+  __syncthreads();
+  if (threadIdx.x < NEST_MAX_MICRO_BATCHES && acc[threadIdx.x]) atomicAdd(&mbnnz[threadIdx.x], acc[threadIdx.x]);
+}
+
+// unpooled: samp_base[perm[q]] = excl[q] - excl[start of q's micro-batch]
+__global__ void k_unpooled_base(int B, int cap, const int32_t* __restrict__ perm,
+                                const int32_t* __restrict__ excl, int32_t* __restrict__ samp_base) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < B; q += gridDim.x * blockDim.x)
+    samp_base[perm[q]] = excl[q] - excl[(q / cap) * cap];
+}
+
+// per bag: occ_mbrow[j] = mb << 28 | output row of occurrence j
+template <bool kWarpPerBag>
+__global__ void k_expand(int64_t nbags, int F, int pooled, const int32_t* __restrict__ bag_off,
+                         const int32_t* __restrict__ mb_of, const int32_t* __restrict__ samp_base,
+                         int32_t* __restrict__ occ_mbrow) {
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  const int64_t step = kWarpPerBag ? nth / 32 : nth;
+  for (int64_t bag = kWarpPerBag ? tid / 32 : tid; bag < nbags; bag += step) {
+    const int b = int(bag / F), f = int(bag - int64_t(b) * F);
+    const int j0 = bag_off[bag], j1 = bag_off[bag + 1];
+    const int32_t mbh = mb_of[b] << kMbShift;
+    const int32_t sb = samp_base[b];
+    const int32_t s0 = bag_off[int64_t(b) * F];
+    for (int j = j0 + (kWarpPerBag ? lane_id() : 0); j < j1; j += kWarpPerBag ? 32 : 1)
+      occ_mbrow[j] = mbh | (pooled ? sb + f : sb + (j - s0));
+  }
+}
+
+// per occurrence: domain index + presence bit
+__global__ void k_mark(const int64_t* __restrict__ keys, int64_t nnz, int T, int W,
+                       const int64_t* __restrict__ rows, const int64_t* __restrict__ seg_base,
+                       uint32_t* __restrict__ occ_dom, uint32_t* __restrict__ bm,
+                       int32_t* __restrict__ err) {
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; j0 < nnz; j0 += nth) {
+    const int64_t j = j0 + lane;
+    uint32_t dom = 0xffffffffu;
+    if (j < nnz) {
+      const uint64_t key = uint64_t(keys[j]);
+      const uint64_t t = key >> kRowBits, row = key & kRowMask;
+      if (t < uint64_t(T) && row < uint64_t(__ldg(rows + t))) {
+        const uint64_t o = W == 1 ? 0 : row % uint64_t(W);
+        const uint64_t lr = W == 1 ? row : row / uint64_t(W);
+        dom = uint32_t(__ldg(seg_base + o * T + t) + int64_t(lr));
+      } else {
+        atomicOr(err, kErrKeyRange);
+      }
+      occ_dom[j] = dom;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, dom);
+    if (dom != 0xffffffffu && (peers & lt) == 0) atomicOr(&bm[dom >> 5], 1u << (dom & 31u));
+  }
+}
+
+// per bitmap word: emit the set bits in ascending order
+__global__ void k_emit(int64_t words, const uint32_t* __restrict__ bm, const int32_t* __restrict__ wr,
+                       int T, int W, int nseg, const int64_t* __restrict__ seg_base,
+                       int64_t* __restrict__ uniq, uint32_t* __restrict__ mask,
+                       int32_t* __restrict__ owner_rows) {
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
+       w += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t x = bm[w];
+    if (!x) continue;
+    int32_t r = wr[w];
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      const int64_t dom = w * 32 + b;
+      // segment (owner, table) containing dom: largest s with seg_base[s] <= dom
+      int lo = 0, hi = nseg;  // seg_base[nseg] = V > dom
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(seg_base + mid) <= dom) lo = mid; else hi = mid;
+      }
+      const int o = lo / T, t = lo - o * T;
+      const int64_t row = (dom - __ldg(seg_base + lo)) * W + o;
+      uniq[r] = (int64_t(t) << kRowBits) | row;
+      mask[r] = 0u;
+      if (owner_rows) owner_rows[r] = int32_t(dom);
+      ++r;
+    }
+  }
+}
+
+// off[o] = rank of the first domain index of owner o (o = 0..W)
+__global__ void k_owner_offsets(int W, int T, const int64_t* __restrict__ seg_base,
+                                const uint32_t* __restrict__ bm, const int32_t* __restrict__ wr,
+                                int32_t* __restrict__ off) {
+  const int o = threadIdx.x;
+  if (o <= W) off[o] = bit_rank(bm, wr, uint32_t(seg_base[int64_t(o) * T]));
+}
+
+// per occurrence: inverse, micro-batch mask, sort key/value
+__global__ void k_inverse(int64_t nnz, const uint32_t* __restrict__ occ_dom,
+                          const int32_t* __restrict__ occ_mbrow, const uint32_t* __restrict__ bm,
+                          const int32_t* __restrict__ wr, int ubits, int32_t* __restrict__ inverse,
+                          uint32_t* __restrict__ mask, uint32_t* __restrict__ skey,
+                          int32_t* __restrict__ sval) {
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t j0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; j0 < nnz; j0 += nth) {
+    const int64_t j = j0 + lane;
+    uint32_t u = 0xffffffffu, bit = 0;
+    if (j < nnz) {
+      const uint32_t dom = occ_dom[j];
+      const int32_t mr = occ_mbrow[j];
+      const uint32_t mb = uint32_t(mr) >> kMbShift;
+      if (dom != 0xffffffffu) {
+        u = uint32_t(bit_rank(bm, wr, dom));
+        bit = 1u << mb;
+      }
+      const uint32_t uu = u == 0xffffffffu ? 0u : u;
+      inverse[j] = int32_t(uu);
+      skey[j] = (mb << ubits) | uu;
+      sval[j] = mr & int32_t(kRowFieldMask);
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, u);
+    const uint32_t bits = __reduce_or_sync(peers, bit);
+    if (u != 0xffffffffu && (peers & lt) == 0) atomicOr(&mask[u], bits);
+  }
+}
+
+// per unique key: per (owner, micro-batch) counts
+__global__ void k_mb_counts(const int32_t* __restrict__ off, int W, int N,
+                            const uint32_t* __restrict__ mask, int32_t* __restrict__ cnt) {
+  __shared__ int32_t sc[NEST_MAX_WORLD * NEST_MAX_MICRO_BATCHES];
+  __shared__ int32_t soff[NEST_MAX_WORLD + 1];
+  for (int i = threadIdx.x; i < W * N; i += blockDim.x) sc[i] = 0;
+  for (int i = threadIdx.x; i <= W; i += blockDim.x) soff[i] = off[i];
+  __syncthreads();
+  const int U = soff[W];
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+    int o = 0;
+    while (o + 1 < W && soff[o + 1] <= u) ++o;
+    const uint32_t m = mask[u];
+    for (int i = 0; i < N; ++i)
+      if ((m >> i) & 1u) atomicAdd(&sc[o * N + i], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < W * N; i += blockDim.x)
+    if (sc[i]) atomicAdd(&cnt[i], sc[i]);
+}
+
+// this rank's row of the count exchange: per owner {U, U_1..U_N, err}
+__global__ void k_finalize_counts(int W, int N, int Nc, const int32_t* __restrict__ off,
+                                  const int32_t* __restrict__ cnt, const int32_t* __restrict__ err,
+                                  int32_t* __restrict__ row) {
+  for (int o = threadIdx.x; o < W; o += blockDim.x) {
+    int32_t* r = row + int64_t(o) * Nc;
+    r[0] = off[o + 1] - off[o];
+    for (int i = 0; i < N; ++i) r[1 + i] = cnt[o * N + i];
+    r[Nc - 1] = *err;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase B (owner side, W > 1)
+// ---------------------------------------------------------------------------
+__global__ void k_pack(const int32_t* __restrict__ Uptr, const int64_t* __restrict__ uniq,
+                       const uint32_t* __restrict__ mask, int64_t* __restrict__ packed) {
+  const int U = *Uptr;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x)
+    packed[u] = uniq[u] | (int64_t(mask[u]) << 56);
+}
+
+__global__ void k_owner_mark(int64_t R, const int64_t* __restrict__ recv, int T, int W, int rank,
+                             const int64_t* __restrict__ rows, const int64_t* __restrict__ lbase,
+                             uint32_t* __restrict__ r_ldom, uint32_t* __restrict__ bm,
+                             int32_t* __restrict__ err) {
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t r0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; r0 < R; r0 += nth) {
+    const int64_t r = r0 + lane;
+    uint32_t ld = 0xffffffffu;
+    if (r < R) {
+      const uint64_t key = uint64_t(recv[r]) & kKeyMask56;
+      const uint64_t t = key >> kRowBits, row = key & kRowMask;
+      if (t < uint64_t(T) && row < uint64_t(__ldg(rows + t)) && row % uint64_t(W) == uint64_t(rank))
+        ld = uint32_t(__ldg(lbase + t) + int64_t(row / uint64_t(W)));
+      else
+        atomicOr(err, kErrShard);
+      r_ldom[r] = ld;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, ld);
+    if (ld != 0xffffffffu && (peers & lt) == 0) atomicOr(&bm[ld >> 5], 1u << (ld & 31u));
+  }
+}
+
+__global__ void k_owner_emit(int64_t words, const uint32_t* __restrict__ bm,
+                             const int32_t* __restrict__ wr, int W, int32_t* __restrict__ owner_rows,
+                             int32_t* __restrict__ src_tab) {
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
+       w += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t x = bm[w];
+    int32_t r = wr[w];
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      owner_rows[r] = int32_t(w * 32 + b);
+      for (int s = 0; s < W; ++s) src_tab[int64_t(r) * W + s] = -1;
+      ++r;
+    }
+  }
+}
+
+struct Offs64 {
+  int32_t v[NEST_MAX_WORLD + 1];
+};
+
+__global__ void k_owner_inv(int64_t R, const uint32_t* __restrict__ r_ldom,
+                            const uint32_t* __restrict__ bm, const int32_t* __restrict__ wr, int W,
+                            Offs64 roff, int32_t* __restrict__ owner_inv, int32_t* __restrict__ src_tab) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < R;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t ld = r_ldom[r];
+    if (ld == 0xffffffffu) {
+      owner_inv[r] = 0;
+      continue;
+    }
+    const int32_t u = bit_rank(bm, wr, ld);
+    owner_inv[r] = u;
+    int s = 0;
+    while (s + 1 < W && roff.v[s + 1] <= r) ++s;
+    src_tab[int64_t(u) * W + s] = int32_t(r);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+static int bits_for(int64_t n) {  // bits to represent values in [0, n)
+  int b = 0;
+  while ((int64_t(1) << b) < n) ++b;
+  return b;
+}
+
+// bitmap popcount prefix: wr[i] = sum_{w<i} popc(bm[w]) for i in [0, nw]; n_out <- total
+static void popc_scan(Ctx& c, const uint32_t* bm, int32_t* wr, int64_t nw, int32_t* total_out,
+                      cudaStream_t st) {
+  scan_exclusive<int32_t>(
+      [=] __device__(int64_t i) { return int32_t(__popc(bm[i])); }, nw,
+      [=] __device__(int64_t i, int32_t v) {
+        wr[i] = v;
+        if (total_out && i == nw) *total_out = v;
+      },
+      c.scan_tmp, st);
+}
+
+void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz,
+                   int B, const int32_t* perm, int N, cudaStream_t st) {
+  const int W = c.W, F = c.F, Nc = c.Nmax + 2;
+  const bool pooled = c.cfg.pooling == NEST_POOL_SUM;
+  s.N = N;
+  s.B = B;
+  s.cap = B / N;
+  // source bitmap: the slot's own bitmap when W == 1 (it doubles as the owner
+  // bitmap used by the refresh), the shared transient one otherwise
+  uint32_t* bm = W == 1 ? s.obm : c.sbm;
+  int32_t* wr = W == 1 ? s.owr : c.swr;
+  NEST_CUDA(cudaMemsetAsync(bm, 0, sizeof(uint32_t) * (c.words + 2), st));
+  int32_t* xfer = s.xfer;
+  int32_t* mbnnz = xfer + int64_t(W) * W * Nc;
+  NEST_CUDA(cudaMemsetAsync(mbnnz, 0, sizeof(int32_t) * (c.Nmax + 1), st));
+  NEST_CUDA(cudaMemsetAsync(c.d_cnt_scratch, 0, sizeof(int32_t) * W * c.Nmax, st));
+  NEST_CUDA(cudaMemcpyAsync(s.bag_off, bag_offsets, sizeof(int32_t) * (int64_t(B) * F + 1),
+                            cudaMemcpyDeviceToDevice, st));
+  // schedule: micro-batch of every sample and output row bases
+  k_sched_prep<<<grid_for(B, 256), 256, 0, st>>>(B, s.cap, F, pooled ? 1 : 0, perm, s.bag_off,
+                                                  s.perm, s.mb_of, s.samp_base, mbnnz);
+  NEST_LAUNCH_CHECK();
+  if (!pooled) {
+    const int32_t* bo = s.bag_off;
+    const int32_t* pm = s.perm;
+    int32_t* tmp = c.samp_scratch;  // scratch [B+1]
+    scan_exclusive<int32_t>(
+        [=] __device__(int64_t q) {
+          const int b = pm[q];
+          return bo[int64_t(b + 1) * F] - bo[int64_t(b) * F];
+        },
+        B, [=] __device__(int64_t q, int32_t v) { tmp[q] = v; }, c.scan_tmp, st);
+    k_unpooled_base<<<grid_for(B, 256), 256, 0, st>>>(B, s.cap, s.perm, tmp, s.samp_base);
+  }
+  const int64_t nbags = int64_t(B) * F;
+  const bool long_bags = nbags > 0 && nnz / nbags >= 16;
+  if (long_bags)
+    k_expand<true><<<grid_for(nbags * 32, 256), 256, 0, st>>>(nbags, F, pooled, s.bag_off, s.mb_of,
+                                                               s.samp_base, c.occ_mbrow);
+  else
+    k_expand<false><<<grid_for(nbags, 256), 256, 0, st>>>(nbags, F, pooled, s.bag_off, s.mb_of,
+                                                           s.samp_base, c.occ_mbrow);
+  NEST_LAUNCH_CHECK();
+  // R1: mark, rank, emit
+  k_mark<<<grid_for(nnz, 256), 256, 0, st>>>(keys, nnz, c.T, W, c.d_rows, c.d_seg_base, c.occ_dom, bm,
+                                             c.d_err);
+  NEST_LAUNCH_CHECK();
+  popc_scan(c, bm, wr, c.words + 1, nullptr, st);
+  k_emit<<<grid_for(c.words, 256), 256, 0, st>>>(c.words, bm, wr, c.T, W, W * c.T, c.d_seg_base,
+                                                 s.uniq, s.mask, W == 1 ? s.owner_rows : nullptr);
+  k_owner_offsets<<<1, 128, 0, st>>>(W, c.T, c.d_seg_base, bm, wr, s.off);
+  s.ubits = bits_for(c.Kcap);
+  k_inverse<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, c.occ_dom, c.occ_mbrow, bm, wr, s.ubits, s.inverse,
+                                                s.mask, c.tkey[0], c.tval[0]);
+  k_mb_counts<<<grid_for(c.Kcap, 256, 148 * 4), 256, 0, st>>>(s.off, W, N, s.mask, c.d_cnt_scratch);
+  k_finalize_counts<<<1, 64, 0, st>>>(W, N, Nc, s.off, c.d_cnt_scratch, c.d_err,
+                                      xfer + int64_t(c.rank) * W * Nc);
+  NEST_LAUNCH_CHECK();
+  // R2: count exchange (every rank's counts and error flags to every rank)
+  if (W > 1) {
+    NEST_NCCL(ncclAllGather(xfer + int64_t(c.rank) * W * Nc, xfer, size_t(W) * Nc, ncclInt32,
+                            c.comm_aux, st));
+  }
+  const size_t xbytes = sizeof(int32_t) * (int64_t(W) * W * Nc + c.Nmax + 1);
+  NEST_CUDA(cudaMemcpyAsync(s.h_xfer, xfer, xbytes, cudaMemcpyDeviceToHost, st));
+  NEST_CUDA(cudaEventRecord(s.ev_sync, st));
+}
+
+// after the host sync: plan from the counts, then R1 tail, R2 keys, R3, R4
+void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
+  const int W = c.W, N = s.N, Nc = c.Nmax + 2, D = c.D;
+  // ---- host plan ----
+  s.all.assign(size_t(W) * W * Nc, 0);
+  for (size_t i = 0; i < s.all.size(); ++i) s.all[i] = s.h_xfer[i];
+  const int32_t* hmbnnz = s.h_xfer + int64_t(W) * W * Nc;
+  auto A = [&](int src, int own, int col) { return s.all[(size_t(src) * W + own) * Nc + col]; };
+  int32_t err = 0;
+  for (int r = 0; r < W; ++r)
+    for (int o = 0; o < W; ++o) err |= int32_t(A(r, o, Nc - 1));
+  err |= s.h_xfer[int64_t(W) * W * Nc + c.Nmax];
+  if (err & kErrKeyRange) throw Error{NEST_ERR_KEY_RANGE, "key out of range (table >= T or row >= rows[table])"};
+  if (err & kErrShard) throw Error{NEST_ERR_SHARD, "owner received a key it does not own"};
+  nest_slot_info_t& info = s.info;
+  info = nest_slot_info_t{};
+  info.num_micro_batches = N;
+  info.batch = s.B;
+  // capacity checks for EVERY rank (all ranks take the same decision)
+  for (int r = 0; r < W; ++r) {
+    int64_t recv = 0, mbrows = 0, mbrecv = 0;
+    for (int o = 0; o < W; ++o) {
+      recv += A(o, r, 0);
+      for (int i = 0; i < N; ++i) {
+        mbrows += A(r, o, 1 + i);
+        mbrecv += A(o, r, 1 + i);
+      }
+    }
+    if (recv > c.Rcap) throw Error{NEST_ERR_CAPACITY, "owner receives more keys than max_recv_keys"};
+    if (mbrows > c.MBcap) throw Error{NEST_ERR_CAPACITY, "micro-batch rows exceed max_mb_rows"};
+    if (mbrecv > c.OMBcap) throw Error{NEST_ERR_CAPACITY, "owner micro-batch rows exceed max_owner_mb_rows"};
+  }
+  int64_t U = 0, R = 0;
+  for (int o = 0; o < W; ++o) U += A(c.rank, o, 0);
+  for (int r = 0; r < W; ++r) R += A(r, c.rank, 0);
+  info.uniq = U;
+  info.recv = R;
+  s.src_base.assign(N + 1, 0);
+  s.own_base.assign(N + 1, 0);
+  s.q0.assign(N + 1, 0);
+  int64_t nnz = 0;
+  for (int i = 0; i < N; ++i) {
+    int64_t ui = 0, ri = 0;
+    for (int o = 0; o < W; ++o) {
+      ui += A(c.rank, o, 1 + i);
+      ri += A(o, c.rank, 1 + i);
+    }
+    info.mb_uniq[i] = ui;
+    info.mb_recv[i] = ri;
+    info.mb_nnz[i] = hmbnnz[i];
+    info.mb_out_rows[i] = c.cfg.pooling == NEST_POOL_SUM ? int64_t(s.cap) * c.F : hmbnnz[i];
+    s.src_base[i + 1] = s.src_base[i] + ui;
+    s.own_base[i + 1] = s.own_base[i] + ri;
+    s.q0[i + 1] = s.q0[i] + hmbnnz[i];
+    nnz += hmbnnz[i];
+  }
+  info.nnz = nnz;
+  s.key_soff.assign(W + 1, 0);
+  s.key_roff.assign(W + 1, 0);
+  for (int o = 0; o < W; ++o) s.key_soff[o + 1] = s.key_soff[o] + A(c.rank, o, 0);
+  for (int r = 0; r < W; ++r) s.key_roff[r + 1] = s.key_roff[r] + A(r, c.rank, 0);
+
+  // ---- R1 tail: per micro-batch positions among its keys, sorted occurrences ----
+  for (int i = 0; i < N; ++i) {
+    const uint32_t* mk = s.mask;
+    int32_t* pos = s.pos + int64_t(i) * (c.Kcap + 1);
+    scan_exclusive<int32_t>([=] __device__(int64_t u) { return int32_t((mk[u] >> i) & 1u); }, U,
+                            [=] __device__(int64_t u, int32_t v) { pos[u] = v; }, c.scan_tmp, st);
+  }
+  int mbbits = 0;
+  while ((1 << mbbits) < N) ++mbbits;
+  radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, s.ubits + mbbits, st);
+
+  if (W == 1) {
+    // owner == source: the owner-unique keys are the unique keys
+    s.n_owner = s.off + 1;
+  } else {
+    // ---- R2: key All2All (key | mask << 56), grouped send/recv ----
+    k_pack<<<grid_for(c.Kcap, 256, 148 * 8), 256, 0, st>>>(s.off + W, s.uniq, s.mask, c.packed);
+    NEST_LAUNCH_CHECK();
+    NEST_NCCL(ncclGroupStart());
+    for (int p = 0; p < W; ++p) {
+      NEST_NCCL(ncclSend(c.packed + s.key_soff[p], size_t(s.key_soff[p + 1] - s.key_soff[p]), ncclInt64,
+                         p, c.comm_aux, st));
+      NEST_NCCL(ncclRecv(s.recv + s.key_roff[p], size_t(s.key_roff[p + 1] - s.key_roff[p]), ncclInt64,
+                         p, c.comm_aux, st));
+    }
+    NEST_NCCL(ncclGroupEnd());
+    // ---- R3: owner dedup on the local domain ----
+    NEST_CUDA(cudaMemsetAsync(s.obm, 0, sizeof(uint32_t) * (c.owords + 2), st));
+    if (R > 0)
+      k_owner_mark<<<grid_for(R, 256), 256, 0, st>>>(R, s.recv, c.T, W, c.rank, c.d_rows, c.d_lbase,
+                                                     c.r_ldom, s.obm, c.d_err);
+    popc_scan(c, s.obm, s.owr, c.owords + 1, s.n_owner, st);
+    k_owner_emit<<<grid_for(c.owords + 1, 256), 256, 0, st>>>(c.owords + 1, s.obm, s.owr, W,
+                                                              s.owner_rows, s.src_tab);
+    Offs64 roff{};
+    for (int r = 0; r <= W; ++r) roff.v[r] = int32_t(s.key_roff[r]);
+    if (R > 0)
+      k_owner_inv<<<grid_for(R, 256), 256, 0, st>>>(R, c.r_ldom, s.obm, s.owr, W, roff, s.owner_inv,
+                                                    s.src_tab);
+    NEST_LAUNCH_CHECK();
+    for (int i = 0; i < N; ++i) {
+      const int64_t* rk = s.recv;
+      int32_t* sp = s.sendpos + int64_t(i) * (c.Rcap + 1);
+      scan_exclusive<int32_t>(
+          [=] __device__(int64_t r) { return int32_t((uint64_t(rk[r]) >> (56 + i)) & 1u); }, R,
+          [=] __device__(int64_t r, int32_t v) { sp[r] = v; }, c.scan_tmp, st);
+    }
+  }
+  // ---- R4: gather the owned rows from the shard into the slot buffer ----
+  launch_gather(c, s, st);
+  (void)D;
+}
+
+}  // namespace nest

@@ -1,0 +1,581 @@
+// Row-moving kernels of the hot path.  All are HBM-bound row copies / sums
+// over fp32 rows of D floats, moved as 128-bit vectors by lane groups
+// (RowGeom<D>): R4 prefetch gather, R6 send gather, R8 pool/expand, R10
+// deterministic segment-sum, R12 fused owner reduce + SGD + write-back, R5
+// dual-buffer refresh, N10 PRF table init.
+#include "nest_internal.cuh"
+
+namespace nest {
+
+#define NEST_DISPATCH_D(dval, ...)                                       \
+  switch (dval) {                                                        \
+    case 16: { constexpr int D = 16; __VA_ARGS__; } break;               \
+    case 32: { constexpr int D = 32; __VA_ARGS__; } break;               \
+    case 64: { constexpr int D = 64; __VA_ARGS__; } break;               \
+    case 128: { constexpr int D = 128; __VA_ARGS__; } break;             \
+    case 256: { constexpr int D = 256; __VA_ARGS__; } break;             \
+    default: throw Error{NEST_ERR_INVALID, "unsupported dim"};           \
+  }
+
+static inline int blocks_for_rows(int64_t rows, int rows_per_block, int max_blocks = 148 * 8) {
+  int64_t b = (rows + rows_per_block - 1) / rows_per_block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return int(b);
+}
+
+constexpr int kRowThreads = 256;
+
+// group id / count helpers for grid-stride loops over rows
+template <int D>
+struct Grp {
+  using G = RowGeom<D>;
+  int64_t g, ng;  // this group's index, number of groups in the grid
+  int l;          // lane within the group
+  __device__ Grp() {
+    const int lane = lane_id();
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    g = warp * G::GPW + lane / G::L;
+    ng = (int64_t(gridDim.x) * blockDim.x >> 5) * G::GPW;
+    l = lane % G::L;
+  }
+  __device__ __forceinline__ int col(int v) const { return (v * G::L + l) * 4; }
+};
+
+template <int D>
+__device__ __forceinline__ void copy_row(float* __restrict__ dst, const float* __restrict__ src,
+                                         const Grp<D>& gp) {
+#pragma unroll
+  for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(dst + gp.col(v), ld_f4(src + gp.col(v)));
+}
+
+// ---------------------------------------------------------------------------
+// R4: buffer[u] = shard[owner_rows[u]]
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_gather(const float* __restrict__ shard,
+                                                        const int32_t* __restrict__ rows,
+                                                        const int32_t* __restrict__ n_dev,
+                                                        float* __restrict__ out) {
+  Grp<D> gp;
+  const int64_t n = *n_dev;
+  constexpr int U = 4;
+  for (int64_t r0 = gp.g * U; r0 < n; r0 += gp.ng * U) {
+    int32_t idx[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) idx[k] = r0 + k < n ? __ldg(rows + r0 + k) : 0;
+    float4 v[U][RowGeom<D>::VPL];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+#pragma unroll
+      for (int q = 0; q < RowGeom<D>::VPL; ++q)
+        if (r0 + k < n) v[k][q] = ldg_f4(shard + int64_t(idx[k]) * D + gp.col(q));
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+#pragma unroll
+      for (int q = 0; q < RowGeom<D>::VPL; ++q)
+        if (r0 + k < n) st_f4(out + (r0 + k) * D + gp.col(q), v[k][q]);
+  }
+}
+
+void launch_gather(Ctx& c, Slot& s, cudaStream_t st) {
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW * 4;
+    k_gather<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        c.shard, s.owner_rows, s.n_owner, s.buffer);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// R6 (owner, W > 1): send rows of micro-batch mb in (source, key) order
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_send_gather(int64_t R, int mb,
+                                                             const int64_t* __restrict__ recv,
+                                                             const int32_t* __restrict__ owner_inv,
+                                                             const int32_t* __restrict__ sendpos,
+                                                             const float* __restrict__ buffer,
+                                                             float* __restrict__ out) {
+  Grp<D> gp;
+  for (int64_t r = gp.g; r < R; r += gp.ng) {
+    if (!((uint64_t(__ldg(recv + r)) >> (56 + mb)) & 1u)) continue;
+    const int64_t dst = __ldg(sendpos + r);
+    const int64_t src = __ldg(owner_inv + r);
+    copy_row<D>(out + dst * D, buffer + src * D, gp);
+  }
+}
+
+void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st) {
+  const int64_t R = s.info.recv;
+  if (R == 0) return;
+  float* out = c.own_rows + s.own_base[mb] * c.D;
+  const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    k_send_gather<D><<<blocks_for_rows(R, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        R, mb, s.recv, s.owner_inv, sp, s.buffer, out);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// R8: pool (sum per bag, left to right) or expand (one row per occurrence)
+// ---------------------------------------------------------------------------
+template <int D, bool W1>
+__global__ void __launch_bounds__(kRowThreads) k_pool(int64_t nrows, int F,
+                                                      const int32_t* __restrict__ perm_mb,
+                                                      const int32_t* __restrict__ bag_off,
+                                                      const int32_t* __restrict__ inverse,
+                                                      const int32_t* __restrict__ pos,
+                                                      const float* __restrict__ src,
+                                                      float* __restrict__ out) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL;
+  for (int64_t q = gp.g; q < nrows; q += gp.ng) {
+    const int p = int(q / F), f = int(q - int64_t(p) * F);
+    const int b = __ldg(perm_mb + p);
+    const int64_t bag = int64_t(b) * F + f;
+    const int j0 = __ldg(bag_off + bag), j1 = __ldg(bag_off + bag + 1);
+    float4 acc[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int j = j0;
+    for (; j + 1 < j1; j += 2) {  // two rows in flight, summed in order
+      const int u0 = __ldg(inverse + j), u1 = __ldg(inverse + j + 1);
+      const int64_t i0 = W1 ? u0 : __ldg(pos + u0), i1 = W1 ? u1 : __ldg(pos + u1);
+      float4 a[VPL], bb[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        a[v] = ldg_f4(src + i0 * D + gp.col(v));
+        bb[v] = ldg_f4(src + i1 * D + gp.col(v));
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) acc[v] = f4add(f4add(acc[v], a[v]), bb[v]);
+    }
+    if (j < j1) {
+      const int u0 = __ldg(inverse + j);
+      const int64_t i0 = W1 ? u0 : __ldg(pos + u0);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(src + i0 * D + gp.col(v)));
+    }
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) st_f4_cs(out + q * D + gp.col(v), acc[v]);
+  }
+}
+
+// unpooled: warp-group per sample of the micro-batch, rows in occurrence order
+template <int D, bool W1>
+__global__ void __launch_bounds__(kRowThreads) k_expand_rows(int nsamp, int F,
+                                                             const int32_t* __restrict__ perm_mb,
+                                                             const int32_t* __restrict__ bag_off,
+                                                             const int32_t* __restrict__ samp_base,
+                                                             const int32_t* __restrict__ inverse,
+                                                             const int32_t* __restrict__ pos,
+                                                             const float* __restrict__ src,
+                                                             float* __restrict__ out) {
+  Grp<D> gp;
+  for (int64_t p = gp.g; p < nsamp; p += gp.ng) {
+    const int b = __ldg(perm_mb + p);
+    const int j0 = __ldg(bag_off + int64_t(b) * F), j1 = __ldg(bag_off + int64_t(b + 1) * F);
+    const int64_t base = __ldg(samp_base + b);
+    for (int j = j0; j < j1; ++j) {
+      const int u = __ldg(inverse + j);
+      const int64_t i = W1 ? u : __ldg(pos + u);
+#pragma unroll
+      for (int v = 0; v < RowGeom<D>::VPL; ++v)
+        st_f4_cs(out + (base + (j - j0)) * D + gp.col(v), ldg_f4(src + i * D + gp.col(v)));
+    }
+  }
+}
+
+void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
+  const bool w1 = c.W == 1;
+  const float* src = w1 ? s.buffer : c.src_rows + s.src_base[mb] * c.D;
+  const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
+  const int32_t* perm_mb = s.perm + int64_t(mb) * s.cap;
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    if (c.cfg.pooling == NEST_POOL_SUM) {
+      const int64_t nrows = int64_t(s.cap) * c.F;
+      if (w1)
+        k_pool<D, true><<<blocks_for_rows(nrows, rpb, 148 * 16), kRowThreads, 0, st>>>(
+            nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+      else
+        k_pool<D, false><<<blocks_for_rows(nrows, rpb, 148 * 16), kRowThreads, 0, st>>>(
+            nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+    } else {
+      if (w1)
+        k_expand_rows<D, true><<<blocks_for_rows(s.cap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+            s.cap, c.F, perm_mb, s.bag_off, s.samp_base, s.inverse, pos, src, out);
+      else
+        k_expand_rows<D, false><<<blocks_for_rows(s.cap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+            s.cap, c.F, perm_mb, s.bag_off, s.samp_base, s.inverse, pos, src, out);
+    }
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// R10: deterministic segment-sum.  The occurrences of micro-batch mb are
+// sorted by unique key (stable, so ascending occurrence order inside a key).
+// Segment k (k = pos_mb[u]) sums dout[row] over its occurrences:
+//   cold (L <= C): one lane group sums the L rows in order;
+//   hot  (L > C): fixed chunks of C rows -> partial rows -> one block sums the
+//   partials in a fixed strided order + fixed tree.  No float atomics, so
+//   the result is bitwise reproducible run to run.
+// ---------------------------------------------------------------------------
+constexpr int kChunk = 32;
+
+__global__ void k_seg_heads(int64_t Ki, const uint32_t* __restrict__ skey, uint32_t umask,
+                            const int32_t* __restrict__ pos, int32_t* __restrict__ seg_start,
+                            int64_t Ui) {
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < Ki;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t u = skey[q] & umask;
+    if (q == 0 || (skey[q - 1] & umask) != u) seg_start[pos[u]] = int32_t(q);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) seg_start[Ui] = int32_t(Ki);
+}
+
+template <int D>
+__device__ __forceinline__ void sum_rows(const int32_t* __restrict__ sval, int64_t q0, int64_t q1,
+                                         const float* __restrict__ dout, const Grp<D>& gp,
+                                         float4 (&acc)[RowGeom<D>::VPL]) {
+  constexpr int VPL = RowGeom<D>::VPL;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t q = q0;
+  for (; q + 3 < q1; q += 4) {
+    int32_t r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[k] = __ldg(sval + q + k);
+    float4 x[4][VPL];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) x[k][v] = ldg_f4(dout + int64_t(r[k]) * D + gp.col(v));
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], x[k][v]);
+  }
+  for (; q < q1; ++q) {
+    const int32_t r = __ldg(sval + q);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(dout + int64_t(r) * D + gp.col(v)));
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, const int32_t* __restrict__ seg_start,
+                                                             const int32_t* __restrict__ sval,
+                                                             const float* __restrict__ dout,
+                                                             float* __restrict__ g) {
+  Grp<D> gp;
+  for (int64_t k = gp.g; k < Ui; k += gp.ng) {
+    const int64_t a = seg_start[k], b = seg_start[k + 1];
+    if (b - a > kChunk) continue;
+    float4 acc[RowGeom<D>::VPL];
+    sum_rows<D>(sval, a, b, dout, gp, acc);
+#pragma unroll
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(g + k * D + gp.col(v), acc[v]);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_segsum_hot_chunks(
+    const int32_t* __restrict__ tot, const int32_t* __restrict__ hot_list,
+    const int32_t* __restrict__ hot_ppos, const int32_t* __restrict__ seg_start,
+    const int32_t* __restrict__ sval, const float* __restrict__ dout, float* __restrict__ partial) {
+  Grp<D> gp;
+  const int H = tot[0], P = tot[1];
+  for (int64_t cidx = gp.g; cidx < P; cidx += gp.ng) {
+    int lo = 0, hi = H;  // largest h with hot_ppos[h] <= cidx
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (hot_ppos[mid] <= cidx) lo = mid; else hi = mid;
+    }
+    const int k = hot_list[lo];
+    const int64_t m = cidx - hot_ppos[lo];
+    const int64_t a = seg_start[k] + m * kChunk;
+    const int64_t e = seg_start[k + 1];
+    const int64_t b = e < a + kChunk ? e : a + kChunk;
+    float4 acc[RowGeom<D>::VPL];
+    sum_rows<D>(sval, a, b, dout, gp, acc);
+#pragma unroll
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(partial + cidx * D + gp.col(v), acc[v]);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
+    const int32_t* __restrict__ tot, const int32_t* __restrict__ hot_list,
+    const int32_t* __restrict__ hot_ppos, const float* __restrict__ partial, float* __restrict__ g) {
+  using G = RowGeom<D>;
+  constexpr int NG = (kRowThreads / 32) * G::GPW;  // groups per block
+  __shared__ float4 red[NG][G::kVec];
+  const int H = tot[0];
+  const int lane = lane_id();
+  const int grp = (threadIdx.x >> 5) * G::GPW + lane / G::L;
+  const int l = lane % G::L;
+  for (int h = blockIdx.x; h < H; h += gridDim.x) {
+    const int k = hot_list[h];
+    const int64_t p0 = hot_ppos[h], np = hot_ppos[h + 1] - p0;
+    float4 acc[G::VPL];
+#pragma unroll
+    for (int v = 0; v < G::VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t m = grp; m < np; m += NG)
+#pragma unroll
+      for (int v = 0; v < G::VPL; ++v)
+        acc[v] = f4add(acc[v], ld_f4(partial + (p0 + m) * D + (v * G::L + l) * 4));
+#pragma unroll
+    for (int v = 0; v < G::VPL; ++v) red[grp][v * G::L + l] = acc[v];
+    __syncthreads();
+    if (grp == 0) {
+#pragma unroll
+      for (int v = 0; v < G::VPL; ++v) {
+        float4 s = red[0][v * G::L + l];
+        for (int q = 1; q < NG; ++q) s = f4add(s, red[q][v * G::L + l]);
+        st_f4(g + int64_t(k) * D + (v * G::L + l) * 4, s);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) {
+  const int64_t Ui = s.info.mb_uniq[mb];
+  const int64_t Ki = s.info.mb_nnz[mb];
+  if (Ui == 0) return;
+  const uint32_t* skey = s.skey + s.q0[mb];
+  const int32_t* sval = s.sval + s.q0[mb];
+  const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
+  const uint32_t umask = (1u << s.ubits) - 1u;
+  float* g = c.src_rows + s.src_base[mb] * c.D;
+  int32_t* seg = c.seg_start;
+  k_seg_heads<<<blocks_for_rows(Ki, 256, 148 * 16), 256, 0, st>>>(Ki, skey, umask, pos, seg, Ui);
+  // hot-segment bookkeeping: (is_hot, chunks) prefix -> hot_list, hot_ppos
+  int32_t* hot_list = c.hot_list;
+  int32_t* hot_ppos = c.seg_aux;
+  int32_t* tot = c.seg_tot;
+  scan_exclusive<I2>(
+      [=] __device__(int64_t k) {
+        const int32_t L = seg[k + 1] - seg[k];
+        return L > kChunk ? I2(1, (L + kChunk - 1) / kChunk) : I2(0, 0);
+      },
+      Ui,
+      [=] __device__(int64_t k, I2 v) {
+        if (k == Ui) {
+          tot[0] = v.a;
+          tot[1] = v.b;
+          hot_ppos[v.a] = v.b;
+        } else if (seg[k + 1] - seg[k] > kChunk) {
+          hot_list[v.a] = int32_t(k);
+          hot_ppos[v.a] = v.b;
+        }
+      },
+      c.scan_tmp_win, st);
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    k_segsum_cold<D><<<blocks_for_rows(Ui, rpb, 148 * 16), kRowThreads, 0, st>>>(Ui, seg, sval, dout, g);
+    k_segsum_hot_chunks<D><<<148 * 4, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, seg, sval, dout,
+                                                            c.partial);
+    k_segsum_hot_final<D><<<148 * 2, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, g);
+  });
+  NEST_LAUNCH_CHECK();
+  (void)skey;
+}
+
+// ---------------------------------------------------------------------------
+// R12: owner reduce over (micro-batch, source) + SGD (Eq. 2) + write-back
+// ---------------------------------------------------------------------------
+struct MbBases {
+  int64_t v[NEST_MAX_MICRO_BATCHES];
+};
+
+template <int D, bool W1>
+__global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
+    const int32_t* __restrict__ n_dev, int N, int W, float lr, MbBases base,
+    const uint32_t* __restrict__ mask, const int32_t* __restrict__ pos, int64_t pos_stride,
+    const int32_t* __restrict__ src_tab, const int64_t* __restrict__ recv,
+    const int32_t* __restrict__ sendpos, int64_t sp_stride, const float* __restrict__ rows,
+    const int32_t* __restrict__ owner_rows, float* __restrict__ buffer, float* __restrict__ shard) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL;
+  const int64_t n = *n_dev;
+  for (int64_t u = gp.g; u < n; u += gp.ng) {
+    float4 acc[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (W1) {
+      const uint32_t m = __ldg(mask + u);
+      for (int i = 0; i < N; ++i) {
+        if (!((m >> i) & 1u)) continue;
+        const int64_t r = base.v[i] + __ldg(pos + i * pos_stride + u);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(rows + r * D + gp.col(v)));
+      }
+    } else {
+      for (int i = 0; i < N; ++i) {
+        for (int s = 0; s < W; ++s) {
+          const int32_t r = __ldg(src_tab + u * W + s);
+          if (r < 0 || !((uint64_t(__ldg(recv + r)) >> (56 + i)) & 1u)) continue;
+          const int64_t row = base.v[i] + __ldg(sendpos + i * sp_stride + r);
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(rows + row * D + gp.col(v)));
+        }
+      }
+    }
+    const int64_t srow = __ldg(owner_rows + u);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      float4 e = ld_f4(buffer + u * D + gp.col(v));
+      e.x = __fmaf_rn(-lr, acc[v].x, e.x);
+      e.y = __fmaf_rn(-lr, acc[v].y, e.y);
+      e.z = __fmaf_rn(-lr, acc[v].z, e.z);
+      e.w = __fmaf_rn(-lr, acc[v].w, e.w);
+      st_f4(buffer + u * D + gp.col(v), e);
+      st_f4_cs(shard + srow * D + gp.col(v), e);
+    }
+  }
+}
+
+void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st) {
+  MbBases b{};
+  const bool w1 = c.W == 1;
+  for (int i = 0; i < s.N; ++i) b.v[i] = w1 ? s.src_base[i] : s.own_base[i];
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    const int grid = blocks_for_rows(c.Uocap, rpb, 148 * 16);
+    if (w1)
+      k_reduce_sgd<D, true><<<grid, kRowThreads, 0, st>>>(
+          s.n_owner, s.N, 1, lr, b, s.mask, s.pos, c.Kcap + 1, nullptr, nullptr, nullptr, 0,
+          c.src_rows, s.owner_rows, s.buffer, c.shard);
+    else
+      k_reduce_sgd<D, false><<<grid, kRowThreads, 0, st>>>(
+          s.n_owner, s.N, c.W, lr, b, nullptr, nullptr, 0, s.src_tab, s.recv, s.sendpos, c.Rcap + 1,
+          c.own_rows, s.owner_rows, s.buffer, c.shard);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// R5: dual-buffer refresh: prefetch[u'] <- active[u] for keys in both sets
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_refresh(
+    const int32_t* __restrict__ n_p, const int32_t* __restrict__ rows_p,
+    const uint32_t* __restrict__ bm_a, const int32_t* __restrict__ wr_a,
+    const float* __restrict__ buf_a, float* __restrict__ buf_p, int32_t* __restrict__ count) {
+  Grp<D> gp;
+  const int64_t n = *n_p;
+  int32_t local = 0;
+  for (int64_t u = gp.g; u < n; u += gp.ng) {
+    const uint32_t ld = uint32_t(__ldg(rows_p + u));
+    if (!bit_test(bm_a, ld)) continue;
+    const int64_t ua = bit_rank(bm_a, wr_a, ld);
+    copy_row<D>(buf_p + u * D, buf_a + ua * D, gp);
+    if (gp.l == 0) ++local;
+  }
+  if (local) atomicAdd(count, local);
+}
+
+void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st) {
+  NEST_CUDA(cudaMemsetAsync(c.n_refreshed, 0, sizeof(int32_t), st));
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    k_refresh<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        p.n_owner, p.owner_rows, a.obm, a.owr, a.buffer, p.buffer, c.n_refreshed);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// N10: PRF initialisation
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float prf_value(uint64_t h1, int j, int mode, float lo, float scale) {
+  const uint64_t h = splitmix64(h1 ^ (uint64_t(j) * 0xD1B54A32D192ED03ull));
+  if (mode == NEST_INIT_DYADIC) return float(int(h >> 60) - 8) * 0.00390625f;
+  if (mode == NEST_INIT_ZERO) return 0.f;
+  const float u = float(uint32_t(h >> 40)) * 5.9604644775390625e-08f;  // 2^-24, exact
+  return __fmaf_rn(scale, u, lo);
+}
+
+__global__ void k_init_tables(int64_t nvec, int D, int T, int W, int rank,
+                              const int64_t* __restrict__ lbase, uint64_t seed, int mode, float lo,
+                              float scale, float* __restrict__ shard) {
+  const int vpr = D / 4;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nvec;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t ld = e / vpr;
+    const int c4 = int(e - ld * vpr);
+    int lo_t = 0, hi_t = T;  // largest t with lbase[t] <= ld
+    while (hi_t - lo_t > 1) {
+      const int mid = (lo_t + hi_t) >> 1;
+      if (__ldg(lbase + mid) <= ld) lo_t = mid; else hi_t = mid;
+    }
+    const int64_t row = (ld - __ldg(lbase + lo_t)) * W + rank;
+    const uint64_t key = (uint64_t(lo_t) << kRowBits) | uint64_t(row);
+    const uint64_t h1 = splitmix64(seed + 0x9E3779B97F4A7C15ull * (key + 1ull));
+    float4 v;
+    v.x = prf_value(h1, c4 * 4 + 0, mode, lo, scale);
+    v.y = prf_value(h1, c4 * 4 + 1, mode, lo, scale);
+    v.z = prf_value(h1, c4 * 4 + 2, mode, lo, scale);
+    v.w = prf_value(h1, c4 * 4 + 3, mode, lo, scale);
+    st_f4_cs(shard + e * 4, v);
+  }
+}
+
+void launch_init_tables(Ctx& c, cudaStream_t st) {
+  const int64_t nvec = c.Vo * c.D / 4;
+  const float lo = float(-1.0 / std::sqrt(double(c.D)));
+  const float scale = float(2.0 / std::sqrt(double(c.D)));
+  if (nvec == 0) return;
+  k_init_tables<<<148 * 32, 256, 0, st>>>(nvec, c.D, c.T, c.W, c.rank, c.d_lbase, c.cfg.seed,
+                                          c.cfg.init_mode, lo, scale, c.shard);
+  NEST_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// parity helper: out[i] = shard row of keys[i]
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_read_rows(
+    int64_t n, const int64_t* __restrict__ keys, int T, int W, int rank,
+    const int64_t* __restrict__ rows, const int64_t* __restrict__ lbase,
+    const float* __restrict__ shard, float* __restrict__ out, int32_t* __restrict__ err) {
+  Grp<D> gp;
+  for (int64_t i = gp.g; i < n; i += gp.ng) {
+    const uint64_t key = uint64_t(keys[i]);
+    const uint64_t t = key >> kRowBits, row = key & kRowMask;
+    const bool ok = t < uint64_t(T) && row < uint64_t(rows[t]) && row % uint64_t(W) == uint64_t(rank);
+    if (!ok) {
+      if (gp.l == 0) atomicOr(err, kErrShard);
+#pragma unroll
+      for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(out + i * D + gp.col(v), make_float4(0, 0, 0, 0));
+      continue;
+    }
+    const int64_t ld = lbase[t] + int64_t(row / uint64_t(W));
+    copy_row<D>(out + i * D, shard + ld * D, gp);
+  }
+}
+
+void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    k_read_rows<D><<<blocks_for_rows(n, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        n, keys, c.T, c.W, c.rank, c.d_rows, c.d_lbase, c.shard, out, c.d_err);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+}  // namespace nest

@@ -1,0 +1,163 @@
+// Stand-in dense tower: the FWP overlap partner, NOT the product (SURVEY R9,
+// BASELINE north_star "fixed stand-in dense tower (cuBLAS GEMMs)").
+// A fixed L-layer bf16 MLP (identity activations) over the pooled rows of a
+// micro-batch viewed as X0 = [B_i, F*d]: forward Y_l = X_{l-1} W_l^T, then a
+// fixed top gradient G, backward dW_l = dY_l^T X_{l-1} and dX_{l-1} = dY_l W_l,
+// with the input gradient dX_0 written as fp32 `dout`.  GEMMs run on the
+// tensor cores through cuBLAS (library GEMMs, allowed for the plain tower).
+#include <cublas_v2.h>
+
+#include "nest_internal.cuh"
+
+namespace nest {
+
+struct Tower {
+  cublasHandle_t h = nullptr;
+  int L = 0, H = 0, in0 = 0;
+  int64_t bmax = 0;
+  __nv_bfloat16* w = nullptr;       // weights, layer l at woff[l], [H, in_l] row-major
+  std::vector<int64_t> woff;
+  __nv_bfloat16* x = nullptr;       // activations X_0..X_{L-1}, X_l at xoff[l]
+  std::vector<int64_t> xoff;
+  __nv_bfloat16* dy[2] = {nullptr, nullptr};  // [bmax, max(H, in0)]
+  __nv_bfloat16* dw = nullptr;      // [H, max in]
+  __nv_bfloat16* gtop = nullptr;    // [bmax, H] fixed top gradient
+  void* ws = nullptr;
+  size_t ws_bytes = 32u << 20;
+  char* mem = nullptr;
+};
+
+#define NEST_CUBLAS(call)                                                                 \
+  do {                                                                                    \
+    cublasStatus_t s_ = (call);                                                           \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                      \
+      throw ::nest::Error{NEST_ERR_CUDA, std::string(#call) + ": cublas status " + std::to_string(int(s_))}; \
+  } while (0)
+
+size_t tower_workspace_bytes(const Ctx& c) {
+  const int L = c.cfg.tower_layers, H = c.cfg.tower_hidden;
+  if (L <= 0) return 0;
+  const int64_t in0 = int64_t(c.F) * c.D, bmax = c.Bcap;
+  int64_t elems = H * in0 + int64_t(L - 1) * H * H;   // weights
+  elems += bmax * in0 + int64_t(L - 1) * bmax * H;   // activations
+  elems += 2 * bmax * std::max<int64_t>(H, in0);     // dy ping-pong
+  elems += int64_t(H) * std::max<int64_t>(H, in0);   // dw
+  elems += bmax * H;                                 // top gradient
+  return size_t(elems) * 2 + (32u << 20) + 8 * 256;
+}
+
+void tower_bind(Ctx& c, char* mem) {
+  if (!mem) return;
+  Tower* t = new Tower();
+  t->mem = mem;
+  c.tower = t;
+}
+
+__global__ void k_fill_bf16(__nv_bfloat16* p, int64_t n, uint64_t seed, float scale) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * uint64_t(i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const float u = float(uint32_t(z >> 40)) * 5.9604644775390625e-08f;  // [0,1)
+    p[i] = __float2bfloat16((2.f * u - 1.f) * scale);
+  }
+}
+
+__global__ void k_cast_bf16(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n4) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(in)[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    reinterpret_cast<__nv_bfloat162*>(out)[2 * i] = a;
+    reinterpret_cast<__nv_bfloat162*>(out)[2 * i + 1] = b;
+  }
+}
+
+void tower_create(Ctx& c) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  NEST_CHECK(t != nullptr, NEST_ERR_INVALID, "tower memory not bound");
+  t->L = c.cfg.tower_layers;
+  t->H = c.cfg.tower_hidden;
+  NEST_CHECK(t->H >= 16 && t->H % 16 == 0, NEST_ERR_INVALID, "tower_hidden must be a positive multiple of 16");
+  t->in0 = c.F * c.D;
+  t->bmax = c.Bcap;
+  Carver w{t->mem};
+  const int L = t->L, H = t->H;
+  const int64_t in0 = t->in0, bmax = t->bmax;
+  t->woff.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) t->woff[l + 1] = t->woff[l] + int64_t(H) * (l == 0 ? in0 : H);
+  t->w = w.take<__nv_bfloat16>(t->woff[L]);
+  t->xoff.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) t->xoff[l + 1] = t->xoff[l] + bmax * (l == 0 ? in0 : H);
+  t->x = w.take<__nv_bfloat16>(t->xoff[L]);
+  t->dy[0] = w.take<__nv_bfloat16>(bmax * std::max<int64_t>(H, in0));
+  t->dy[1] = w.take<__nv_bfloat16>(bmax * std::max<int64_t>(H, in0));
+  t->dw = w.take<__nv_bfloat16>(int64_t(H) * std::max<int64_t>(H, in0));
+  t->gtop = w.take<__nv_bfloat16>(bmax * H);
+  t->ws = w.take<char>(int64_t(t->ws_bytes));
+  NEST_CUBLAS(cublasCreate(&t->h));
+  NEST_CUBLAS(cublasSetWorkspace(t->h, t->ws, t->ws_bytes));
+  NEST_CUBLAS(cublasSetMathMode(t->h, CUBLAS_DEFAULT_MATH));
+  for (int l = 0; l < L; ++l) {
+    const int64_t fan_in = l == 0 ? in0 : H;
+    k_fill_bf16<<<1024, 256>>>(t->w + t->woff[l], int64_t(H) * fan_in, 1000 + l, 1.f / std::sqrt(float(fan_in)));
+  }
+  k_fill_bf16<<<1024, 256>>>(t->gtop, bmax * H, 77, 1.f / 1024.f);
+  NEST_LAUNCH_CHECK();
+  NEST_CUDA(cudaDeviceSynchronize());
+}
+
+void tower_destroy(Ctx& c) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  if (!t) return;
+  if (t->h) cublasDestroy(t->h);
+  delete t;
+  c.tower = nullptr;
+}
+
+// row-major C[M,N] = op(A)[M,K] * op(B)[K,N]
+static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void* A, int lda,
+                    const void* B, int ldb, void* C, int ldc, cudaDataType ctype) {
+  const float alpha = 1.f, beta = 0.f;
+  NEST_CUBLAS(cublasGemmEx(t->h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K,
+                           &alpha, B, CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C, ctype, ldc,
+                           CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+}
+
+void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  const int64_t bm = rows / c.F;
+  if (bm == 0) return;
+  NEST_CHECK(bm <= t->bmax, NEST_ERR_CAPACITY, "tower batch exceeds max_batch");
+  NEST_CUBLAS(cublasSetStream(t->h, st));
+  const int L = t->L, H = t->H, in0 = t->in0, M = int(bm);
+  k_cast_bf16<<<148 * 8, 256, 0, st>>>(pooled, t->x, bm * in0 / 4);
+  NEST_LAUNCH_CHECK();
+  // forward: X_l = X_{l-1} W_l^T  (the last layer's output Y_L is not needed)
+  for (int l = 0; l < L - 1; ++l) {
+    const int in = l == 0 ? in0 : H;
+    gemm_rm(t, false, true, M, H, in, t->x + t->xoff[l], in, t->w + t->woff[l], in, t->x + t->xoff[l + 1], H,
+            CUDA_R_16BF);
+  }
+  {  // last layer forward (output discarded: dY_L is the fixed gradient)
+    const int in = L == 1 ? in0 : H;
+    gemm_rm(t, false, true, M, H, in, t->x + t->xoff[L - 1], in, t->w + t->woff[L - 1], in, t->dy[1], H,
+            CUDA_R_16BF);
+  }
+  // backward
+  const __nv_bfloat16* dy = t->gtop;
+  int cur = 0;
+  for (int l = L - 1; l >= 0; --l) {
+    const int in = l == 0 ? in0 : H;
+    gemm_rm(t, true, false, H, in, M, dy, H, t->x + t->xoff[l], in, t->dw, in, CUDA_R_16BF);  // dW_l
+    if (l == 0) {
+      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, dout, in, CUDA_R_32F);  // dX_0 (fp32)
+    } else {
+      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, t->dy[cur], in, CUDA_R_16BF);
+      dy = t->dy[cur];
+      cur ^= 1;
+    }
+  }
+}
+
+}  // namespace nest

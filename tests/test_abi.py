@@ -1,0 +1,57 @@
+"""The C-ABI library loads and exports every symbol include/nest.h declares
+(no compute calls: runs without a GPU)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2604_06956_b200 import build as B
+    B.build()
+    from paper_2604_06956_b200 import _lib as L
+    return L.load()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "nest.h")).read()
+    return sorted(set(re.findall(r"NEST_API\s+[\w\s\*]+?\b(nest_\w+)\s*\(", src)))
+
+
+def test_header_declares_expected_api():
+    from paper_2604_06956_b200 import _lib as L
+    assert declared_symbols() == sorted(L.SYMBOLS)
+
+
+def test_every_declared_symbol_exported(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_host_only_calls(lib):
+    from paper_2604_06956_b200 import _lib as L
+    rows = (C.c_int64 * 4)(1000, 1000, 1000, 1001)
+    cfg = L.Config(world=2, rank=1, num_tables=4, dim=16, table_rows=rows, pooling=0,
+                   num_features=4, max_keys=1000, max_batch=64, max_micro_batches=4, seed=1)
+    tb, wb = C.c_size_t(), C.c_size_t()
+    assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 0
+    # rank 1 of 2 owns the odd rows: 500 + 500 + 500 + 500
+    assert lib.nest_shard_rows(C.byref(cfg)) == 2000
+    assert tb.value == 2000 * 16 * 4 and wb.value > 0
+    cfg.dim = 48
+    assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 1  # INVALID
+    assert b"dim" in lib.nest_last_error(None)
+    assert lib.nest_version().startswith(b"nestpipe")
+
+
+def test_sm100a_cubin_present():
+    """The library carries sm_100a SASS (no PTX-only JIT path)."""
+    import subprocess
+    from paper_2604_06956_b200 import build as B
+    B.build()
+    out = subprocess.run(["cuobjdump", "--list-elf", B.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out

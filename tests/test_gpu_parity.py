@@ -1,0 +1,261 @@
+"""GPU parity: libnest.so (through the C ABI) vs the CPU oracle (-m gpu).
+
+Bar (BASELINE north_star): keys, routing, counts and offsets bit-exact;
+pooled rows, gradients and tables within 1e-5 relative (normwise per row,
+SURVEY §8(c) Q13) -- and bit-exact in parity regime P1 (dyadic values, where
+every sum is exact in fp32).
+"""
+import numpy as np
+import pytest
+
+import workload as WL
+from oracle import cluster as OC
+from oracle import pipeline as OP
+from oracle import prf as OPRF
+from oracle import routing as OR
+from oracle import step as OS
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2604_06956_b200 import NestContext, NestError  # noqa: E402
+from paper_2604_06956_b200.runner import Runner  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def to_dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV, dtype)
+
+
+def make_ctx(cfg, B, N=1, K=None, init="dyadic", seed=1, **kw):
+    K = K or int(B * cfg.num_features * cfg.bag_len[1])
+    return NestContext(cfg.table_rows, cfg.dim, pooling=cfg.pooling, max_keys=K, max_batch=B,
+                       max_micro_batches=N, seed=seed, init_mode=init, device=DEV, **kw)
+
+
+def rel_rowwise_ok(gpu, ref, tol=1e-5, scale=None):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    num = np.linalg.norm(gpu - ref, axis=1)
+    den = np.linalg.norm(ref if scale is None else scale, axis=1)
+    return np.all(num <= tol * np.maximum(den, 1e-30))
+
+
+# --------------------------------------------------------------------------- init
+@pytest.mark.parametrize("init", ["uniform", "dyadic"])
+def test_init_tables_match_prf(init):
+    cfg = WL.CONFIGS["tiny"]
+    ctx = make_ctx(cfg, 32, init=init, seed=7)
+    keys = np.array([(t << 40) | r for t in range(4) for r in (0, 1, 17, 500, 999)], dtype=np.int64)
+    got = ctx.read_rows(to_dev(keys, torch.int64)).cpu().numpy()
+    ref = OPRF.init_rows(7, keys, cfg.dim, init)
+    assert np.array_equal(got, ref)
+
+
+# --------------------------------------------------------------------------- route
+@pytest.mark.parametrize("N,B,seed", [(1, 32, 0), (2, 32, 1), (4, 64, 2), (8, 64, 3)])
+def test_route_w1_bit_exact(N, B, seed):
+    cfg = WL.CONFIGS["tiny"]
+    keys, offs = WL.gen_batch(cfg, seed, 0, 0, batch=B)
+    ctx = make_ctx(cfg, B, N=N)
+    perm, mbo = ctx.fwp_schedule(None, None, B, N, "sequential")
+    ctx.route(0, to_dev(keys, torch.int64), to_dev(offs, torch.int32), B, perm=perm, mb_offsets=mbo, N=N)
+    v = ctx.route_view(0)
+    mb = OR.mb_of_occurrence(offs, cfg.num_features, perm.cpu().numpy(), mbo.cpu().numpy())
+    rs = OR.route_source(keys, 1, mb, N)
+    assert np.array_equal(v["uniq"], rs.uniq)
+    assert np.array_equal(v["inverse"], rs.inverse)
+    assert np.array_equal(v["mask"].astype(np.int64), rs.mask)
+    assert np.array_equal(v["pos"].astype(np.int64), rs.pos)
+    assert v["send_counts"][0, 0] == rs.send_counts[0]
+    assert np.array_equal(v["send_counts"][0, 1:1 + N], rs.mb_counts[:, 0])
+    # owner side at W=1: owner rows are the shard rows of uniq, ascending
+    assert v["n_owner"] == len(rs.uniq)
+    tab, row = WL.unpack_keys(rs.uniq)
+    assert np.array_equal(v["owner_rows"], tab * 1000 + row)
+    # the gathered buffer equals the PRF rows of uniq (R4)
+    assert np.array_equal(v["buffer"], OPRF.init_rows(1, rs.uniq, cfg.dim, "dyadic"))
+
+
+def test_route_mid_size_radix_tiles_and_ragged_tail():
+    """Several radix tiles (4096) with a ragged tail, heavy skew -> hot keys."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(5000, 3000, 200, 77), zipf=1.3, bag_repeats=True)
+    B = 3000
+    keys, offs = WL.gen_batch(cfg, 5, 0, 0, batch=B)
+    ctx = make_ctx(cfg, B, N=4, K=len(keys) + 11)
+    perm, mbo = ctx.fwp_schedule(None, None, B, 4, "sequential")
+    ctx.route(1, to_dev(keys, torch.int64), to_dev(offs, torch.int32), B, perm=perm, mb_offsets=mbo, N=4)
+    v = ctx.route_view(1)
+    mb = OR.mb_of_occurrence(offs, 4, perm.cpu().numpy(), mbo.cpu().numpy())
+    rs = OR.route_source(keys, 1, mb, 4)
+    assert np.array_equal(v["uniq"], rs.uniq)
+    assert np.array_equal(v["inverse"], rs.inverse)
+    assert np.array_equal(v["mask"].astype(np.int64), rs.mask)
+    assert np.array_equal(v["pos"].astype(np.int64), rs.pos)
+
+
+# --------------------------------------------------------------------------- full steps
+def _run_w1(cfg, B, N, T, init, dmode, lr, pipelined, seed=3, grad_mode="lin"):
+    F, d = cfg.num_features, cfg.dim
+    batches = [[WL.gen_batch(cfg, seed, t, 0, batch=B)] for t in range(T)]
+    pooled_mode = cfg.pooling == "sum"
+    douts = [[WL.gen_dout(seed, t, 0, B * F if pooled_mode else len(batches[t][0][0]), d, dmode)]
+             for t in range(T)]
+    K = max(len(b[0][0]) for b in batches)
+    ctx = make_ctx(cfg, B, N=N, K=K, init=init, seed=11)
+    run = Runner(ctx, N=N, pipelined=pipelined, lr_over_B=lr)
+    dev_b = [(to_dev(b[0][0], torch.int64), to_dev(b[0][1], torch.int32), B) for b in batches]
+    pooled_gpu = []
+    for t in range(T):
+        cap = B // N
+
+        def dout_fn(tt, i, pooled, t=t):
+            if grad_mode == "quad":
+                return pooled
+            if pooled_mode:
+                return to_dev(douts[t][0][i * cap * F:(i + 1) * cap * F], torch.float32)
+            o = batches[t][0][1]
+            return to_dev(douts[t][0][o[i * cap * F]:o[(i + 1) * cap * F]], torch.float32)
+        outs = run.step(dev_b[t], dev_b[t + 1] if t + 1 < T else None, dout_fn)
+        torch.cuda.synchronize()
+        pooled_gpu.append([o.cpu().numpy() for o in outs])
+    tab = OS.LazyTable(11, d, init)
+    ref_pooled, ref_rows = [], []
+    for t in range(T):
+        res = OS.sync_step(tab, batches[t], douts[t], lr, pooling=cfg.pooling, grad_mode=grad_mode)
+        ref_pooled.append(res.pooled[0])
+    allk = np.unique(np.concatenate([b[0][0] for b in batches]))
+    got = ctx.read_rows(to_dev(allk, torch.int64)).cpu().numpy()
+    return pooled_gpu, ref_pooled, got, tab.get(allk), tab
+
+
+@pytest.mark.parametrize("N,pipelined,grad", [(1, False, "lin"), (1, True, "lin"), (2, True, "lin"),
+                                              (4, True, "quad"), (8, False, "lin")])
+def test_train_w1_dyadic_bit_exact(N, pipelined, grad):
+    """P1: 10 steps, pooled rows of every step and the final tables bit-exact.
+    QUAD couples dout to the pooled values, whose dyadic resolution halves
+    with every update, so past step 2 it is compared in regime P2 (1e-5)."""
+    cfg = WL.CONFIGS["tiny"]
+    B = 32
+    pg, pr, got, ref, _ = _run_w1(cfg, B, N, 10, "dyadic", "dyadic", 2.0 ** -10, pipelined, grad_mode=grad)
+    for t in range(10):
+        if grad == "lin" or t < 2:
+            assert np.array_equal(np.concatenate(pg[t]), pr[t]), f"pooled step {t}"
+        else:
+            assert rel_rowwise_ok(np.concatenate(pg[t]), pr[t]), f"pooled step {t}"
+    if grad == "lin":
+        assert np.array_equal(got, ref)
+    else:
+        assert rel_rowwise_ok(got, ref)
+
+
+def test_train_w1_realistic_within_tolerance():
+    """P2: uniform init, normal gradients, 10 steps: 1e-5 relative per row."""
+    cfg = WL.CONFIGS["tiny"]
+    B = 64
+    pg, pr, got, ref, _ = _run_w1(cfg, B, 4, 10, "uniform", "realistic", 0.05, True)
+    for t in range(10):
+        assert rel_rowwise_ok(np.concatenate(pg[t]), pr[t])
+    assert rel_rowwise_ok(got, ref)
+
+
+def test_train_mid_size_hot_segments_p1():
+    """Hot keys with thousands of occurrences exercise the chunked two-level
+    segment reduce; P1 keeps the comparison bit-exact."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(4000, 50, 9, 2000), zipf=1.4, bag_repeats=True, dim=128)
+    B = 4096
+    pg, pr, got, ref, _ = _run_w1(cfg, B, 2, 3, "dyadic", "dyadic", 2.0 ** -12, True)
+    for t in range(3):
+        assert np.array_equal(np.concatenate(pg[t]), pr[t])
+    assert np.array_equal(got, ref)
+
+
+def test_run_to_run_bitwise_deterministic():
+    cfg = WL.CONFIGS["tiny"].with_(zipf=1.3, bag_repeats=True)
+    a = _run_w1(cfg, 256, 2, 3, "uniform", "realistic", 0.1, True)[2]
+    b = _run_w1(cfg, 256, 2, 3, "uniform", "realistic", 0.1, True)[2]
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("d", [16, 32, 64, 256])
+def test_dims(d):
+    cfg = WL.CONFIGS["tiny"].with_(dim=d)
+    pg, pr, got, ref, _ = _run_w1(cfg, 32, 2, 3, "dyadic", "dyadic", 2.0 ** -10, True)
+    assert np.array_equal(got, ref)
+
+
+def test_unpooled_expand_p1():
+    cfg = WL.CONFIGS["tiny"].with_(pooling="none", bag_len=(4, 9), bag_repeats=True)
+    B = 32
+    pg, pr, got, ref, _ = _run_w1(cfg, B, 2, 3, "dyadic", "dyadic", 2.0 ** -10, True)
+    for t in range(3):
+        assert np.array_equal(np.concatenate(pg[t]), pr[t])
+    assert np.array_equal(got, ref)
+
+
+# --------------------------------------------------------------------------- errors
+def test_error_paths():
+    cfg = WL.CONFIGS["tiny"]
+    keys, offs = WL.gen_batch(cfg, 0, 0, 0, batch=32)
+    ctx = make_ctx(cfg, 32, N=4)
+    with pytest.raises(NestError) as e:
+        ctx.fwp_schedule(None, None, 30, 4)
+    assert e.value.status == "NEST_ERR_DIVISIBILITY"
+    out = torch.empty((8 * 4, 16), device=DEV)
+    with pytest.raises(NestError) as e:
+        ctx.lookup_fwd(0, 0, out)
+    assert e.value.status == "NEST_ERR_ORDER"
+    bad = keys.copy()
+    bad[5] = (2 << 40) | 5000          # row >= rows[2]
+    with pytest.raises(NestError) as e:
+        ctx.route(0, to_dev(bad, torch.int64), to_dev(offs, torch.int32), 32)
+    assert e.value.status == "NEST_ERR_KEY_RANGE"
+    with pytest.raises(NestError):     # sticky
+        ctx.route(0, to_dev(keys, torch.int64), to_dev(offs, torch.int32), 32)
+
+
+# --------------------------------------------------------------------------- full size
+def test_dlrm_full_size_w1_sampled():
+    """BASELINE configs[1] at W=1 (the bench launch configuration): routing
+    invariants at full size, sampled pooled rows and sampled updated rows
+    computed one by one by the oracle."""
+    cfg = WL.CONFIGS["dlrm"]
+    B, N, F, d = cfg.batch_local, 4, cfg.num_features, cfg.dim
+    keys, offs = WL.gen_batch(cfg, 0, 0, 0)
+    ctx = NestContext(cfg.table_rows, d, max_keys=len(keys), max_batch=B, max_micro_batches=N,
+                      seed=5, init_mode="uniform", device=DEV)
+    run = Runner(ctx, N=N, pipelined=False, lr_over_B=0.5)
+    kd, od = to_dev(keys, torch.int64), to_dev(offs, torch.int32)
+    cap = B // N
+    dout_all = torch.randn(B * F, d, device=DEV, generator=torch.Generator(DEV).manual_seed(0))
+    outs = run.step((kd, od, B), None, lambda t, i, p: dout_all[i * cap * F:(i + 1) * cap * F])
+    torch.cuda.synchronize()
+    v = ctx.route_view(0)
+    info = v["info"]
+    # routing invariants at full size
+    assert info.uniq == len(np.unique(keys))
+    assert (np.diff(v["uniq"]) > 0).all()
+    assert np.array_equal(v["uniq"][v["inverse"]], keys)
+    # sampled pooled rows: oracle computes each bag from PRF rows
+    rng = np.random.default_rng(0)
+    for q in rng.integers(0, B * F, size=64):
+        i, r = divmod(int(q), cap * F)
+        b, f = i * cap + r // F, r % F
+        bag = keys[offs[b * F + f]:offs[b * F + f + 1]]
+        ref = OS.pool_sum(OPRF.init_rows(5, bag, d), np.array([0, len(bag)]))[0]
+        assert rel_rowwise_ok(outs[i][r][None].cpu().numpy(), ref[None])
+    # sampled updated rows: e' = e0 - s * sum of the bag grads of its occurrences
+    dnp = dout_all.cpu().numpy().astype(np.float64)
+    bag_of = np.repeat(np.arange(B * F), np.diff(offs))
+    sample = rng.choice(np.unique(keys), size=64, replace=False)
+    got = ctx.read_rows(to_dev(sample, torch.int64)).cpu().numpy()
+    for k, row in zip(sample, got):
+        occ = np.nonzero(keys == k)[0]
+        g = dnp[bag_of[occ]].sum(axis=0)
+        ref = OS.sgd_rows(OPRF.init_rows(5, np.array([k]), d), g[None], 0.5)[0]
+        scale = np.abs(dnp[bag_of[occ]]).sum(axis=0) * 0.5 + np.abs(ref)
+        assert np.all(np.abs(row - ref) <= 1e-5 * scale + 1e-7)
