@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Embedding-step benchmark (BASELINE.json metric) for the NestPipe hot path.
+
+One step = the whole hot path of SURVEY.md §8(a) over one batch per GPU:
+FWP schedule, DBP route of the next batch (dedup, count exchange, key
+All2All, owner dedup, prefetch gather), the frozen window of N micro-batches
+(send gather, embedding All2All, pool, stand-in tower fwd+bwd, segment-sum,
+gradient All2All), the fused owner reduce + SGD + write-back, and the
+dual-buffer refresh.  Weak scaling: 65,536 samples per GPU, fixed tables.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (this
+tier's reference arm) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workload as WL  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "samples/s"
+NVLINK_PEER_GBS = 770.0    # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="dlrm", choices=["dlrm", "tiny", "dbp_stress"])
+    ap.add_argument("--micro-batches", type=int, default=4)
+    ap.add_argument("--schedule", default="sequential", choices=["sequential", "clustered"])
+    ap.add_argument("--variant", default="et", choices=["et", "e"],
+                    help="et: embedding + stand-in tower (FWP overlap partner); e: embedding only")
+    ap.add_argument("--batches", type=int, default=3, help="distinct batches cycled per rank")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fwp-compare", action="store_true")
+    ap.add_argument("--trace", default="", help="write the per-stage trace JSON here")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("bf16_tflops_sustained", 1400.0)), "measured"
+    return 6650.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{gpu_index}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- workload
+def rank_batches(cfg, seed, rank, P):
+    return [WL.gen_batch(cfg, seed, t, rank) for t in range(P)]
+
+
+# ----------------------------------------------------------------------------- oracle arms
+def oracle_sample_step(cfg, seed, rank, samples, step=0):
+    """One oracle step (source routing + Eq. 1/2 step) on a bounded sample."""
+    from oracle import routing as OR
+    from oracle import step as OS
+    keys, offs = WL.gen_batch(cfg, seed, step, rank, batch=samples)
+    dout = WL.gen_dout(seed, step, rank, samples * cfg.num_features, cfg.dim, "realistic")
+    t0 = time.perf_counter()
+    OR.route_source(keys, 1)
+    tab = OS.LazyTable(seed, cfg.dim)
+    OS.sync_step(tab, [(keys, offs)], [dout], 1e-3, pooling=cfg.pooling)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, seed, budget_s=15.0):
+    samples = 1024
+    dt = oracle_sample_step(cfg, seed, 0, samples)
+    while dt < budget_s / 4 and samples < cfg.batch_local:
+        samples = min(cfg.batch_local, samples * 4)
+        dt = oracle_sample_step(cfg, seed, 0, samples)
+    return {"value": samples / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "host_cpus": len(os.sched_getaffinity(0)),
+            "sample": f"{samples} of {cfg.batch_local} samples of one rank's {cfg.name} batch; "
+                      f"oracle route_source + sync_step (numpy fp64, single thread), {dt:.2f} s"}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    samples = 1024
+    for t in range(args.warmup):
+        oracle_sample_step(cfg, args.seed, 0, samples, t)
+    tot = 0.0
+    for t in range(args.steps):
+        tot += oracle_sample_step(cfg, args.seed, 0, samples, args.warmup + t)
+    v = samples * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_json(args, cfg, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{samples} samples per step of one rank's {cfg.name} batch "
+                                       "(oracle route_source + sync_step, numpy fp64, 1 thread)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(args, cfg, world):
+    return {"workload": cfg.name, "tables": cfg.num_tables, "total_rows": int(sum(cfg.table_rows)),
+            "dim": cfg.dim, "batch_per_gpu": cfg.batch_local, "global_batch": cfg.batch_local * world,
+            "bag_len": f"U{{{cfg.bag_len[0]}..{cfg.bag_len[1]}}}", "zipf": cfg.zipf, "pooling": cfg.pooling,
+            "micro_batches": args.micro_batches, "schedule": args.schedule,
+            "variant": "E+T (embedding + stand-in tower)" if args.variant == "et" else "E (embedding only)",
+            "tower": f"{cfg.tower_layers}x{cfg.tower_hidden} bf16 cuBLAS" if args.variant == "et" else None,
+            "parallelism": f"tables row-sharded over {world} GPU(s), data-parallel samples",
+            "l2": "inputs larger than L2 (tables 4*rows*dim bytes, GB-scale per-step traffic)",
+            "pipelined": "DBP (route t+1 on aux stream) + FWP (comm/compute streams)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    cfg = WL.CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "RANK" in os.environ:
+        pass  # torchrun decides
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if args.warmup < 3:
+        args.warmup = 3
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2604_06956_b200 import NestContext, unique_ids
+    from paper_2604_06956_b200.runner import Runner
+
+    N = args.micro_batches
+    B, F, d = cfg.batch_local, cfg.num_features, cfg.dim
+    batches = rank_batches(cfg, args.seed, rank, args.batches)
+    K = max(len(k) for k, _ in batches)
+    uids = None
+    if world > 1:
+        obj = [unique_ids() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uids = obj[0]
+    ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, pooling=cfg.pooling, max_keys=K + 1024,
+                      max_batch=B, max_micro_batches=N, seed=args.seed + 1, init_mode="uniform",
+                      tower_layers=cfg.tower_layers if args.variant == "et" else 0,
+                      tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev,
+                      max_recv_keys=(int(1.6 * K) if world > 1 else 0),
+                      max_owner_mb_rows=(int(1.6 * K) if world > 1 else 0))
+    torch.cuda.synchronize()
+    # inputs resident in HBM (value) and pinned host copies (e2e)
+    dev_b = [(torch.from_numpy(k).to(dev), torch.from_numpy(o).to(dev), B) for k, o in batches]
+    host_b = [(torch.from_numpy(k).pin_memory(), torch.from_numpy(o).pin_memory()) for k, o in batches]
+    lr = 1e-3 / (B * world)
+
+    def make_dout_fn(runner):
+        if args.variant == "et":
+            douts = {}
+
+            def fn(t, i, pooled):
+                key = (i, pooled.shape[0])
+                if key not in douts:
+                    douts[key] = torch.empty_like(pooled)
+                ctx.tower_fwd_bwd(pooled, douts[key], stream=runner.compute)
+                return douts[key]
+            return fn
+        fixed = {}
+
+        def fn(t, i, pooled):
+            key = (i, pooled.shape[0])
+            if key not in fixed:
+                g = torch.Generator(device=dev).manual_seed(1000 + i)
+                fixed[key] = torch.randn(pooled.shape, generator=g, device=dev) * 1e-2
+            return fixed[key]
+        return fn
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def timed(runner, steps, t0, source=None, profile=False):
+        """Runs `steps` steps; returns device ms (max over ranks)."""
+        dout_fn = make_dout_fn(runner)
+        barrier()
+        if profile:
+            ctx.profile_enable(True)
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(runner.compute)
+        h2d = d2h = 0
+        for s in range(steps):
+            t = t0 + s
+            cur, nxt = t % len(dev_b), (t + 1) % len(dev_b)
+            if source == "host":
+                # e2e: this step's NEXT batch arrives from pinned host memory
+                hk, ho = host_b[nxt]
+                nk = torch.empty(hk.shape, dtype=hk.dtype, device=dev)
+                no = torch.empty(ho.shape, dtype=ho.dtype, device=dev)
+                nk.copy_(hk, non_blocking=True)
+                no.copy_(ho, non_blocking=True)
+                h2d += hk.numel() * 8 + ho.numel() * 4
+                nb = (nk, no, B)
+            else:
+                nb = dev_b[nxt]
+            # the current batch was routed by the previous step (DBP); only an
+            # unprimed runner routes it here
+            outs = runner.step(dev_b[cur], nb, dout_fn, keep_outputs=True)
+            if source == "host":
+                res = outs[-1][0].to("cpu", non_blocking=False)   # the step's result row
+                d2h += res.numel() * 4
+        runner.compute.wait_stream(runner.comm)
+        runner.compute.wait_stream(runner.aux)
+        end.record(runner.compute)
+        torch.cuda.synchronize()
+        ms = start.elapsed_time(end)
+        prof = None
+        if profile:
+            ctx.profile_enable(False)
+            prof = ctx.profile_read()
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms, prof, h2d, d2h
+
+    runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr)
+    timed(runner, args.warmup, 0)
+    clocks = Clocks(local)
+    clocks.start()
+    ms, prof, _, _ = timed(runner, args.steps, args.warmup, profile=True)
+    clk = clocks.stop()
+    value = B * world * args.steps / (ms / 1e3)
+
+    # e2e through the public API with host inputs (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        r2 = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr)
+        r2.t = runner.t
+        timed(r2, 2, runner.t, source="host")
+        ms_e, _, h2d, d2h = timed(r2, args.steps, r2.t, source="host")
+        counts_bytes = 4 * (world * world * (N + 2) + N + 1)
+        e2e = {"value": B * world * args.steps / (ms_e / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d // args.steps,
+               "d2h_bytes_per_step": d2h // args.steps + counts_bytes,
+               "ms_per_step": ms_e / args.steps}
+
+    # exposed All2All without FWP (N = 1) for comparison
+    no_fwp = None
+    if world > 1 and not args.no_fwp_compare and N > 1:
+        r1 = Runner(ctx, N=1, schedule="sequential", pipelined=True, lr_over_B=lr)
+        r1.t = runner.t + args.steps
+        timed(r1, 3, r1.t)
+        ms1, prof1, _, _ = timed(r1, max(5, args.steps // 2), r1.t, profile=True)
+        no_fwp = {"ms_per_step": ms1 / max(5, args.steps // 2),
+                  "a2a_exposed_ms_per_step": prof1["summary"]["a2a_exposed_ms"] / max(5, args.steps // 2),
+                  "a2a_ms_per_step": prof1["summary"]["a2a_ms"] / max(5, args.steps // 2)}
+
+    if rank == 0:
+        hbm_peak, bf16_peak, src = peaks()
+        st = prof["stages"]
+        steps = args.steps
+        stages = {}
+        for name, s in st.items():
+            if s["records"] == 0:
+                continue
+            e = {"ms_per_step": s["ms"] / steps, "launches_per_step": s["launches"] / steps,
+                 "records_per_step": s["records"] / steps}
+            if name == "tower":
+                e["tflops"] = s["bytes"] / (s["ms"] * 1e9) if s["ms"] else None
+            elif name in ("emb_a2a", "grad_a2a", "key_a2a"):
+                e["nvlink_gbs"] = s["bytes"] / (s["ms"] * 1e6) if s["ms"] else None
+            else:
+                gbs = s["bytes"] / (s["ms"] * 1e6) if s["ms"] else None
+                e["hbm_gbs"] = gbs
+                e["frac_of_measured_hbm"] = gbs / hbm_peak if gbs else None
+            stages[name] = e
+        hbm_stages = ["route", "sort", "owner_dedup", "gather", "refresh", "send_gather", "pool", "segsum", "update"]
+        dom = max((n for n in hbm_stages if n in stages), key=lambda n: st[n]["ms"])
+        ds = st[dom]
+        achieved = ds["bytes"] / (ds["ms"] * 1e6)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            key = f"{cfg.name}/W{world}/N{N}/{dom}"
+            if key in tj:
+                traffic = tj[key]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": src,
+                    "bytes_per_launch": ds["bytes"] / ds["records"], "ms_per_launch": ds["ms"] / ds["records"]}
+        summ = prof["summary"]
+        a2a = None
+        if world > 1:
+            a2a_bytes = st["emb_a2a"]["bytes"] + st["grad_a2a"]["bytes"]
+            a2a_ms = summ["a2a_ms"]
+            a2a = {"physical_ms_per_step": a2a_ms / steps,
+                   "exposed_ms_per_step": summ["a2a_exposed_ms"] / steps,
+                   "exposed_ratio": summ["a2a_exposed_ms"] / a2a_ms if a2a_ms else None,
+                   "nvlink_gbs_per_gpu": a2a_bytes / (a2a_ms * 1e6) if a2a_ms else None,
+                   "frac_of_peer_770": (a2a_bytes / (a2a_ms * 1e6)) / NVLINK_PEER_GBS if a2a_ms else None,
+                   "frac_of_nominal_900": (a2a_bytes / (a2a_ms * 1e6)) / NVLINK_NOMINAL_GBS if a2a_ms else None,
+                   "without_fwp": no_fwp}
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg, args.seed)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_json(args, cfg, world), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": int(summ["launches"]), "clocks": clk, "a2a": a2a,
+                "stages": stages,
+                "trace": {"span_ms_per_step": summ["span_ms"] / steps,
+                          "compute_busy_ms_per_step": summ["compute_busy_ms"] / steps}}
+        if args.trace:
+            json.dump({"stages": st, "summary": summ}, open(args.trace, "w"), indent=1)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

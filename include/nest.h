@@ -224,6 +224,37 @@ NEST_API nest_status_t nest_route_view(const nest_ctx_t* ctx, int32_t slot, nest
 NEST_API nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out,
                              void* stream);
 
+/* ---- tracing: CUDA events around every stage of the path ---- */
+enum { NEST_PROFILE_STAGES = 14 };
+typedef struct {
+  char name[24];        /* stage: schedule, route, sort, key_a2a, owner_dedup, gather, refresh,
+                           send_gather, emb_a2a, pool, tower, segsum, grad_a2a, update */
+  int32_t stream;       /* 0 compute, 1 comm, 2 aux */
+  int32_t records;      /* instrumented calls */
+  int32_t launches;     /* libnest kernels launched by those calls (NCCL / cuBLAS not counted) */
+  int32_t pad;
+  double ms;            /* summed event-measured durations */
+  double bytes;         /* summed algorithmic bytes; FLOPs for `tower`;
+                           off-GPU bytes for the All2All stages */
+} nest_profile_stage_t;
+
+typedef struct {
+  double span_ms;         /* first stage start to last stage end */
+  double a2a_ms;          /* summed durations of the embedding + gradient All2Alls */
+  double a2a_union_ms;    /* measure of the union of those intervals */
+  double a2a_exposed_ms;  /* All2All time not covered by any compute-stream stage */
+  double compute_busy_ms; /* measure of the union of compute-stream stages */
+  int64_t launches;       /* libnest kernels launched while tracing */
+} nest_profile_summary_t;
+
+/* on != 0: synchronize the device, drop old records and start tracing;
+ * on == 0: stop tracing (records are kept for nest_profile_read). */
+NEST_API nest_status_t nest_profile_enable(nest_ctx_t* ctx, int32_t on);
+/* Synchronizes the device and aggregates the records: stages[NEST_PROFILE_STAGES]
+ * (may be NULL) and the summary (may be NULL). */
+NEST_API nest_status_t nest_profile_read(nest_ctx_t* ctx, nest_profile_stage_t* stages,
+                                         nest_profile_summary_t* summary);
+
 /* Message of the last error of ctx (or of the last failed nest_create when ctx is NULL). */
 NEST_API const char* nest_last_error(const nest_ctx_t* ctx);
 

@@ -147,6 +147,19 @@ class NestContext:
                                             _stream(stream)))
         return out
 
+    def profile_enable(self, on: bool = True) -> None:
+        self._check(self.lib.nest_profile_enable(self.ctx, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        stages = (L.ProfileStage * L.PROFILE_STAGES)()
+        summ = L.ProfileSummary()
+        self._check(self.lib.nest_profile_read(self.ctx, stages, C.byref(summ)))
+        out = {"stages": {}, "summary": {k: getattr(summ, k) for k, _ in L.ProfileSummary._fields_}}
+        for s in stages:
+            out["stages"][s.name.decode()] = {"stream": s.stream, "records": s.records,
+                                              "launches": s.launches, "ms": s.ms, "bytes": s.bytes}
+        return out
+
     def route_view(self, slot: int) -> dict:
         """Copies of a slot's routing results (host numpy) for parity checks."""
         torch = self.torch

@@ -23,7 +23,9 @@ MAX_MICRO_BATCHES = 8
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
            "nest_create", "nest_destroy", "nest_init_tables", "nest_fwp_schedule", "nest_route",
            "nest_dbp_refresh", "nest_lookup_fwd", "nest_grad_bwd_update", "nest_tower_fwd_bwd",
-           "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_last_error"]
+           "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_profile_enable",
+           "nest_profile_read", "nest_last_error"]
+PROFILE_STAGES = 14
 
 
 class NestError(RuntimeError):
@@ -58,6 +60,16 @@ class RouteView(C.Structure):
                 ("n_owner", C.c_void_p), ("buffer", C.c_void_p)]
 
 
+class ProfileStage(C.Structure):
+    _fields_ = [("name", C.c_char * 24), ("stream", C.c_int32), ("records", C.c_int32),
+                ("launches", C.c_int32), ("pad", C.c_int32), ("ms", C.c_double), ("bytes", C.c_double)]
+
+
+class ProfileSummary(C.Structure):
+    _fields_ = [("span_ms", C.c_double), ("a2a_ms", C.c_double), ("a2a_union_ms", C.c_double),
+                ("a2a_exposed_ms", C.c_double), ("compute_busy_ms", C.c_double), ("launches", C.c_int64)]
+
+
 _lib = None
 
 
@@ -88,6 +100,8 @@ def load() -> C.CDLL:
         "nest_slot_info": ([vp, i32, C.POINTER(SlotInfo)], i32),
         "nest_route_view": ([vp, i32, C.POINTER(RouteView)], i32),
         "nest_read_rows": ([vp, vp, i64, vp, vp], i32),
+        "nest_profile_enable": ([vp, i32], i32),
+        "nest_profile_read": ([vp, C.POINTER(ProfileStage), C.POINTER(ProfileSummary)], i32),
         "nest_last_error": ([vp], C.c_char_p),
     }
     for name, (args, res) in sig.items():

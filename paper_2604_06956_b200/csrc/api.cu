@@ -291,6 +291,7 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   cudaDeviceSynchronize();
   if (c->tower) tower_destroy(*c);
+  profile_destroy(*c);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
   for (auto& s : c->slot) {
@@ -325,6 +326,7 @@ nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int3
     NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || mode == NEST_SCHED_CLUSTERED, NEST_ERR_INVALID, "bad mode");
     NEST_CHECK(perm_out && mb_offsets_out, NEST_ERR_INVALID, "null output");
     NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || (keys && bag_offsets), NEST_ERR_INVALID, "null batch");
+    ProfScope ps(*c, ST_SCHEDULE, SK_AUX, S(stream));
     launch_schedule(*c, keys, bag_offsets, B, N, mode, perm_out, mb_offsets_out, S(stream));
   });
 }
@@ -349,9 +351,13 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
     // its write-back done before this gather reads the shard (reading Q8)
     NEST_CUDA(cudaStreamWaitEvent(st, s.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, s.ev_free, 0));
+    int pid = prof_begin(*c, ST_ROUTE, SK_AUX, st);
     route_phase_a(*c, s, keys, bag_offsets, nnz, B, perm, N, st);
+    prof_end(*c, pid, st, 0.0, nullptr, 0.0, c->cfg.pooling == NEST_POOL_SUM ? 12 : 15);
     NEST_CUDA(cudaEventSynchronize(s.ev_sync));  // the one host sync (All2All sizes)
     route_phase_b(*c, s, st);
+    // 12 K + 8 U_s (keys + inverse + uniq)
+    prof_add_bytes(*c, pid, 12.0 * double(s.info.nnz) + 8.0 * double(s.info.uniq));
     NEST_CUDA(cudaEventRecord(s.ev_gather, st));
     s.routed = true;
     s.updated = false;
@@ -370,7 +376,12 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
     cudaStream_t st = S(stream);
     NEST_CUDA(cudaStreamWaitEvent(st, a.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, p.ev_gather, 0));
+    ProfScope ps(*c, ST_REFRESH, SK_COMPUTE, st);
     launch_refresh(*c, a, p, st);
+    // 8 (U_o + U_o') key reads + 2 I rows (I counted on the device)
+    ps.bytes = 8.0 * double(std::min(a.info.recv, c->Uocap) + std::min(p.info.recv, c->Uocap));
+    ps.dcount = c->n_refreshed;
+    ps.bpc = 2.0 * c->D * sizeof(float);
     NEST_CUDA(cudaEventRecord(a.ev_free, st));
   });
 }
@@ -394,20 +405,38 @@ nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* 
         NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_ready, 0));
         NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_gather, 0));
       }
-      launch_send_gather(*c, s, mb, ms);
+      const double row = double(c->D) * sizeof(float);
+      {
+        ProfScope ps(*c, ST_SEND_GATHER, SK_COMM, ms);
+        launch_send_gather(*c, s, mb, ms);
+        // R_{o,i} buffer rows read + R_{o,i} rows written + 12 B of indices per received key
+        ps.bytes = 2.0 * row * double(s.info.mb_recv[mb]) + 12.0 * double(s.info.recv);
+      }
       std::vector<int64_t> scnt(c->W), rcnt(c->W);
       const int Nc = c->Nmax + 2;
       for (int p = 0; p < c->W; ++p) {
         scnt[p] = s.all[(size_t(p) * c->W + c->rank) * Nc + 1 + mb];  // owner -> requester p
         rcnt[p] = s.all[(size_t(c->rank) * c->W + p) * Nc + 1 + mb];  // from owner p
       }
-      a2a_rows(*c, c->own_rows + s.own_base[mb] * c->D, scnt, c->src_rows + s.src_base[mb] * c->D, rcnt, ms);
+      {
+        ProfScope ps(*c, ST_EMB_A2A, SK_COMM, ms);
+        a2a_rows(*c, c->own_rows + s.own_base[mb] * c->D, scnt, c->src_rows + s.src_base[mb] * c->D, rcnt, ms);
+        ps.launches = 0;
+        ps.bytes = row * double(s.info.mb_recv[mb] - scnt[c->rank]);  // rows sent off-GPU
+      }
       NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_emb[mb], 0));
     } else if (mb == 0) {
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));
     }
+    ProfScope ps(*c, ST_POOL, SK_COMPUTE, cs);
     launch_pool(*c, s, mb, out, cs);
+    {
+      // U_{s,i} rows + 4 K_i + output rows
+      const double row = double(c->D) * sizeof(float);
+      ps.bytes = row * double(s.info.mb_uniq[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
+                 row * double(s.info.mb_out_rows[mb]);
+    }
   });
 }
 
@@ -422,7 +451,18 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
     NEST_CHECK(dout != nullptr || s.info.mb_out_rows[mb] == 0, NEST_ERR_INVALID, "null dout");
     cudaStream_t cs = S(compute), ms = S(comm);
     Slot& other = c->slot[1 - slot];
-    launch_segsum(*c, s, mb, dout, cs);
+    const double row = double(c->D) * sizeof(float);
+    {
+      ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
+      launch_segsum(*c, s, mb, dout, cs);
+      ps.launches = s.info.mb_uniq[mb] > 0 ? 7 : 0;
+      // gradient rows read + 4 K_i + U_{s,i} rows written
+      ps.bytes = row * double(s.info.mb_out_rows[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
+                 row * double(s.info.mb_uniq[mb]);
+    }
+    // sum_i R_{o,i} gradient rows + 3 U_o rows (buffer r/w + shard write)
+    double upd_fixed = 0;
+    for (int i = 0; i < s.N; ++i) upd_fixed += row * double(c->W > 1 ? s.info.mb_recv[i] : s.info.mb_uniq[i]);
     if (c->W > 1) {
       NEST_CUDA(cudaEventRecord(s.ev_grad[mb], cs));
       NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_grad[mb], 0));
@@ -432,16 +472,33 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
         scnt[p] = s.all[(size_t(c->rank) * c->W + p) * Nc + 1 + mb];  // requester -> owner p
         rcnt[p] = s.all[(size_t(p) * c->W + c->rank) * Nc + 1 + mb];  // from requester p
       }
-      a2a_rows(*c, c->src_rows + s.src_base[mb] * c->D, scnt, c->own_rows + s.own_base[mb] * c->D, rcnt, ms);
+      {
+        ProfScope ps(*c, ST_GRAD_A2A, SK_COMM, ms);
+        a2a_rows(*c, c->src_rows + s.src_base[mb] * c->D, scnt, c->own_rows + s.own_base[mb] * c->D, rcnt, ms);
+        ps.launches = 0;
+        ps.bytes = row * double(s.info.mb_uniq[mb] - scnt[c->rank]);  // rows sent off-GPU
+      }
       if (mb == s.N - 1) {
         NEST_CUDA(cudaStreamWaitEvent(ms, other.ev_gather, 0));
-        launch_reduce_sgd(*c, s, lr_over_B, ms);
+        {
+          ProfScope ps(*c, ST_UPDATE, SK_COMM, ms);
+          launch_reduce_sgd(*c, s, lr_over_B, ms);
+          ps.bytes = upd_fixed;
+          ps.dcount = s.n_owner;
+          ps.bpc = 3.0 * row;
+        }
         NEST_CUDA(cudaEventRecord(s.ev_update, ms));
         NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
       }
     } else if (mb == s.N - 1) {
       NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
-      launch_reduce_sgd(*c, s, lr_over_B, cs);
+      {
+        ProfScope ps(*c, ST_UPDATE, SK_COMPUTE, cs);
+        launch_reduce_sgd(*c, s, lr_over_B, cs);
+        ps.bytes = upd_fixed;
+        ps.dcount = s.n_owner;
+        ps.bpc = 3.0 * row;
+      }
       NEST_CUDA(cudaEventRecord(s.ev_update, cs));
     }
     if (mb == s.N - 1) s.updated = true;
@@ -455,7 +512,12 @@ nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t r
   return guard(c, [&] {
     NEST_CHECK(c->tower != nullptr, NEST_ERR_INVALID, "tower_layers == 0");
     NEST_CHECK(rows % c->F == 0, NEST_ERR_INVALID, "rows must be a multiple of F");
+    ProfScope ps(*c, ST_TOWER, SK_COMPUTE, S(stream));
     tower_run(*c, pooled, rows, dout, S(stream));
+    const double M = double(rows / c->F), in0 = double(c->F) * c->D, H = c->cfg.tower_hidden;
+    const int L = c->cfg.tower_layers;
+    ps.bytes = 3.0 * 2.0 * M * (in0 * H + double(L - 1) * H * H);  // FLOPs (fwd + dW + dX)
+    ps.launches = 1;  // the cast kernel (the GEMMs are cuBLAS)
   });
 }
 
@@ -492,6 +554,19 @@ nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, fl
     NEST_CHECK(n >= 0 && (n == 0 || (keys && out)), NEST_ERR_INVALID, "bad arguments");
     launch_read_rows(*c, keys, n, out, S(stream));
   });
+}
+
+nest_status_t nest_profile_enable(nest_ctx_t* ctx, int32_t on) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { profile_enable(*c, on != 0); });
+}
+
+nest_status_t nest_profile_read(nest_ctx_t* ctx, nest_profile_stage_t* stages,
+                                nest_profile_summary_t* summary) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { profile_read(*c, stages, summary); });
 }
 
 const char* nest_last_error(const nest_ctx_t* ctx) {

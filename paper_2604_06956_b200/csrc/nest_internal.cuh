@@ -97,8 +97,40 @@ struct Slot {
               ev_grad[NEST_MAX_MICRO_BATCHES] = {}, ev_ready = nullptr, ev_sync = nullptr;
 };
 
+// ----------------------------------------------------------------------------
+// tracing: CUDA events around every stage (SURVEY §5 tracing), read back by
+// nest_profile_read; stage bytes are the algorithmic bytes of SURVEY §8(d)
+// ----------------------------------------------------------------------------
+enum Stage : int {
+  ST_SCHEDULE = 0, ST_ROUTE, ST_SORT, ST_KEY_A2A, ST_OWNER_DEDUP, ST_GATHER, ST_REFRESH,
+  ST_SEND_GATHER, ST_EMB_A2A, ST_POOL, ST_TOWER, ST_SEGSUM, ST_GRAD_A2A, ST_UPDATE, ST_COUNT
+};
+enum StreamKind : int { SK_COMPUTE = 0, SK_COMM = 1, SK_AUX = 2 };
+
+struct ProfRec {
+  int stage, kind;
+  cudaEvent_t e0, e1;
+  double bytes;          // fixed part of the algorithmic bytes
+  int cidx;              // index into the pinned device-count ring (-1: none)
+  double bytes_per_cnt;  // bytes per unit of that device count
+  int launches;
+};
+
+struct Profiler {
+  bool on = false;
+  cudaEvent_t ref = nullptr;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t next_ev = 0;
+  int32_t* hcnt = nullptr;   // pinned ring of device counts copied at record time
+  int ncnt = 0, cap_cnt = 1 << 16;
+  int64_t launches = 0;      // kernels launched while on
+  cudaStream_t ref_stream = nullptr;
+};
+
 struct Ctx {
   nest_config_t cfg{};
+  Profiler prof;
   std::vector<int64_t> rows;       // [T]
   int W = 1, rank = 0, T = 0, D = 0, F = 1, Nmax = 1;
   int64_t Kcap = 0, Bcap = 0, Rcap = 0, Uocap = 0, MBcap = 0, OMBcap = 0, Pcap = 0;
@@ -386,6 +418,24 @@ void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st);
 void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int B, int N, int mode,
                      int32_t* perm, int32_t* mb_offsets, cudaStream_t st);
+// tracing hooks (api.cu); cheap no-ops unless profiling is on
+int prof_begin(Ctx& c, int stage, int kind, cudaStream_t st);
+void prof_end(Ctx& c, int id, cudaStream_t st, double bytes, const int32_t* dcount = nullptr,
+              double bytes_per_cnt = 0.0, int launches = 1) noexcept;
+void prof_add_bytes(Ctx& c, int id, double bytes) noexcept;
+void profile_enable(Ctx& c, bool on);
+void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* sum);
+void profile_destroy(Ctx& c);
+struct ProfScope {
+  Ctx& c;
+  int id;
+  cudaStream_t st;
+  double bytes = 0, bpc = 0;
+  const int32_t* dcount = nullptr;
+  int launches = 1;
+  ProfScope(Ctx& cc, int stage, int kind, cudaStream_t s) : c(cc), id(prof_begin(cc, stage, kind, s)), st(s) {}
+  ~ProfScope() { prof_end(c, id, st, bytes, dcount, bpc, launches); }
+};
 void tower_create(Ctx& c);
 void tower_destroy(Ctx& c);
 void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st);

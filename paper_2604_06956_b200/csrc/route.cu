@@ -560,55 +560,78 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
   for (int r = 0; r < W; ++r) s.key_roff[r + 1] = s.key_roff[r] + A(r, c.rank, 0);
 
   // ---- R1 tail: per micro-batch positions among its keys, sorted occurrences ----
-  for (int i = 0; i < N; ++i) {
-    const uint32_t* mk = s.mask;
-    int32_t* pos = s.pos + int64_t(i) * (c.Kcap + 1);
-    scan_exclusive<int32_t>([=] __device__(int64_t u) { return int32_t((mk[u] >> i) & 1u); }, U,
-                            [=] __device__(int64_t u, int32_t v) { pos[u] = v; }, c.scan_tmp, st);
-  }
   int mbbits = 0;
   while ((1 << mbbits) < N) ++mbbits;
-  radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, s.ubits + mbbits, st);
+  {
+    ProfScope ps(c, ST_SORT, SK_AUX, st);
+    for (int i = 0; i < N; ++i) {
+      const uint32_t* mk = s.mask;
+      int32_t* pos = s.pos + int64_t(i) * (c.Kcap + 1);
+      scan_exclusive<int32_t>([=] __device__(int64_t u) { return int32_t((mk[u] >> i) & 1u); }, U,
+                              [=] __device__(int64_t u, int32_t v) { pos[u] = v; }, c.scan_tmp, st);
+    }
+    radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, s.ubits + mbbits, st);
+    const int passes = (s.ubits + mbbits) <= 8 ? 1 : (s.ubits + mbbits + 7) / 8;
+    ps.launches = 3 * N + (nnz > 0 ? 5 * passes : 0);
+    // pos scans read masks + write N positions; every pass reads + writes (key, value)
+    ps.bytes = double(U) * 4 * (1 + N) + double(nnz) * 16 * passes;
+  }
 
   if (W == 1) {
     // owner == source: the owner-unique keys are the unique keys
     s.n_owner = s.off + 1;
   } else {
-    // ---- R2: key All2All (key | mask << 56), grouped send/recv ----
-    k_pack<<<grid_for(c.Kcap, 256, 148 * 8), 256, 0, st>>>(s.off + W, s.uniq, s.mask, c.packed);
-    NEST_LAUNCH_CHECK();
-    NEST_NCCL(ncclGroupStart());
-    for (int p = 0; p < W; ++p) {
-      NEST_NCCL(ncclSend(c.packed + s.key_soff[p], size_t(s.key_soff[p + 1] - s.key_soff[p]), ncclInt64,
-                         p, c.comm_aux, st));
-      NEST_NCCL(ncclRecv(s.recv + s.key_roff[p], size_t(s.key_roff[p + 1] - s.key_roff[p]), ncclInt64,
-                         p, c.comm_aux, st));
+    {
+      // ---- R2: key All2All (key | mask << 56), grouped send/recv ----
+      ProfScope ps(c, ST_KEY_A2A, SK_AUX, st);
+      k_pack<<<grid_for(c.Kcap, 256, 148 * 8), 256, 0, st>>>(s.off + W, s.uniq, s.mask, c.packed);
+      NEST_LAUNCH_CHECK();
+      NEST_NCCL(ncclGroupStart());
+      for (int p = 0; p < W; ++p) {
+        NEST_NCCL(ncclSend(c.packed + s.key_soff[p], size_t(s.key_soff[p + 1] - s.key_soff[p]), ncclInt64,
+                           p, c.comm_aux, st));
+        NEST_NCCL(ncclRecv(s.recv + s.key_roff[p], size_t(s.key_roff[p + 1] - s.key_roff[p]), ncclInt64,
+                           p, c.comm_aux, st));
+      }
+      NEST_NCCL(ncclGroupEnd());
+      ps.bytes = 8.0 * double(U - (s.key_soff[c.rank + 1] - s.key_soff[c.rank]));  // off-GPU
     }
-    NEST_NCCL(ncclGroupEnd());
-    // ---- R3: owner dedup on the local domain ----
-    NEST_CUDA(cudaMemsetAsync(s.obm, 0, sizeof(uint32_t) * (c.owords + 2), st));
-    if (R > 0)
-      k_owner_mark<<<grid_for(R, 256), 256, 0, st>>>(R, s.recv, c.T, W, c.rank, c.d_rows, c.d_lbase,
-                                                     c.r_ldom, s.obm, c.d_err);
-    popc_scan(c, s.obm, s.owr, c.owords + 1, s.n_owner, st);
-    k_owner_emit<<<grid_for(c.owords + 1, 256), 256, 0, st>>>(c.owords + 1, s.obm, s.owr, W,
-                                                              s.owner_rows, s.src_tab);
-    Offs64 roff{};
-    for (int r = 0; r <= W; ++r) roff.v[r] = int32_t(s.key_roff[r]);
-    if (R > 0)
-      k_owner_inv<<<grid_for(R, 256), 256, 0, st>>>(R, c.r_ldom, s.obm, s.owr, W, roff, s.owner_inv,
-                                                    s.src_tab);
-    NEST_LAUNCH_CHECK();
-    for (int i = 0; i < N; ++i) {
-      const int64_t* rk = s.recv;
-      int32_t* sp = s.sendpos + int64_t(i) * (c.Rcap + 1);
-      scan_exclusive<int32_t>(
-          [=] __device__(int64_t r) { return int32_t((uint64_t(rk[r]) >> (56 + i)) & 1u); }, R,
-          [=] __device__(int64_t r, int32_t v) { sp[r] = v; }, c.scan_tmp, st);
+    {
+      // ---- R3: owner dedup on the local domain ----
+      ProfScope ps(c, ST_OWNER_DEDUP, SK_AUX, st);
+      NEST_CUDA(cudaMemsetAsync(s.obm, 0, sizeof(uint32_t) * (c.owords + 2), st));
+      if (R > 0)
+        k_owner_mark<<<grid_for(R, 256), 256, 0, st>>>(R, s.recv, c.T, W, c.rank, c.d_rows, c.d_lbase,
+                                                       c.r_ldom, s.obm, c.d_err);
+      popc_scan(c, s.obm, s.owr, c.owords + 1, s.n_owner, st);
+      k_owner_emit<<<grid_for(c.owords + 1, 256), 256, 0, st>>>(c.owords + 1, s.obm, s.owr, W,
+                                                                s.owner_rows, s.src_tab);
+      Offs64 roff{};
+      for (int r = 0; r <= W; ++r) roff.v[r] = int32_t(s.key_roff[r]);
+      if (R > 0)
+        k_owner_inv<<<grid_for(R, 256), 256, 0, st>>>(R, c.r_ldom, s.obm, s.owr, W, roff, s.owner_inv,
+                                                      s.src_tab);
+      NEST_LAUNCH_CHECK();
+      for (int i = 0; i < N; ++i) {
+        const int64_t* rk = s.recv;
+        int32_t* sp = s.sendpos + int64_t(i) * (c.Rcap + 1);
+        scan_exclusive<int32_t>(
+            [=] __device__(int64_t r) { return int32_t((uint64_t(rk[r]) >> (56 + i)) & 1u); }, R,
+            [=] __device__(int64_t r, int32_t v) { sp[r] = v; }, c.scan_tmp, st);
+      }
+      ps.launches = 2 * (R > 0) + 3 + 1 + 3 * N;
+      ps.bytes = 12.0 * double(R);  // 12 R_o + 8 U_o
+      ps.dcount = s.n_owner;
+      ps.bpc = 8.0;
     }
   }
-  // ---- R4: gather the owned rows from the shard into the slot buffer ----
-  launch_gather(c, s, st);
+  {
+    // ---- R4: gather the owned rows from the shard into the slot buffer ----
+    ProfScope ps(c, ST_GATHER, SK_AUX, st);
+    launch_gather(c, s, st);
+    ps.dcount = s.n_owner;
+    ps.bpc = 2.0 * c.D * sizeof(float);  // 2 U_o row
+  }
   (void)D;
 }
 
