@@ -224,6 +224,25 @@ NEST_API nest_status_t nest_route_view(const nest_ctx_t* ctx, int32_t slot, nest
 NEST_API nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out,
                              void* stream);
 
+/* All2All plan of one batch, as nest_route derives it after the count
+ * exchange (host-only; exposed so the multi-rank bookkeeping can be tested
+ * without GPUs).  all_counts: host int32 [W][W][max_micro_batches+2]:
+ * all_counts[s][o] = {keys source s sends to owner o, the same per
+ * micro-batch 1..N, error flags}.  Returns the same error / capacity decision
+ * nest_route takes (identical on every rank). */
+typedef struct {
+  int64_t uniq;                                 /* U_s of cfg->rank */
+  int64_t recv;                                 /* R_o of cfg->rank */
+  int64_t key_send_off[NEST_MAX_WORLD + 1];     /* key All2All send displacements */
+  int64_t key_recv_off[NEST_MAX_WORLD + 1];     /* key All2All receive displacements */
+  int64_t mb_uniq[NEST_MAX_MICRO_BATCHES];      /* rows received per micro-batch */
+  int64_t mb_recv[NEST_MAX_MICRO_BATCHES];      /* rows sent as owner per micro-batch */
+  int64_t src_base[NEST_MAX_MICRO_BATCHES + 1]; /* row base of micro-batch i (requester side) */
+  int64_t own_base[NEST_MAX_MICRO_BATCHES + 1]; /* row base of micro-batch i (owner side) */
+} nest_exchange_plan_t;
+NEST_API nest_status_t nest_exchange_plan(const nest_config_t* cfg, int32_t N,
+                                          const int32_t* all_counts, nest_exchange_plan_t* plan);
+
 /* ---- tracing: CUDA events around every stage of the path ---- */
 enum { NEST_PROFILE_STAGES = 14 };
 typedef struct {

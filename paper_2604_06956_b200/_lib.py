@@ -23,7 +23,7 @@ MAX_MICRO_BATCHES = 8
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
            "nest_create", "nest_destroy", "nest_init_tables", "nest_fwp_schedule", "nest_route",
            "nest_dbp_refresh", "nest_lookup_fwd", "nest_grad_bwd_update", "nest_tower_fwd_bwd",
-           "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_profile_enable",
+           "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
            "nest_profile_read", "nest_last_error"]
 PROFILE_STAGES = 14
 
@@ -58,6 +58,17 @@ class RouteView(C.Structure):
                 ("pos", C.c_void_p), ("send_counts", C.c_void_p), ("all_counts", C.c_void_p),
                 ("recv_keys", C.c_void_p), ("owner_rows", C.c_void_p), ("owner_inv", C.c_void_p),
                 ("n_owner", C.c_void_p), ("buffer", C.c_void_p)]
+
+
+MAX_WORLD = 64
+
+
+class ExchangePlan(C.Structure):
+    _fields_ = [("uniq", C.c_int64), ("recv", C.c_int64),
+                ("key_send_off", C.c_int64 * (MAX_WORLD + 1)), ("key_recv_off", C.c_int64 * (MAX_WORLD + 1)),
+                ("mb_uniq", C.c_int64 * MAX_MICRO_BATCHES), ("mb_recv", C.c_int64 * MAX_MICRO_BATCHES),
+                ("src_base", C.c_int64 * (MAX_MICRO_BATCHES + 1)),
+                ("own_base", C.c_int64 * (MAX_MICRO_BATCHES + 1))]
 
 
 class ProfileStage(C.Structure):
@@ -100,6 +111,7 @@ def load() -> C.CDLL:
         "nest_slot_info": ([vp, i32, C.POINTER(SlotInfo)], i32),
         "nest_route_view": ([vp, i32, C.POINTER(RouteView)], i32),
         "nest_read_rows": ([vp, vp, i64, vp, vp], i32),
+        "nest_exchange_plan": ([C.POINTER(Config), i32, vp, C.POINTER(ExchangePlan)], i32),
         "nest_profile_enable": ([vp, i32], i32),
         "nest_profile_read": ([vp, C.POINTER(ProfileStage), C.POINTER(ProfileSummary)], i32),
         "nest_last_error": ([vp], C.c_char_p),

@@ -273,8 +273,14 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       ncclUniqueId id0, id1;
       std::memcpy(&id0, nccl_uids, sizeof(id0));
       std::memcpy(&id1, reinterpret_cast<const char*>(nccl_uids) + sizeof(id0), sizeof(id1));
-      NEST_NCCL(ncclCommInitRank(&c->comm, c->W, id0, c->rank));
-      NEST_NCCL(ncclCommInitRank(&c->comm_aux, c->W, id1, c->rank));
+      // bound NCCL's CTAs so the All2Alls leave SMs to the overlapped compute
+      // (SURVEY H3); NEST_NCCL_MAX_CTAS overrides
+      ncclConfig_t cfg0 = NCCL_CONFIG_INITIALIZER, cfg1 = NCCL_CONFIG_INITIALIZER;
+      const char* mc = std::getenv("NEST_NCCL_MAX_CTAS");
+      cfg0.maxCTAs = mc ? std::atoi(mc) : 16;
+      cfg1.maxCTAs = mc ? std::atoi(mc) : 8;
+      NEST_NCCL(ncclCommInitRankConfig(&c->comm, c->W, id0, c->rank, &cfg0));
+      NEST_NCCL(ncclCommInitRankConfig(&c->comm_aux, c->W, id1, c->rank, &cfg1));
     }
     if (c->cfg.tower_layers > 0) tower_create(*c);
   });
@@ -553,6 +559,16 @@ nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, fl
   return guard(c, [&] {
     NEST_CHECK(n >= 0 && (n == 0 || (keys && out)), NEST_ERR_INVALID, "bad arguments");
     launch_read_rows(*c, keys, n, out, S(stream));
+  });
+}
+
+nest_status_t nest_exchange_plan(const nest_config_t* cfg, int32_t N, const int32_t* all_counts,
+                                 nest_exchange_plan_t* plan) {
+  return guard(nullptr, [&] {
+    NEST_CHECK(all_counts && plan, NEST_ERR_INVALID, "null argument");
+    Ctx c;
+    derive(c, cfg);
+    exchange_plan(c, N, all_counts, *plan);
   });
 }
 

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -408,6 +409,7 @@ void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t*
 void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz,
                    int B, const int32_t* perm, int N, cudaStream_t st);
 void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
+void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p);
 void launch_init_tables(Ctx& c, cudaStream_t st);
 void launch_gather(Ctx& c, Slot& s, cudaStream_t st);
 void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st);

@@ -497,25 +497,23 @@ void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offs
   NEST_CUDA(cudaEventRecord(s.ev_sync, st));
 }
 
-// after the host sync: plan from the counts, then R1 tail, R2 keys, R3, R4
-void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
-  const int W = c.W, N = s.N, Nc = c.Nmax + 2, D = c.D;
-  // ---- host plan ----
-  s.all.assign(size_t(W) * W * Nc, 0);
-  for (size_t i = 0; i < s.all.size(); ++i) s.all[i] = s.h_xfer[i];
-  const int32_t* hmbnnz = s.h_xfer + int64_t(W) * W * Nc;
-  auto A = [&](int src, int own, int col) { return s.all[(size_t(src) * W + own) * Nc + col]; };
+// The All2All plan of one batch from the gathered counts (pure host; every
+// rank sees every rank's counts and error flags, so all ranks take the same
+// error / capacity decision).  all: [W][W][Nmax+2], all[s][o] = what source s
+// sends to owner o: {U, U_1..U_N, err}.
+void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p) {
+  const int W = c.W, Nc = c.Nmax + 2;
+  NEST_CHECK(N >= 1 && N <= c.Nmax, NEST_ERR_INVALID, "N out of range");
+  auto A = [&](int src, int own, int col) { return int64_t(all[(size_t(src) * W + own) * Nc + col]); };
   int32_t err = 0;
   for (int r = 0; r < W; ++r)
-    for (int o = 0; o < W; ++o) err |= int32_t(A(r, o, Nc - 1));
-  err |= s.h_xfer[int64_t(W) * W * Nc + c.Nmax];
+    for (int o = 0; o < W; ++o) {
+      err |= int32_t(A(r, o, Nc - 1));
+      for (int col = 0; col <= N; ++col)
+        NEST_CHECK(A(r, o, col) >= 0, NEST_ERR_INVALID, "negative count");
+    }
   if (err & kErrKeyRange) throw Error{NEST_ERR_KEY_RANGE, "key out of range (table >= T or row >= rows[table])"};
   if (err & kErrShard) throw Error{NEST_ERR_SHARD, "owner received a key it does not own"};
-  nest_slot_info_t& info = s.info;
-  info = nest_slot_info_t{};
-  info.num_micro_batches = N;
-  info.batch = s.B;
-  // capacity checks for EVERY rank (all ranks take the same decision)
   for (int r = 0; r < W; ++r) {
     int64_t recv = 0, mbrows = 0, mbrecv = 0;
     for (int o = 0; o < W; ++o) {
@@ -529,35 +527,57 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     if (mbrows > c.MBcap) throw Error{NEST_ERR_CAPACITY, "micro-batch rows exceed max_mb_rows"};
     if (mbrecv > c.OMBcap) throw Error{NEST_ERR_CAPACITY, "owner micro-batch rows exceed max_owner_mb_rows"};
   }
-  int64_t U = 0, R = 0;
-  for (int o = 0; o < W; ++o) U += A(c.rank, o, 0);
-  for (int r = 0; r < W; ++r) R += A(r, c.rank, 0);
-  info.uniq = U;
-  info.recv = R;
-  s.src_base.assign(N + 1, 0);
-  s.own_base.assign(N + 1, 0);
-  s.q0.assign(N + 1, 0);
-  int64_t nnz = 0;
+  p = nest_exchange_plan_t{};
+  for (int o = 0; o < W; ++o) p.key_send_off[o + 1] = p.key_send_off[o] + A(c.rank, o, 0);
+  for (int r = 0; r < W; ++r) p.key_recv_off[r + 1] = p.key_recv_off[r] + A(r, c.rank, 0);
+  p.uniq = p.key_send_off[W];
+  p.recv = p.key_recv_off[W];
   for (int i = 0; i < N; ++i) {
     int64_t ui = 0, ri = 0;
     for (int o = 0; o < W; ++o) {
       ui += A(c.rank, o, 1 + i);
       ri += A(o, c.rank, 1 + i);
     }
-    info.mb_uniq[i] = ui;
-    info.mb_recv[i] = ri;
+    p.mb_uniq[i] = ui;
+    p.mb_recv[i] = ri;
+    p.src_base[i + 1] = p.src_base[i] + ui;
+    p.own_base[i + 1] = p.own_base[i] + ri;
+  }
+}
+
+// after the host sync: plan from the counts, then R1 tail, R2 keys, R3, R4
+void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
+  const int W = c.W, N = s.N, Nc = c.Nmax + 2, D = c.D;
+  // ---- host plan ----
+  s.all.assign(size_t(W) * W * Nc, 0);
+  for (size_t i = 0; i < s.all.size(); ++i) s.all[i] = s.h_xfer[i];
+  const int32_t* hmbnnz = s.h_xfer + int64_t(W) * W * Nc;
+  if (s.h_xfer[int64_t(W) * W * Nc + c.Nmax] & kErrKeyRange)
+    throw Error{NEST_ERR_KEY_RANGE, "key out of range (table >= T or row >= rows[table])"};
+  nest_exchange_plan_t plan;
+  exchange_plan(c, N, s.h_xfer, plan);
+  nest_slot_info_t& info = s.info;
+  info = nest_slot_info_t{};
+  info.num_micro_batches = N;
+  info.batch = s.B;
+  const int64_t U = plan.uniq, R = plan.recv;
+  info.uniq = U;
+  info.recv = R;
+  s.src_base.assign(plan.src_base, plan.src_base + N + 1);
+  s.own_base.assign(plan.own_base, plan.own_base + N + 1);
+  s.q0.assign(N + 1, 0);
+  int64_t nnz = 0;
+  for (int i = 0; i < N; ++i) {
+    info.mb_uniq[i] = plan.mb_uniq[i];
+    info.mb_recv[i] = plan.mb_recv[i];
     info.mb_nnz[i] = hmbnnz[i];
     info.mb_out_rows[i] = c.cfg.pooling == NEST_POOL_SUM ? int64_t(s.cap) * c.F : hmbnnz[i];
-    s.src_base[i + 1] = s.src_base[i] + ui;
-    s.own_base[i + 1] = s.own_base[i] + ri;
     s.q0[i + 1] = s.q0[i] + hmbnnz[i];
     nnz += hmbnnz[i];
   }
   info.nnz = nnz;
-  s.key_soff.assign(W + 1, 0);
-  s.key_roff.assign(W + 1, 0);
-  for (int o = 0; o < W; ++o) s.key_soff[o + 1] = s.key_soff[o] + A(c.rank, o, 0);
-  for (int r = 0; r < W; ++r) s.key_roff[r + 1] = s.key_roff[r] + A(r, c.rank, 0);
+  s.key_soff.assign(plan.key_send_off, plan.key_send_off + W + 1);
+  s.key_roff.assign(plan.key_recv_off, plan.key_recv_off + W + 1);
 
   // ---- R1 tail: per micro-batch positions among its keys, sorted occurrences ----
   int mbbits = 0;

@@ -32,7 +32,8 @@ class Runner:
         self.lr = lr_over_B
         dev = ctx.device
         self.compute = torch.cuda.Stream(device=dev)
-        self.comm = torch.cuda.Stream(device=dev) if ctx.world > 1 else self.compute
+        # comm stream at high priority: its CTAs are scheduled first as SMs free up
+        self.comm = torch.cuda.Stream(device=dev, priority=-1) if ctx.world > 1 else self.compute
         self.aux = torch.cuda.Stream(device=dev)
         self.t = 0
         self.primed = False

@@ -1,0 +1,136 @@
+"""Multi-GPU parity worker (launched by torchrun; see tests/test_gpu_multi.py).
+
+Every rank runs the pipelined DBP + FWP path through libnest.so with real NCCL
+All2Alls; rank 0 compares against the CPU oracle over the global batch:
+routing (uniq / inverse / masks / count exchange / received keys / owner rows)
+bit-exact, pooled rows and tables bit-exact in regime P1 and within 1e-5 in P2.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import workload as WL  # noqa: E402
+from oracle import cluster as OC  # noqa: E402
+from oracle import routing as OR  # noqa: E402
+from oracle import step as OS  # noqa: E402
+from paper_2604_06956_b200 import NestContext, unique_ids  # noqa: E402
+from paper_2604_06956_b200.runner import Runner  # noqa: E402
+
+
+def rel_ok(a, b, tol=1e-5):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.all(np.linalg.norm(a - b, axis=1) <= tol * np.maximum(np.linalg.norm(b, axis=1), 1e-30))
+
+
+def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids):
+    F, d = cfg.num_features, cfg.dim
+    batches = [[WL.gen_batch(cfg, 21, t, r, batch=B) for r in range(world)] for t in range(T)]
+    douts = [[WL.gen_dout(21, t, r, B * F, d, dmode) for r in range(world)] for t in range(T)]
+    K = max(len(b[rank][0]) for b in batches)
+    ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, max_keys=K, max_batch=B,
+                      max_micro_batches=N, seed=13, init_mode=init, nccl_uids=uids, device=dev)
+    run = Runner(ctx, N=N, pipelined=True, lr_over_B=lr)
+    mine = [(torch.from_numpy(b[rank][0]).to(dev), torch.from_numpy(b[rank][1]).to(dev), B) for b in batches]
+    cap = B // N
+    pooled = []
+    for t in range(T):
+        dd = torch.from_numpy(douts[t][rank]).to(dev)
+        outs = run.step(mine[t], mine[t + 1] if t + 1 < T else None,
+                        lambda tt, i, p, dd=dd: dd[i * cap * F:(i + 1) * cap * F])
+        torch.cuda.synchronize()
+        pooled.append(np.concatenate([o.cpu().numpy() for o in outs]))
+    # route view of the last batch
+    view = ctx.route_view((T - 1) % 2)
+    allk = np.unique(np.concatenate([b[r][0] for b in batches for r in range(world)]))
+    owned = allk[(allk & ((1 << 40) - 1)) % world == rank]
+    rows = ctx.read_rows(torch.from_numpy(owned).to(dev)).cpu().numpy()
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object((pooled, owned, rows, {k: v for k, v in view.items() if k != "info"}), gathered, dst=0)
+    ok = True
+    if rank == 0:
+        tab = OS.LazyTable(13, d, init)
+        for t in range(T):
+            res = OS.sync_step(tab, batches[t], douts[t], lr)
+            for r in range(world):
+                g = gathered[r][0][t]
+                good = np.array_equal(g, res.pooled[r]) if dmode == "dyadic" else rel_ok(g, res.pooled[r])
+                if not good:
+                    print(f"[{name}] pooled mismatch step {t} rank {r}", flush=True)
+                    ok = False
+        for r in range(world):
+            owned_r, rows_r = gathered[r][1], gathered[r][2]
+            ref = tab.get(owned_r)
+            good = np.array_equal(rows_r, ref) if dmode == "dyadic" else rel_ok(rows_r, ref)
+            if not good:
+                print(f"[{name}] table mismatch rank {r}", flush=True)
+                ok = False
+        # routing of the last batch, bit-exact
+        perm, mbo = OC.cluster_sequential(B, N)
+        mbs = [OR.mb_of_occurrence(batches[T - 1][r][1], F, perm, mbo) for r in range(world)]
+        src, own = OR.route_all(batches[T - 1], world, mbs, N)
+        Nc = N + 2
+        for r in range(world):
+            v = gathered[r][3]
+            checks = {
+                "uniq": np.array_equal(v["uniq"], src[r].uniq),
+                "inverse": np.array_equal(v["inverse"], src[r].inverse),
+                "mask": np.array_equal(v["mask"].astype(np.int64), src[r].mask),
+                "send_counts": np.array_equal(v["send_counts"][:, 0], src[r].send_counts)
+                and np.array_equal(v["send_counts"][:, 1:1 + N].T, src[r].mb_counts),
+                "recv_keys": np.array_equal(v["recv_keys"] & ((1 << 56) - 1), own[r].recv_keys)
+                and np.array_equal(v["recv_keys"] >> 56, own[r].recv_mask),
+                "owner_inv": np.array_equal(v["owner_inv"], own[r].owner_inv),
+            }
+            ok_keys = own[r].owner_keys
+            tabs, rws = ok_keys >> 40, ok_keys & ((1 << 40) - 1)
+            lb = np.concatenate([[0], np.cumsum([(rt - r + world - 1) // world for rt in cfg.table_rows])])
+            checks["owner_rows"] = np.array_equal(v["owner_rows"], lb[tabs] + rws // world)
+            for s in range(world):
+                checks[f"all_counts[{s}]"] = np.array_equal(v["all_counts"][s][:, 0], src[s].send_counts)
+            bad = [k for k, good in checks.items() if not good]
+            if bad:
+                print(f"[{name}] routing mismatch rank {r}: {bad}", flush=True)
+                ok = False
+        print(f"[{name}] {'OK' if ok else 'FAIL'}", flush=True)
+    ctx.close()
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.broadcast(flag, 0)
+    return bool(flag.item())
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cases = [
+        ("tiny-P1-N2", WL.CONFIGS["tiny"], 32, 2, 6, "dyadic", "dyadic", 2.0 ** -10),
+        ("tiny-P1-N1", WL.CONFIGS["tiny"], 32, 1, 4, "dyadic", "dyadic", 2.0 ** -10),
+        ("skew-P1-N4", WL.CONFIGS["tiny"].with_(table_rows=(3000, 40, 7, 999), zipf=1.4, bag_repeats=True,
+                                                 dim=128), 1024, 4, 3, "dyadic", "dyadic", 2.0 ** -12),
+        ("mid-P2-N4", WL.CONFIGS["tiny"].with_(table_rows=(20000, 5000, 333, 100000), zipf=1.1,
+                                                bag_repeats=True, dim=64), 2048, 4, 4, "uniform",
+         "realistic", 0.02),
+    ]
+    all_ok = True
+    for case in cases:
+        obj = [unique_ids() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        all_ok &= run_case(*case, rank, world, dev, obj[0])
+    dist.barrier(device_ids=[local])
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU ALL OK" if all_ok else "MGPU FAILED", flush=True)
+    sys.exit(0 if all_ok else 1)
+
+
+if __name__ == "__main__":
+    main()
