@@ -160,9 +160,12 @@ NEST_API nest_status_t nest_init_tables(nest_ctx_t* ctx, void* stream);
  * by sample id; NEST_SCHED_CLUSTERED runs the round-based key-centric greedy.
  * Outputs: perm_out int32[B] (samples of micro-batch i are
  * perm_out[mb_offsets_out[i] .. mb_offsets_out[i+1]), ascending id inside a
- * micro-batch), mb_offsets_out int32[N+1].  B mod N != 0 -> NEST_ERR_DIVISIBILITY. */
+ * micro-batch), mb_offsets_out int32[N+1].  B mod N != 0 -> NEST_ERR_DIVISIBILITY.
+ * keys / bag_offsets / nnz: the local batch (unused by SEQUENTIAL).  Issue it
+ * on the same stream as the following nest_route (they share scratch).
+ * CLUSTERED needs B < 2^21 and at most 16,383 distinct keys per sample. */
 NEST_API nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys,
-                                const int32_t* bag_offsets, int32_t B, int32_t N,
+                                const int32_t* bag_offsets, int64_t nnz, int32_t B, int32_t N,
                                 int32_t mode, int32_t* perm_out,
                                 int32_t* mb_offsets_out, void* stream);
 
@@ -192,6 +195,14 @@ NEST_API nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot,
  * out: fp32 [mb_out_rows, d]; pooled row p*F+f is bag (perm[mb_off+p], f). */
 NEST_API nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out,
                               void* compute, void* comm);
+
+/* The communication half of nest_lookup_fwd for micro-batch mb, issued early
+ * (FWP stream scheduling: "communication should be launched as
+ * early as possible within the frozen window"): owner send gather + embedding
+ * All2All on `comm`.  The later nest_lookup_fwd of the same micro-batch then
+ * only waits for it and pools on `compute`.  No-op when world == 1. */
+NEST_API nest_status_t nest_lookup_prefetch(nest_ctx_t* ctx, int32_t slot, int32_t mb,
+                                            void* compute, void* comm);
 
 /* Backward of micro-batch mb: per unique
  * key of the micro-batch, deterministic segment-sum of the gradients dout of

@@ -107,7 +107,8 @@ class NestContext:
         perm = torch.empty(B, dtype=torch.int32, device=self.device)
         mbo = torch.empty(N + 1, dtype=torch.int32, device=self.device)
         m = {"sequential": L.SCHED_SEQUENTIAL, "clustered": L.SCHED_CLUSTERED}[mode]
-        self._check(self.lib.nest_fwp_schedule(self.ctx, _ptr(keys), _ptr(bag_offsets), B, N, m,
+        nnz = 0 if keys is None else int(keys.numel())
+        self._check(self.lib.nest_fwp_schedule(self.ctx, _ptr(keys), _ptr(bag_offsets), nnz, B, N, m,
                                                _ptr(perm), _ptr(mbo), _stream(stream)))
         return perm, mbo
 
@@ -118,6 +119,10 @@ class NestContext:
 
     def dbp_refresh(self, active: int, prefetch: int, stream=None) -> None:
         self._check(self.lib.nest_dbp_refresh(self.ctx, active, prefetch, _stream(stream)))
+
+    def lookup_prefetch(self, slot: int, mb: int, compute=None, comm=None) -> None:
+        self._check(self.lib.nest_lookup_prefetch(self.ctx, slot, mb, _stream(compute),
+                                                  _stream(comm if comm is not None else compute)))
 
     def lookup_fwd(self, slot: int, mb: int, out, compute=None, comm=None) -> None:
         self._check(self.lib.nest_lookup_fwd(self.ctx, slot, mb, _ptr(out), _stream(compute),

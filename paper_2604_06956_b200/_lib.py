@@ -22,7 +22,8 @@ MAX_MICRO_BATCHES = 8
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
            "nest_create", "nest_destroy", "nest_init_tables", "nest_fwp_schedule", "nest_route",
-           "nest_dbp_refresh", "nest_lookup_fwd", "nest_grad_bwd_update", "nest_tower_fwd_bwd",
+           "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_grad_bwd_update",
+           "nest_tower_fwd_bwd",
            "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
            "nest_profile_read", "nest_last_error"]
 PROFILE_STAGES = 14
@@ -102,9 +103,10 @@ def load() -> C.CDLL:
         "nest_create": ([C.POINTER(Config), vp, vp, vp, vp, C.POINTER(vp)], i32),
         "nest_destroy": ([vp], i32),
         "nest_init_tables": ([vp, vp], i32),
-        "nest_fwp_schedule": ([vp, vp, vp, i32, i32, i32, vp, vp, vp], i32),
+        "nest_fwp_schedule": ([vp, vp, vp, i64, i32, i32, i32, vp, vp, vp], i32),
         "nest_route": ([vp, i32, vp, vp, i64, i32, vp, vp, i32, vp], i32),
         "nest_dbp_refresh": ([vp, i32, i32, vp], i32),
+        "nest_lookup_prefetch": ([vp, i32, i32, vp, vp], i32),
         "nest_lookup_fwd": ([vp, i32, i32, vp, vp, vp], i32),
         "nest_grad_bwd_update": ([vp, i32, i32, vp, f32, vp, vp], i32),
         "nest_tower_fwd_bwd": ([vp, vp, i64, vp, vp], i32),

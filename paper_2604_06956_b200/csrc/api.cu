@@ -110,11 +110,29 @@ static size_t layout(Ctx& c, char* base) {
   c.hot_list = w.take<int32_t>(K + 1);
   c.seg_tot = w.take<int32_t>(4);
   c.partial = w.take<float>(c.Pcap * D);
-  c.src_rows = w.take<float>(c.MBcap * D);
-  c.own_rows = W > 1 ? w.take<float>(c.OMBcap * D) : c.src_rows;
+  if (xfer_wanted(int(W))) {
+    c.src_rows = c.own_rows = nullptr;  // live in the IPC exchange window (xfer_setup)
+  } else {
+    c.src_rows = w.take<float>(c.MBcap * D);
+    c.own_rows = W > 1 ? w.take<float>(c.OMBcap * D) : c.src_rows;
+  }
   c.d_err = w.take<int32_t>(4);
   c.d_cnt_scratch = w.take<int32_t>(W * Nm + 1);
   c.n_refreshed = w.take<int32_t>(4);
+  if (Nm > 1) {
+    c.cl_bm = w.take<uint32_t>(c.words + 2);
+    c.cl_wr = w.take<int32_t>(c.words + 2);
+    c.cl_samp = w.take<int32_t>(K);
+    c.cl_sk = w.take<uint32_t>(K);
+    c.cl_sv = w.take<int32_t>(K);
+    c.cl_u = w.take<int32_t>(K);
+    c.cl_inmask = w.take<uint32_t>(K);
+    c.cl_size = w.take<int32_t>(B);
+    c.cl_grp = w.take<int32_t>(B);
+    c.cl_S = w.take<int32_t>(Nm * B);
+    c.cl_new = w.take<int32_t>(B);
+    c.cl_small = w.take<int64_t>(4);
+  }
   for (int si = 0; si < 2; ++si) {
     Slot& s = c.slot[si];
     s.uniq = w.take<int64_t>(K);
@@ -193,6 +211,43 @@ static void a2a_rows(Ctx& c, const float* send, const std::vector<int64_t>& scnt
     ro += rcnt[p];
   }
   NEST_NCCL(ncclGroupEnd());
+}
+
+// R6 + R7 of micro-batch mb on the comm stream: owner send gather + embedding
+// All2All into the requester's receive rows; records ev_emb[mb]
+static void lookup_comm(Ctx& c, Slot& s, int mb, cudaStream_t cs, cudaStream_t ms) {
+  if (mb == 0 || s.prefetched == 0) {
+    // the window starts after everything queued on compute (the refresh) and
+    // the slot's gather; later micro-batches only follow the comm chain
+    NEST_CUDA(cudaEventRecord(s.ev_ready, cs));
+    NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_ready, 0));
+    NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_gather, 0));
+  }
+  const double row = double(c.D) * sizeof(float);
+  {
+    ProfScope ps(c, ST_SEND_GATHER, SK_COMM, ms);
+    launch_send_gather(c, s, mb, ms);
+    // R_{o,i} buffer rows read + R_{o,i} rows written + 12 B of indices per received key
+    ps.bytes = 2.0 * row * double(s.info.mb_recv[mb]) + 12.0 * double(s.info.recv);
+  }
+  std::vector<int64_t> scnt(c.W), rcnt(c.W);
+  const int Nc = c.Nmax + 2;
+  for (int p = 0; p < c.W; ++p) {
+    scnt[p] = s.all[(size_t(p) * c.W + c.rank) * Nc + 1 + mb];  // owner -> requester p
+    rcnt[p] = s.all[(size_t(c.rank) * c.W + p) * Nc + 1 + mb];  // from owner p
+  }
+  {
+    ProfScope ps(c, ST_EMB_A2A, SK_COMM, ms);
+    if (c.xfer_ce) {
+      xfer_push_emb(c, s, mb, ms, s.ev_emb[mb]);  // records ev_emb after the self rows
+    } else {
+      a2a_rows(c, c.own_rows + s.own_base[mb] * c.D, scnt, c.src_rows + s.src_base[mb] * c.D, rcnt, ms);
+      NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
+    }
+    ps.launches = 0;
+    ps.bytes = row * double(s.info.mb_recv[mb] - scnt[c.rank]);  // rows sent off-GPU
+  }
+  s.prefetched |= 1u << mb;
 }
 
 }  // namespace nest
@@ -281,6 +336,7 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       cfg1.maxCTAs = mc ? std::atoi(mc) : 8;
       NEST_NCCL(ncclCommInitRankConfig(&c->comm, c->W, id0, c->rank, &cfg0));
       NEST_NCCL(ncclCommInitRankConfig(&c->comm_aux, c->W, id1, c->rank, &cfg1));
+      if (xfer_wanted(c->W)) xfer_setup(*c, st0);
     }
     if (c->cfg.tower_layers > 0) tower_create(*c);
   });
@@ -298,6 +354,7 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   cudaDeviceSynchronize();
   if (c->tower) tower_destroy(*c);
   profile_destroy(*c);
+  xfer_destroy(*c);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
   for (auto& s : c->slot) {
@@ -321,7 +378,7 @@ nest_status_t nest_init_tables(nest_ctx_t* ctx, void* stream) {
 }
 
 nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int32_t* bag_offsets,
-                                int32_t B, int32_t N, int32_t mode, int32_t* perm_out,
+                                int64_t nnz, int32_t B, int32_t N, int32_t mode, int32_t* perm_out,
                                 int32_t* mb_offsets_out, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
@@ -331,9 +388,13 @@ nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int3
     NEST_CHECK(B % N == 0, NEST_ERR_DIVISIBILITY, "B mod N != 0");
     NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || mode == NEST_SCHED_CLUSTERED, NEST_ERR_INVALID, "bad mode");
     NEST_CHECK(perm_out && mb_offsets_out, NEST_ERR_INVALID, "null output");
-    NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || (keys && bag_offsets), NEST_ERR_INVALID, "null batch");
+    NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || ((keys || nnz == 0) && bag_offsets), NEST_ERR_INVALID,
+               "null batch");
+    NEST_CHECK(nnz >= 0 && nnz <= c->Kcap, NEST_ERR_CAPACITY, "nnz exceeds max_keys");
+    NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || N == 1 || c->cl_u != nullptr, NEST_ERR_INVALID,
+               "clustered schedule needs max_micro_batches > 1");
     ProfScope ps(*c, ST_SCHEDULE, SK_AUX, S(stream));
-    launch_schedule(*c, keys, bag_offsets, B, N, mode, perm_out, mb_offsets_out, S(stream));
+    launch_schedule(*c, keys, bag_offsets, nnz, B, N, mode, perm_out, mb_offsets_out, S(stream));
   });
 }
 
@@ -367,6 +428,8 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
     NEST_CUDA(cudaEventRecord(s.ev_gather, st));
     s.routed = true;
     s.updated = false;
+    s.prefetched = 0;
+    s.epoch = ++c->epoch;
   });
 }
 
@@ -392,6 +455,19 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
   });
 }
 
+nest_status_t nest_lookup_prefetch(nest_ctx_t* ctx, int32_t slot, int32_t mb, void* compute, void* comm) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    Slot& s = slot_of(*c, slot);
+    NEST_CHECK(s.routed, NEST_ERR_ORDER, "prefetch before route");
+    NEST_CHECK(!s.updated, NEST_ERR_ORDER, "prefetch after the window closed (S:568)");
+    NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
+    NEST_CHECK(!((s.prefetched >> mb) & 1u), NEST_ERR_ORDER, "micro-batch already prefetched");
+    if (c->W > 1) lookup_comm(*c, s, mb, S(compute), S(comm));
+  });
+}
+
 nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out, void* compute,
                               void* comm) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
@@ -404,34 +480,9 @@ nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* 
     NEST_CHECK(out != nullptr, NEST_ERR_INVALID, "null out");
     cudaStream_t cs = S(compute), ms = S(comm);
     if (c->W > 1) {
-      if (mb == 0) {
-        // the window starts after everything queued on compute (refresh) and
-        // the slot's gather; later micro-batches only follow the comm chain
-        NEST_CUDA(cudaEventRecord(s.ev_ready, cs));
-        NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_ready, 0));
-        NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_gather, 0));
-      }
-      const double row = double(c->D) * sizeof(float);
-      {
-        ProfScope ps(*c, ST_SEND_GATHER, SK_COMM, ms);
-        launch_send_gather(*c, s, mb, ms);
-        // R_{o,i} buffer rows read + R_{o,i} rows written + 12 B of indices per received key
-        ps.bytes = 2.0 * row * double(s.info.mb_recv[mb]) + 12.0 * double(s.info.recv);
-      }
-      std::vector<int64_t> scnt(c->W), rcnt(c->W);
-      const int Nc = c->Nmax + 2;
-      for (int p = 0; p < c->W; ++p) {
-        scnt[p] = s.all[(size_t(p) * c->W + c->rank) * Nc + 1 + mb];  // owner -> requester p
-        rcnt[p] = s.all[(size_t(c->rank) * c->W + p) * Nc + 1 + mb];  // from owner p
-      }
-      {
-        ProfScope ps(*c, ST_EMB_A2A, SK_COMM, ms);
-        a2a_rows(*c, c->own_rows + s.own_base[mb] * c->D, scnt, c->src_rows + s.src_base[mb] * c->D, rcnt, ms);
-        ps.launches = 0;
-        ps.bytes = row * double(s.info.mb_recv[mb] - scnt[c->rank]);  // rows sent off-GPU
-      }
-      NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
+      if (!((s.prefetched >> mb) & 1u)) lookup_comm(*c, s, mb, cs, ms);
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_emb[mb], 0));
+      if (c->xfer_ce) xfer_wait_emb(*c, s, mb, cs);   // every owner's rows have landed
     } else if (mb == 0) {
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));
     }
@@ -480,11 +531,15 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
       }
       {
         ProfScope ps(*c, ST_GRAD_A2A, SK_COMM, ms);
-        a2a_rows(*c, c->src_rows + s.src_base[mb] * c->D, scnt, c->own_rows + s.own_base[mb] * c->D, rcnt, ms);
+        if (c->xfer_ce)
+          xfer_push_grad(*c, s, mb, ms);
+        else
+          a2a_rows(*c, c->src_rows + s.src_base[mb] * c->D, scnt, c->own_rows + s.own_base[mb] * c->D, rcnt, ms);
         ps.launches = 0;
         ps.bytes = row * double(s.info.mb_uniq[mb] - scnt[c->rank]);  // rows sent off-GPU
       }
       if (mb == s.N - 1) {
+        if (c->xfer_ce) xfer_wait_grads(*c, s, ms);  // every requester's gradients have landed
         NEST_CUDA(cudaStreamWaitEvent(ms, other.ev_gather, 0));
         {
           ProfScope ps(*c, ST_UPDATE, SK_COMM, ms);

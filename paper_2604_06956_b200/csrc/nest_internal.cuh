@@ -93,6 +93,8 @@ struct Slot {
   std::vector<int64_t> src_base, own_base, q0;   // per mb: row bases / sorted-occurrence starts
   std::vector<int64_t> key_soff, key_roff;       // key All2All offsets
   int ubits = 0;
+  uint32_t epoch = 0;              // window sequence number (same on every rank)
+  uint32_t prefetched = 0;         // micro-batches whose embedding All2All is issued
   bool routed = false, updated = false;
   cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
               ev_grad[NEST_MAX_MICRO_BATCHES] = {}, ev_ready = nullptr, ev_sync = nullptr;
@@ -167,7 +169,29 @@ struct Ctx {
   int32_t* d_err = nullptr;        // [1]
   int32_t* d_cnt_scratch = nullptr; // [W*(Nmax)] mb counts scratch
   int32_t* n_refreshed = nullptr;  // [1] rows copied by the last refresh
+  // FWP clustering scratch (cluster.cu)
+  uint32_t* cl_bm = nullptr;       // [words+2]
+  int32_t* cl_wr = nullptr;        // [words+2]
+  int32_t* cl_samp = nullptr;      // [Kcap] sample of each occurrence
+  uint32_t* cl_sk = nullptr;       // [Kcap]
+  int32_t* cl_sv = nullptr;        // [Kcap]
+  int32_t* cl_u = nullptr;         // [Kcap] key id of first occurrences in a sample, else -1
+  uint32_t* cl_inmask = nullptr;   // [Kcap] groups whose union holds the key
+  int32_t* cl_size = nullptr;      // [Bcap]
+  int32_t* cl_grp = nullptr;       // [Bcap]
+  int32_t* cl_S = nullptr;         // [Nmax][Bcap]
+  int32_t* cl_new = nullptr;       // [Bcap]
+  int64_t* cl_small = nullptr;     // [4]
   Slot slot[2];
+  uint32_t epoch = 0;
+  // copy-engine All2All transport (xfer.cu)
+  bool xfer_ce = false;
+  void* xwin = nullptr;            // library-owned, IPC-exported exchange window
+  size_t xwin_bytes = 0, xoff_own = 0, xoff_flags = 0;
+  uint32_t* xflags = nullptr;      // [2][Nmax][W] epoch flags written by peers
+  std::vector<void*> peer_win;
+  std::vector<float*> peer_src, peer_own;
+  std::vector<uint32_t*> peer_flags;
   ncclComm_t comm = nullptr, comm_aux = nullptr;
   nest_status_t sticky = NEST_OK;
   std::string last_error;
@@ -418,7 +442,7 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st);
 void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st);
 void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st);
 void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
-void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int B, int N, int mode,
+void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N, int mode,
                      int32_t* perm, int32_t* mb_offsets, cudaStream_t st);
 // tracing hooks (api.cu); cheap no-ops unless profiling is on
 int prof_begin(Ctx& c, int stage, int kind, cudaStream_t st);
@@ -438,6 +462,14 @@ struct ProfScope {
   ProfScope(Ctx& cc, int stage, int kind, cudaStream_t s) : c(cc), id(prof_begin(cc, stage, kind, s)), st(s) {}
   ~ProfScope() { prof_end(c, id, st, bytes, dcount, bpc, launches); }
 };
+// copy-engine transport (xfer.cu)
+bool xfer_wanted(int W);
+void xfer_setup(Ctx& c, cudaStream_t st);
+void xfer_destroy(Ctx& c);
+void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_self);
+void xfer_wait_emb(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void xfer_wait_grads(Ctx& c, Slot& s, cudaStream_t st);
 void tower_create(Ctx& c);
 void tower_destroy(Ctx& c);
 void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st);

@@ -11,13 +11,13 @@ __global__ void k_schedule_sequential(int B, int N, int32_t* __restrict__ perm,
   if (blockIdx.x == 0 && threadIdx.x <= N) mb_offsets[threadIdx.x] = threadIdx.x * cap;
 }
 
-void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int B, int N,
+void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N,
                     int32_t* perm, int32_t* mb_offsets, cudaStream_t st);
 
-void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int B, int N, int mode,
+void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N, int mode,
                      int32_t* perm, int32_t* mb_offsets, cudaStream_t st) {
   if (mode == NEST_SCHED_CLUSTERED && N > 1) {
-    launch_cluster(c, keys, bag_offsets, B, N, perm, mb_offsets, st);
+    launch_cluster(c, keys, bag_offsets, nnz, B, N, perm, mb_offsets, st);
     return;
   }
   int grid = (B + 255) / 256;

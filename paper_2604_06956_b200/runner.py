@@ -75,10 +75,15 @@ class Runner:
             self.primed = True
         outs = self.out_buffers(a)
         self.outs = outs if keep_outputs else []
-        ctx.lookup_fwd(a, 0, outs[0], cs, ms)
+        # comm stream: emb_1, emb_2, grad_1, emb_3, grad_2, ... (emb A2A of
+        # micro-batch i+1 queued before grad A2A of i); compute stream:
+        # pool_i, tower_i, segsum_i -- compute never waits for a later
+        # micro-batch's communication
+        ctx.lookup_prefetch(a, 0, cs, ms)
         for i in range(self.N):
+            ctx.lookup_fwd(a, i, outs[i], cs, ms)
             if i + 1 < self.N:
-                ctx.lookup_fwd(a, i + 1, outs[i + 1], cs, ms)
+                ctx.lookup_prefetch(a, i + 1, cs, ms)
             with torch.cuda.stream(cs):
                 dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
             if i == self.N - 1 and self.pipelined and next_batch is not None:

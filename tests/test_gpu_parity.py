@@ -197,6 +197,56 @@ def test_unpooled_expand_p1():
     assert np.array_equal(got, ref)
 
 
+# --------------------------------------------------------------------------- clustering
+@pytest.mark.parametrize("case", ["tiny-N2", "tiny-N4", "corr-N4", "corr-N8", "dlrmish-N4"])
+def test_cluster_bit_exact_vs_oracle(case):
+    """R14: GPU round-based greedy == oracle.cluster.cluster_rounds (perm + offsets)."""
+    if case.startswith("tiny"):
+        cfg, B, N = WL.CONFIGS["tiny"], 32, int(case[-1])
+        keys, offs = WL.gen_batch(cfg, 4, 0, 0, batch=B)
+    elif case.startswith("corr"):
+        cfg, B, N = WL.CONFIGS["tiny"].with_(table_rows=(3000,) * 4), 512, int(case[-1])
+        keys, offs = WL.gen_correlated_batch(cfg, 2, 0, 0, groups=16, rho=0.7, batch=B)
+    else:
+        cfg = WL.CONFIGS["dlrm"].with_(table_rows=tuple(r // 50 for r in WL.CONFIGS["dlrm"].table_rows))
+        B, N = 2048, 4
+        keys, offs = WL.gen_batch(cfg, 1, 0, 0, batch=B)
+    ctx = make_ctx(cfg, B, N=max(N, 2), K=len(keys))
+    perm, mbo = ctx.fwp_schedule(to_dev(keys, torch.int64), to_dev(offs, torch.int32), B, N, "clustered")
+    ref_perm, ref_mbo = OC.cluster_rounds(OC.sample_keysets(keys, offs, cfg.num_features), N)
+    assert np.array_equal(perm.cpu().numpy(), ref_perm)
+    assert np.array_equal(mbo.cpu().numpy(), ref_mbo)
+
+
+def test_train_w1_clustered_p1_bit_exact():
+    """Prop. 2 on the GPU: a clustered FWP window gives the Eq. 1 tables."""
+    cfg = WL.CONFIGS["tiny"]
+    B, N, T, F, d = 64, 4, 4, cfg.num_features, cfg.dim
+    batches = [WL.gen_batch(cfg, 8, t, 0, batch=B) for t in range(T)]
+    douts = [WL.gen_dout(8, t, 0, B * F, d, "dyadic") for t in range(T)]
+    ctx = make_ctx(cfg, B, N=N, K=max(len(b[0]) for b in batches), init="dyadic", seed=11)
+    run = Runner(ctx, N=N, schedule="clustered", pipelined=True, lr_over_B=2.0 ** -10)
+    db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), B) for k, o in batches]
+    cap = B // N
+    for t in range(T):
+        def dout_fn(tt, i, pooled, t=t):
+            perm = run.sched[t % 2][0].cpu().numpy()
+            samples = perm[i * cap:(i + 1) * cap]
+            bags = (samples[:, None] * F + np.arange(F)[None, :]).reshape(-1)
+            return to_dev(douts[t][bags], torch.float32)
+        outs = run.step(db[t], db[t + 1] if t + 1 < T else None, dout_fn)
+        torch.cuda.synchronize()
+        perm = run.sched[t % 2][0].cpu().numpy()
+        tab_ref = OS.LazyTable(11, d, "dyadic")
+        for tt in range(t + 1):
+            res = OS.sync_step(tab_ref, [batches[tt]], [douts[tt]], 2.0 ** -10)
+        pooled = np.concatenate([o.cpu().numpy() for o in outs])
+        order = (perm[:, None] * F + np.arange(F)[None, :]).reshape(-1)
+        assert np.array_equal(pooled, res.pooled[0][order])
+    allk = np.unique(np.concatenate([b[0] for b in batches]))
+    assert np.array_equal(ctx.read_rows(to_dev(allk, torch.int64)).cpu().numpy(), tab_ref.get(allk))
+
+
 # --------------------------------------------------------------------------- errors
 def test_error_paths():
     cfg = WL.CONFIGS["tiny"]
