@@ -232,7 +232,7 @@ def main():
                 key = (i, pooled.shape[0])
                 if key not in douts:
                     douts[key] = torch.empty_like(pooled)
-                ctx.tower_fwd_bwd(pooled, douts[key], stream=runner.compute)
+                ctx.tower_fwd_bwd(pooled, douts[key], stream=torch.cuda.current_stream())  # dense lane
                 return douts[key]
             return fn
         fixed = {}
@@ -280,9 +280,7 @@ def main():
             if source == "host":
                 res = outs[-1][0].to("cpu", non_blocking=False)   # the step's result row
                 d2h += res.numel() * 4
-        runner.compute.wait_stream(runner.comm)
-        runner.compute.wait_stream(runner.aux)
-        end.record(runner.compute)
+        end.record(runner.join())
         torch.cuda.synchronize()
         ms = start.elapsed_time(end)
         prof = None

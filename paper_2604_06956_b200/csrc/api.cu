@@ -448,7 +448,7 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
     ProfScope ps(*c, ST_REFRESH, SK_COMPUTE, st);
     launch_refresh(*c, a, p, st);
     // 8 (U_o + U_o') key reads + 2 I rows (I counted on the device)
-    ps.bytes = 8.0 * double(std::min(a.info.recv, c->Uocap) + std::min(p.info.recv, c->Uocap));
+    ps.bytes = 8.0 * double(std::min(p.info.recv, c->Uocap));  // U_o' keys + bit tests
     ps.dcount = c->n_refreshed;
     ps.bpc = 2.0 * c->D * sizeof(float);
     NEST_CUDA(cudaEventRecord(a.ev_free, st));
@@ -517,7 +517,9 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
       ps.bytes = row * double(s.info.mb_out_rows[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
                  row * double(s.info.mb_uniq[mb]);
     }
-    // sum_i R_{o,i} gradient rows + 3 U_o rows (buffer r/w + shard write)
+    // sum_i R_{o,i} gradient rows + U_o buffer rows read + U_o rows
+    // written back (the survey's third U_o row, the buffer rewrite, is not needed:
+    // the refresh copies written-back rows)
     double upd_fixed = 0;
     for (int i = 0; i < s.N; ++i) upd_fixed += row * double(c->W > 1 ? s.info.mb_recv[i] : s.info.mb_uniq[i]);
     if (c->W > 1) {
@@ -546,7 +548,7 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
           launch_reduce_sgd(*c, s, lr_over_B, ms);
           ps.bytes = upd_fixed;
           ps.dcount = s.n_owner;
-          ps.bpc = 3.0 * row;
+          ps.bpc = 2.0 * row;  // frozen buffer row read + shard write-back
         }
         NEST_CUDA(cudaEventRecord(s.ev_update, ms));
         NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
@@ -558,7 +560,7 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
         launch_reduce_sgd(*c, s, lr_over_B, cs);
         ps.bytes = upd_fixed;
         ps.dcount = s.n_owner;
-        ps.bpc = 3.0 * row;
+        ps.bpc = 2.0 * row;  // frozen buffer row read + shard write-back
       }
       NEST_CUDA(cudaEventRecord(s.ev_update, cs));
     }

@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
         }
       }
     }
+    // the updated row goes to the shard only (write-back): the
+    // dual-buffer refresh reads written-back rows from the shard, so the
+    // frozen active buffer is never rewritten (one row of traffic less)
     const int64_t srow = __ldg(owner_rows + u);
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
@@ -435,7 +438,6 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
       e.y = __fmaf_rn(-lr, acc[v].y, e.y);
       e.z = __fmaf_rn(-lr, acc[v].z, e.z);
       e.w = __fmaf_rn(-lr, acc[v].w, e.w);
-      st_f4(buffer + u * D + gp.col(v), e);
       st_f4_cs(shard + srow * D + gp.col(v), e);
     }
   }
@@ -461,22 +463,42 @@ void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// R5: dual-buffer refresh: prefetch[u'] <- active[u] for keys in both sets
+// R5: dual-buffer refresh: for every key of the prefetch slot that the active
+// slot also holds (bit test in the active slot's owner bitmap), overwrite the
+// prefetched row with the updated row.  The update wrote that row back to the
+// shard (same bits as the active copy, reading R-REFRESH), so it is copied
+// from shard[ldom] -- no rank lookup, no merge of key lists.
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_refresh(
     const int32_t* __restrict__ n_p, const int32_t* __restrict__ rows_p,
-    const uint32_t* __restrict__ bm_a, const int32_t* __restrict__ wr_a,
-    const float* __restrict__ buf_a, float* __restrict__ buf_p, int32_t* __restrict__ count) {
+    const uint32_t* __restrict__ bm_a, const float* __restrict__ shard, float* __restrict__ buf_p,
+    int32_t* __restrict__ count) {
   Grp<D> gp;
   const int64_t n = *n_p;
   int32_t local = 0;
-  for (int64_t u = gp.g; u < n; u += gp.ng) {
-    const uint32_t ld = uint32_t(__ldg(rows_p + u));
-    if (!bit_test(bm_a, ld)) continue;
-    const int64_t ua = bit_rank(bm_a, wr_a, ld);
-    copy_row<D>(buf_p + u * D, buf_a + ua * D, gp);
-    if (gp.l == 0) ++local;
+  constexpr int U = 4;
+  for (int64_t u0 = gp.g * U; u0 < n; u0 += gp.ng * U) {
+    uint32_t ld[U];
+    bool hit[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      ld[k] = u0 + k < n ? uint32_t(__ldg(rows_p + u0 + k)) : 0u;
+      hit[k] = u0 + k < n && bit_test(bm_a, ld[k]);
+    }
+    float4 v[U][RowGeom<D>::VPL];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+#pragma unroll
+      for (int q = 0; q < RowGeom<D>::VPL; ++q)
+        if (hit[k]) v[k][q] = ldg_f4(shard + int64_t(ld[k]) * D + gp.col(q));
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+#pragma unroll
+      for (int q = 0; q < RowGeom<D>::VPL; ++q)
+        if (hit[k]) st_f4(buf_p + (u0 + k) * D + gp.col(q), v[k][q]);
+      if (hit[k] && gp.l == 0) ++local;
+    }
   }
   if (local) atomicAdd(count, local);
 }
@@ -484,9 +506,9 @@ __global__ void __launch_bounds__(kRowThreads) k_refresh(
 void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st) {
   NEST_CUDA(cudaMemsetAsync(c.n_refreshed, 0, sizeof(int32_t), st));
   NEST_DISPATCH_D(c.D, {
-    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW * 4;
     k_refresh<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
-        p.n_owner, p.owner_rows, a.obm, a.owr, a.buffer, p.buffer, c.n_refreshed);
+        p.n_owner, p.owner_rows, a.obm, c.shard, p.buffer, c.n_refreshed);
   });
   NEST_LAUNCH_CHECK();
 }

@@ -98,13 +98,13 @@ void tower_create(Ctx& c) {
   NEST_CUBLAS(cublasCreate(&t->h));
   NEST_CUBLAS(cublasSetWorkspace(t->h, t->ws, t->ws_bytes));
   NEST_CUBLAS(cublasSetMathMode(t->h, CUBLAS_DEFAULT_MATH));
-  // leave SMs for the comm stream so FWP's All2Alls overlap the tower
-  // (SURVEY H3); NEST_TOWER_SM_RESERVE overrides (0 at W=1: nothing to overlap)
+  // leave SMs to the embedding lane (pool / segment-sum / send gather) that
+  // FWP overlaps with the tower; NEST_TOWER_SM_RESERVE overrides
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const char* rv = std::getenv("NEST_TOWER_SM_RESERVE");
-    const int reserve = rv ? std::atoi(rv) : (c.W > 1 ? 16 : 0);
+    const int reserve = rv ? std::atoi(rv) : 24;
     if (reserve > 0 && reserve < sms) NEST_CUBLAS(cublasSetSmCountTarget(t->h, sms - reserve));
   }
   for (int l = 0; l < L; ++l) {

@@ -5,12 +5,13 @@ order); all work runs in libnest.so.  The order follows the paper:
 
 * DBP: Key Routing + Retrieval of batch t+1 (``nest_route`` on the
   aux stream) overlaps the window of batch t; after update(t) the dual-buffer
-  refresh copies the intersection Active -> Prefetch; the slot roles swap.
-* FWP: the window of batch t runs N micro-batches; the
-  embedding All2All of micro-batch i+1 is issued on the comm stream before
-  micro-batch i's dense compute ("communication launched as early as
-  possible"), gradients of micro-batch i follow its compute, and the single
-  deferred update runs after micro-batch N.
+  refresh overwrites the intersection in the prefetch slot; the slots swap.
+* FWP: the window of batch t runs N micro-batches on
+  separate lanes -- a comm stream (owner send gather + All2All, issued as
+  early as possible), an embedding stream (pool / segment-sum, the
+  sparse side of forward / backward) and a dense stream (the stand-in tower).
+  Pooling micro-batch i+1 and the gradients of micro-batch i run while the
+  tower computes; the single deferred update follows micro-batch N.
 """
 from __future__ import annotations
 
@@ -23,22 +24,26 @@ from . import NestContext
 
 class Runner:
     """Drives one rank through steps.  `dout_fn(t, i, pooled_i) -> dout_i`
-    supplies the loss gradient of micro-batch i (LIN: a fixed tensor, QUAD:
-    pooled itself, tower: the stand-in tower's input gradient)."""
+    supplies the loss gradient of micro-batch i on the dense stream (LIN: a
+    fixed tensor, QUAD: pooled itself, tower: the stand-in tower's input
+    gradient)."""
 
     def __init__(self, ctx: NestContext, N: int = 1, schedule: str = "sequential",
                  pipelined: bool = True, lr_over_B: float = 2.0 ** -10):
         self.ctx, self.N, self.schedule, self.pipelined = ctx, N, schedule, pipelined
         self.lr = lr_over_B
         dev = ctx.device
-        self.compute = torch.cuda.Stream(device=dev)
-        # comm stream at high priority: its CTAs are scheduled first as SMs free up
+        self.compute = torch.cuda.Stream(device=dev)            # embedding lane
+        # comm lane at high priority: its kernels are scheduled first as SMs free up
         self.comm = torch.cuda.Stream(device=dev, priority=-1) if ctx.world > 1 else self.compute
-        self.aux = torch.cuda.Stream(device=dev)
+        self.dense = torch.cuda.Stream(device=dev)              # tower lane
+        self.aux = torch.cuda.Stream(device=dev)                # DBP lookahead
         self.t = 0
         self.primed = False
         self.outs: List[torch.Tensor] = []
         self.sched = {}
+        self._ev_pool = [torch.cuda.Event() for _ in range(8)]
+        self._ev_dense = [torch.cuda.Event() for _ in range(8)]
 
     # -- helpers ---------------------------------------------------------------
     def _schedule(self, slot, keys, offs, B, stream):
@@ -53,7 +58,7 @@ class Runner:
     def out_buffers(self, slot) -> List[torch.Tensor]:
         info = self.ctx.slot_info(slot)
         outs = []
-        with torch.cuda.stream(self.compute):   # allocation stream = use stream
+        with torch.cuda.stream(self.compute):   # allocation stream = producing stream
             for i in range(self.N):
                 rows = int(info.mb_out_rows[i])
                 outs.append(torch.empty((rows, self.ctx.dim), dtype=torch.float32,
@@ -68,24 +73,29 @@ class Runner:
         ctx = self.ctx
         keys, offs, B = batch
         a, p = self.t % 2, (self.t + 1) % 2
-        cs, ms = self.compute, self.comm
+        cs, ms, ds = self.compute, self.comm, self.dense
         cs.wait_stream(torch.cuda.current_stream(ctx.device))   # batch uploads
         if not self.pipelined or not self.primed:
             self._route(a, keys, offs, B, cs)
             self.primed = True
         outs = self.out_buffers(a)
         self.outs = outs if keep_outputs else []
-        # comm stream: emb_1, emb_2, grad_1, emb_3, grad_2, ... (emb A2A of
-        # micro-batch i+1 queued before grad A2A of i); compute stream:
-        # pool_i, tower_i, segsum_i -- compute never waits for a later
-        # micro-batch's communication
+        # embedding lane: pool_0, pool_1, seg_0, pool_2, seg_1, ... (pool of
+        # micro-batch i+1 is queued before the gradients of i); comm lane:
+        # emb_0, emb_1, grad_0, emb_2, grad_1, ...; dense lane: tower_i
         ctx.lookup_prefetch(a, 0, cs, ms)
+        ctx.lookup_fwd(a, 0, outs[0], cs, ms)
+        self._ev_pool[0].record(cs)
         for i in range(self.N):
-            ctx.lookup_fwd(a, i, outs[i], cs, ms)
             if i + 1 < self.N:
                 ctx.lookup_prefetch(a, i + 1, cs, ms)
-            with torch.cuda.stream(cs):
+                ctx.lookup_fwd(a, i + 1, outs[i + 1], cs, ms)
+                self._ev_pool[i + 1].record(cs)
+            ds.wait_event(self._ev_pool[i])
+            with torch.cuda.stream(ds):
                 dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
+            self._ev_dense[i].record(ds)
+            cs.wait_event(self._ev_dense[i])
             if i == self.N - 1 and self.pipelined and next_batch is not None:
                 nk, no, nB = next_batch
                 self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
@@ -95,3 +105,11 @@ class Runner:
             ctx.dbp_refresh(a, p, cs)
         self.t += 1
         return outs
+
+    def join(self, stream=None):
+        """Make `stream` (default: the embedding lane) wait for every lane."""
+        s = stream or self.compute
+        for other in (self.comm, self.dense, self.aux):
+            if other is not s:
+                s.wait_stream(other)
+        return s
