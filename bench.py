@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="dlrm", choices=["dlrm", "tiny", "dbp_stress"])
-    ap.add_argument("--micro-batches", type=int, default=4)
+    ap.add_argument("--micro-batches", type=int, default=0,
+                    help="FWP micro-batches N; 0 = auto: 1 at one GPU (no All2All to hide), 2 otherwise")
     ap.add_argument("--schedule", default="sequential", choices=["sequential", "clustered"])
     ap.add_argument("--variant", default="et", choices=["et", "e"],
                     help="et: embedding + stand-in tower (FWP overlap partner); e: embedding only")
@@ -189,6 +190,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and "RANK" in os.environ:
         pass  # torchrun decides
+    if args.micro_batches <= 0:
+        args.micro_batches = 1 if world == 1 else 2
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

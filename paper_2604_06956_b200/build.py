@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-warn-spills",
            "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-I", cublas_inc,
            *sources(),
-           "-L", nccl_lib, "-L", cublas_lib, "-l:libnccl.so.2", "-l:libcublas.so.12",
+           "-L", nccl_lib, "-L", cublas_lib, "-l:libnccl.so.2", "-l:libcublas.so.12", "-l:libcublasLt.so.12",
            "-Xlinker", f"-rpath={nccl_lib}:{cublas_lib}",
            "-o", tmp]
     if verbose:

@@ -75,7 +75,8 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
   else
     c.OMBcap = cfg->max_owner_mb_rows > 0 ? cfg->max_owner_mb_rows
                                           : (c.Nmax > 1 ? 2 * c.Rcap : c.Rcap);
-  c.Pcap = 2 * c.Kcap / 32 + 64;
+  c.Pcap = 2 * c.Kcap / 32 + 64;   // partial rows for chunk length >= 32
+  if (const char* e = std::getenv("NEST_SEG_CHUNK")) c.seg_chunk = std::max(32, std::atoi(e));
 }
 
 size_t tower_workspace_bytes(const Ctx& c);

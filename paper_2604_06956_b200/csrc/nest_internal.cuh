@@ -184,6 +184,7 @@ struct Ctx {
   int64_t* cl_small = nullptr;     // [4]
   Slot slot[2];
   uint32_t epoch = 0;
+  int seg_chunk = 32;              // segment-sum: cold threshold = hot chunk length (>= 32)
   // copy-engine All2All transport (xfer.cu)
   bool xfer_ce = false;
   void* xwin = nullptr;            // library-owned, IPC-exported exchange window

@@ -268,14 +268,15 @@ __device__ __forceinline__ void sum_rows(const int32_t* __restrict__ sval, int64
 }
 
 template <int D>
-__global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, const int32_t* __restrict__ seg_start,
+__global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, int chunk,
+                                                             const int32_t* __restrict__ seg_start,
                                                              const int32_t* __restrict__ sval,
                                                              const float* __restrict__ dout,
                                                              float* __restrict__ g) {
   Grp<D> gp;
   for (int64_t k = gp.g; k < Ui; k += gp.ng) {
     const int64_t a = seg_start[k], b = seg_start[k + 1];
-    if (b - a > kChunk) continue;
+    if (b - a > chunk) continue;
     float4 acc[RowGeom<D>::VPL];
     sum_rows<D>(sval, a, b, dout, gp, acc);
 #pragma unroll
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, const i
 
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_chunks(
-    const int32_t* __restrict__ tot, const int32_t* __restrict__ hot_list,
+    int chunk, const int32_t* __restrict__ tot, const int32_t* __restrict__ hot_list,
     const int32_t* __restrict__ hot_ppos, const int32_t* __restrict__ seg_start,
     const int32_t* __restrict__ sval, const float* __restrict__ dout, float* __restrict__ partial) {
   Grp<D> gp;
@@ -298,9 +299,9 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_chunks(
     }
     const int k = hot_list[lo];
     const int64_t m = cidx - hot_ppos[lo];
-    const int64_t a = seg_start[k] + m * kChunk;
+    const int64_t a = seg_start[k] + m * chunk;
     const int64_t e = seg_start[k + 1];
-    const int64_t b = e < a + kChunk ? e : a + kChunk;
+    const int64_t b = e < a + chunk ? e : a + chunk;
     float4 acc[RowGeom<D>::VPL];
     sum_rows<D>(sval, a, b, dout, gp, acc);
 #pragma unroll
@@ -359,10 +360,11 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
   int32_t* hot_list = c.hot_list;
   int32_t* hot_ppos = c.seg_aux;
   int32_t* tot = c.seg_tot;
+  const int chunk = c.seg_chunk;
   scan_exclusive<I2>(
       [=] __device__(int64_t k) {
         const int32_t L = seg[k + 1] - seg[k];
-        return L > kChunk ? I2(1, (L + kChunk - 1) / kChunk) : I2(0, 0);
+        return L > chunk ? I2(1, (L + chunk - 1) / chunk) : I2(0, 0);
       },
       Ui,
       [=] __device__(int64_t k, I2 v) {
@@ -370,7 +372,7 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
           tot[0] = v.a;
           tot[1] = v.b;
           hot_ppos[v.a] = v.b;
-        } else if (seg[k + 1] - seg[k] > kChunk) {
+        } else if (seg[k + 1] - seg[k] > chunk) {
           hot_list[v.a] = int32_t(k);
           hot_ppos[v.a] = v.b;
         }
@@ -378,8 +380,8 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
       c.scan_tmp_win, st);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_segsum_cold<D><<<blocks_for_rows(Ui, rpb, 148 * 16), kRowThreads, 0, st>>>(Ui, seg, sval, dout, g);
-    k_segsum_hot_chunks<D><<<148 * 4, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, seg, sval, dout,
+    k_segsum_cold<D><<<blocks_for_rows(Ui, rpb, 148 * 16), kRowThreads, 0, st>>>(Ui, chunk, seg, sval, dout, g);
+    k_segsum_hot_chunks<D><<<148 * 4, kRowThreads, 0, st>>>(chunk, tot, hot_list, hot_ppos, seg, sval, dout,
                                                             c.partial);
     k_segsum_hot_final<D><<<148 * 2, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, g);
   });

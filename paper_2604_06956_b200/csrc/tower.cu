@@ -5,14 +5,27 @@
 // fixed top gradient G, backward dW_l = dY_l^T X_{l-1} and dX_{l-1} = dY_l W_l,
 // with the input gradient dX_0 written as fp32 `dout`.  GEMMs run on the
 // tensor cores through cuBLAS (library GEMMs, allowed for the plain tower).
+#include <cublasLt.h>
 #include <cublas_v2.h>
+
+#include <map>
 
 #include "nest_internal.cuh"
 
 namespace nest {
 
+struct GemmPlan {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  cublasLtMatmulAlgo_t algo{};
+  bool have_algo = false;
+};
+
 struct Tower {
   cublasHandle_t h = nullptr;
+  cublasLtHandle_t lt = nullptr;
+  int32_t sm_target = 0;
+  std::map<std::string, struct GemmPlan> plans;
   int L = 0, H = 0, in0 = 0;
   int64_t bmax = 0;
   __nv_bfloat16* w = nullptr;       // weights, layer l at woff[l], [H, in_l] row-major
@@ -105,8 +118,12 @@ void tower_create(Ctx& c) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const char* rv = std::getenv("NEST_TOWER_SM_RESERVE");
     const int reserve = rv ? std::atoi(rv) : 24;
-    if (reserve > 0 && reserve < sms) NEST_CUBLAS(cublasSetSmCountTarget(t->h, sms - reserve));
+    if (reserve > 0 && reserve < sms) {
+      NEST_CUBLAS(cublasSetSmCountTarget(t->h, sms - reserve));
+      t->sm_target = sms - reserve;
+    }
   }
+  NEST_CUBLAS(cublasLtCreate(&t->lt));
   for (int l = 0; l < L; ++l) {
     const int64_t fan_in = l == 0 ? in0 : H;
     k_fill_bf16<<<1024, 256>>>(t->w + t->woff[l], int64_t(H) * fan_in, 1000 + l, 1.f / std::sqrt(float(fan_in)));
@@ -120,17 +137,87 @@ void tower_destroy(Ctx& c) {
   Tower* t = reinterpret_cast<Tower*>(c.tower);
   if (!t) return;
   if (t->h) cublasDestroy(t->h);
+  for (auto& kv : t->plans) {
+    cublasLtMatmulDescDestroy(kv.second.op);
+    cublasLtMatrixLayoutDestroy(kv.second.a);
+    cublasLtMatrixLayoutDestroy(kv.second.b);
+    cublasLtMatrixLayoutDestroy(kv.second.c);
+  }
+  if (t->lt) cublasLtDestroy(t->lt);
   delete t;
   c.tower = nullptr;
 }
 
-// row-major C[M,N] = op(A)[M,K] * op(B)[K,N]
+// row-major C[M,N] = op(A)[M,K] * op(B)[K,N] through cublasLt.  The first call
+// of every shape times the top heuristic algorithms on the real buffers and
+// keeps the fastest (one-time autotune; the bench's warm-up absorbs it).
+
+static GemmPlan& plan_for(Tower* t, bool ta, bool tb, int M, int N, int K, int lda, int ldb, int ldc,
+                          cudaDataType ctype) {
+  const std::string key = std::to_string(ta) + "," + std::to_string(tb) + "," + std::to_string(M) + "," +
+                          std::to_string(N) + "," + std::to_string(K) + "," + std::to_string(int(ctype));
+  auto it = t->plans.find(key);
+  if (it != t->plans.end()) return it->second;
+  GemmPlan p;
+  NEST_CUBLAS(cublasLtMatmulDescCreate(&p.op, CUBLAS_COMPUTE_32F, CUDA_R_32F));
+  // column-major view: C^T[N,M] = op(B)^T[N,K] * op(A)^T[K,M]
+  const cublasOperation_t oa = tb ? CUBLAS_OP_T : CUBLAS_OP_N, ob = ta ? CUBLAS_OP_T : CUBLAS_OP_N;
+  NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &oa, sizeof(oa)));
+  NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &ob, sizeof(ob)));
+  if (t->sm_target > 0)
+    NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_SM_COUNT_TARGET, &t->sm_target,
+                                               sizeof(t->sm_target)));
+  NEST_CUBLAS(cublasLtMatrixLayoutCreate(&p.a, CUDA_R_16BF, oa == CUBLAS_OP_N ? N : K, oa == CUBLAS_OP_N ? K : N, ldb));
+  NEST_CUBLAS(cublasLtMatrixLayoutCreate(&p.b, CUDA_R_16BF, ob == CUBLAS_OP_N ? K : M, ob == CUBLAS_OP_N ? M : K, lda));
+  NEST_CUBLAS(cublasLtMatrixLayoutCreate(&p.c, ctype, N, M, ldc));
+  return t->plans.emplace(key, p).first->second;
+}
+
 static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void* A, int lda,
-                    const void* B, int ldb, void* C, int ldc, cudaDataType ctype) {
+                    const void* B, int ldb, void* C, int ldc, cudaDataType ctype, cudaStream_t st) {
   const float alpha = 1.f, beta = 0.f;
-  NEST_CUBLAS(cublasGemmEx(t->h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, N, M, K,
-                           &alpha, B, CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C, ctype, ldc,
-                           CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
+  GemmPlan& p = plan_for(t, ta, tb, M, N, K, lda, ldb, ldc, ctype);
+  if (!p.have_algo) {
+    cublasLtMatmulPreference_t pref;
+    NEST_CUBLAS(cublasLtMatmulPreferenceCreate(&pref));
+    NEST_CUBLAS(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &t->ws_bytes,
+                                                     sizeof(t->ws_bytes)));
+    cublasLtMatmulHeuristicResult_t res[8];
+    int n = 0;
+    NEST_CUBLAS(cublasLtMatmulAlgoGetHeuristic(t->lt, p.op, p.a, p.b, p.c, p.c, pref, 8, res, &n));
+    cublasLtMatmulPreferenceDestroy(pref);
+    NEST_CHECK(n > 0, NEST_ERR_CUDA, "no cublasLt algorithm for a tower GEMM");
+    cudaEvent_t e0, e1;
+    NEST_CUDA(cudaEventCreate(&e0));
+    NEST_CUDA(cudaEventCreate(&e1));
+    float best = 1e30f;
+    int bi = 0;
+    for (int i = 0; i < n; ++i) {
+      if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
+      bool ok = true;
+      for (int rep = 0; rep < 3 && ok; ++rep) {  // warm + 2 timed
+        if (rep == 1) cudaEventRecord(e0, st);
+        ok = cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &res[i].algo, t->ws,
+                            t->ws_bytes, st) == CUBLAS_STATUS_SUCCESS;
+      }
+      if (!ok) continue;
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) {
+        best = ms;
+        bi = i;
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    NEST_CHECK(best < 1e29f, NEST_ERR_CUDA, "no working cublasLt algorithm for a tower GEMM");
+    p.algo = res[bi].algo;
+    p.have_algo = true;
+  }
+  NEST_CUBLAS(cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, t->ws,
+                             t->ws_bytes, st));
 }
 
 void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st) {
@@ -146,23 +233,23 @@ void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStrea
   for (int l = 0; l < L - 1; ++l) {
     const int in = l == 0 ? in0 : H;
     gemm_rm(t, false, true, M, H, in, t->x + t->xoff[l], in, t->w + t->woff[l], in, t->x + t->xoff[l + 1], H,
-            CUDA_R_16BF);
+            CUDA_R_16BF, st);
   }
   {  // last layer forward (output discarded: dY_L is the fixed gradient)
     const int in = L == 1 ? in0 : H;
     gemm_rm(t, false, true, M, H, in, t->x + t->xoff[L - 1], in, t->w + t->woff[L - 1], in, t->dy[1], H,
-            CUDA_R_16BF);
+            CUDA_R_16BF, st);
   }
   // backward
   const __nv_bfloat16* dy = t->gtop;
   int cur = 0;
   for (int l = L - 1; l >= 0; --l) {
     const int in = l == 0 ? in0 : H;
-    gemm_rm(t, true, false, H, in, M, dy, H, t->x + t->xoff[l], in, t->dw, in, CUDA_R_16BF);  // dW_l
+    gemm_rm(t, true, false, H, in, M, dy, H, t->x + t->xoff[l], in, t->dw, in, CUDA_R_16BF, st);  // dW_l
     if (l == 0) {
-      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, dout, in, CUDA_R_32F);  // dX_0 (fp32)
+      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, dout, in, CUDA_R_32F, st);  // dX_0 (fp32)
     } else {
-      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, t->dy[cur], in, CUDA_R_16BF);
+      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, t->dy[cur], in, CUDA_R_16BF, st);
       dy = t->dy[cur];
       cur ^= 1;
     }

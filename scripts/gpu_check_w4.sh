@@ -1,0 +1,12 @@
+timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1 --master-port 29811 tests/mgpu_worker.py > gpurun_out/mgpu_w4.log 2>&1; echo mgpu_w4_rc=$?; grep -E "ALL OK|FAIL|mismatch|Error" gpurun_out/mgpu_w4.log | head -5
+for N in 1 2 4; do
+timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1 --master-port $((29820+N)) bench.py --gpus 4 --steps 30 --warmup 3 --no-e2e --micro-batches $N > gpurun_out/w4_n$N.log 2>&1; echo N=$N rc=$?
+done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob("gpurun_out/w4_n*.log")):
+    try:
+        l=[x for x in open(f) if x.startswith("{")][-1]; d=json.loads(l); a=d["a2a"]; st=d["stages"]
+        print(f.split('/')[-1], round(d["value"]/1e6,2), "Msps", round(d["ms_per_step"],3), "ms | a2a", round(a["physical_ms_per_step"],3), "exp", round(a["exposed_ms_per_step"],3), "GB/s", round(a["nvlink_gbs_per_gpu"],1), "| nofwp", a["without_fwp"], "| tower", round(st["tower"]["ms_per_step"],3), "pool", round(st["pool"]["ms_per_step"],3), "seg", round(st["segsum"]["ms_per_step"],3), "sg", round(st["send_gather"]["ms_per_step"],3), "upd", round(st["update"]["ms_per_step"],3))
+    except Exception as e: print(f, "err", e)
+PY
