@@ -225,6 +225,20 @@ static void lookup_comm(Ctx& c, Slot& s, int mb, cudaStream_t cs, cudaStream_t m
     NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_gather, 0));
   }
   const double row = double(c.D) * sizeof(float);
+  if (c.a2a_mode == A2A_FUSED) {
+    // R6 + R7 in one kernel: gather rows of the frozen buffer and store them
+    // straight into every requester's receive rows over NVLink
+    {
+      ProfScope ps(c, ST_EMB_A2A, SK_COMM, ms);
+      launch_send_push(c, s, mb, ms);
+      int64_t self = s.all[(size_t(c.rank) * c.W + c.rank) * (c.Nmax + 2) + 1 + mb];
+      ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+    }
+    NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
+    xfer_signal(c, s, 0, mb, ms);
+    s.prefetched |= 1u << mb;
+    return;
+  }
   {
     ProfScope ps(c, ST_SEND_GATHER, SK_COMM, ms);
     launch_send_gather(c, s, mb, ms);
@@ -510,13 +524,40 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
     cudaStream_t cs = S(compute), ms = S(comm);
     Slot& other = c->slot[1 - slot];
     const double row = double(c->D) * sizeof(float);
+    const bool fused = c->a2a_mode == A2A_FUSED;
     {
-      ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
-      launch_segsum(*c, s, mb, dout, cs);
+      ProfScope ps(*c, fused ? ST_GRAD_A2A : ST_SEGSUM, SK_COMPUTE, cs);
+      if (fused) {
+        // R10 + R11 in one pass: each key's gradient row is stored straight
+        // into its owner's receive rows (peer memory over NVLink)
+        const int W = c->W, Nc = c->Nmax + 2;
+        PeerRows out{};
+        int64_t acc = 0;
+        for (int o = 0; o < W; ++o) {   // owner-major positions of the micro-batch's keys
+          int64_t dst = own_base_at(s, *c, o, mb);
+          for (int r = 0; r < c->rank; ++r) dst += s.all[(size_t(r) * W + o) * Nc + 1 + mb];
+          out.base[o] = c->peer_own[o] + dst * c->D;
+          out.off[o] = int32_t(acc);
+          acc += s.all[(size_t(c->rank) * W + o) * Nc + 1 + mb];
+        }
+        out.off[W] = int32_t(acc);
+        out.n = W;
+        out.fence = 1;
+        launch_segsum_to(*c, s, mb, dout, out, cs);
+        xfer_signal(*c, s, 1, mb, cs);
+      } else {
+        launch_segsum(*c, s, mb, dout, cs);
+      }
       ps.launches = s.info.mb_uniq[mb] > 0 ? 7 : 0;
-      // gradient rows read + 4 K_i + U_{s,i} rows written
-      ps.bytes = row * double(s.info.mb_out_rows[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
-                 row * double(s.info.mb_uniq[mb]);
+      if (fused) {
+        // accounted as the gradient All2All: rows stored off-GPU
+        const int64_t self = s.all[(size_t(c->rank) * c->W + c->rank) * (c->Nmax + 2) + 1 + mb];
+        ps.bytes = row * double(s.info.mb_uniq[mb] - self);
+      } else {
+        // gradient rows read + 4 K_i + U_{s,i} rows written
+        ps.bytes = row * double(s.info.mb_out_rows[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
+                   row * double(s.info.mb_uniq[mb]);
+      }
     }
     // sum_i R_{o,i} gradient rows + U_o buffer rows read + U_o rows
     // written back (the survey's third U_o row, the buffer rewrite, is not needed:
@@ -532,7 +573,7 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
         scnt[p] = s.all[(size_t(c->rank) * c->W + p) * Nc + 1 + mb];  // requester -> owner p
         rcnt[p] = s.all[(size_t(p) * c->W + c->rank) * Nc + 1 + mb];  // from requester p
       }
-      {
+      if (!fused) {
         ProfScope ps(*c, ST_GRAD_A2A, SK_COMM, ms);
         if (c->xfer_ce)
           xfer_push_grad(*c, s, mb, ms);

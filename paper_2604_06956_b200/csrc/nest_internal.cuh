@@ -185,8 +185,9 @@ struct Ctx {
   Slot slot[2];
   uint32_t epoch = 0;
   int seg_chunk = 32;              // segment-sum: cold threshold = hot chunk length (>= 32)
-  // copy-engine All2All transport (xfer.cu)
-  bool xfer_ce = false;
+  // copy-engine / fused All2All transports (xfer.cu)
+  bool xfer_ce = false;            // peer windows mapped (CE or fused mode)
+  int a2a_mode = 0;                // A2AMode
   void* xwin = nullptr;            // library-owned, IPC-exported exchange window
   size_t xwin_bytes = 0, xoff_own = 0, xoff_flags = 0;
   uint32_t* xflags = nullptr;      // [2][Nmax][W] epoch flags written by peers
@@ -463,6 +464,22 @@ struct ProfScope {
   ProfScope(Ctx& cc, int stage, int kind, cudaStream_t s) : c(cc), id(prof_begin(cc, stage, kind, s)), st(s) {}
   ~ProfScope() { prof_end(c, id, st, bytes, dcount, bpc, launches); }
 };
+// output maps of the fused gather->NVLink-put kernels (rows.cu): position p of
+// a micro-batch's (owner- or source-major) row list goes to row
+// base[s] + (p - off[s]) with off[s] <= p < off[s+1]
+struct PeerRows {
+  float* base[NEST_MAX_WORLD];
+  int32_t off[NEST_MAX_WORLD + 1];
+  int32_t n;          // number of segments (W, or 1 for a purely local map)
+  int32_t fence;      // 1: writes go to peer memory (system fence at the end)
+};
+enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
+int a2a_mode_wanted(int W);
+int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb);
+int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb);
+void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st);
+void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st);
 // copy-engine transport (xfer.cu)
 bool xfer_wanted(int W);
 void xfer_setup(Ctx& c, cudaStream_t st);

@@ -267,21 +267,30 @@ __device__ __forceinline__ void sum_rows(const int32_t* __restrict__ sval, int64
   }
 }
 
+// destination row of position p under a PeerRows map (local or a peer's window)
+__device__ __forceinline__ float* map_row(const PeerRows& m, int64_t p, int D) {
+  int s = 0;
+  while (s + 1 < m.n && m.off[s + 1] <= p) ++s;
+  return m.base[s] + (p - m.off[s]) * D;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, int chunk,
                                                              const int32_t* __restrict__ seg_start,
                                                              const int32_t* __restrict__ sval,
                                                              const float* __restrict__ dout,
-                                                             float* __restrict__ g) {
+                                                             const PeerRows out) {
   Grp<D> gp;
   for (int64_t k = gp.g; k < Ui; k += gp.ng) {
     const int64_t a = seg_start[k], b = seg_start[k + 1];
     if (b - a > chunk) continue;
     float4 acc[RowGeom<D>::VPL];
     sum_rows<D>(sval, a, b, dout, gp, acc);
+    float* g = map_row(out, k, D);
 #pragma unroll
-    for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(g + k * D + gp.col(v), acc[v]);
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(g + gp.col(v), acc[v]);
   }
+  if (out.fence) __threadfence_system();
 }
 
 template <int D>
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_chunks(
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
     const int32_t* __restrict__ tot, const int32_t* __restrict__ hot_list,
-    const int32_t* __restrict__ hot_ppos, const float* __restrict__ partial, float* __restrict__ g) {
+    const int32_t* __restrict__ hot_ppos, const float* __restrict__ partial, const PeerRows out) {
   using G = RowGeom<D>;
   constexpr int NG = (kRowThreads / 32) * G::GPW;  // groups per block
   __shared__ float4 red[NG][G::kVec];
@@ -334,18 +343,74 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
     for (int v = 0; v < G::VPL; ++v) red[grp][v * G::L + l] = acc[v];
     __syncthreads();
     if (grp == 0) {
+      float* g = map_row(out, k, D);
 #pragma unroll
       for (int v = 0; v < G::VPL; ++v) {
         float4 s = red[0][v * G::L + l];
         for (int q = 1; q < NG; ++q) s = f4add(s, red[q][v * G::L + l]);
-        st_f4(g + int64_t(k) * D + (v * G::L + l) * 4, s);
+        st_f4(g + (v * G::L + l) * 4, s);
       }
     }
     __syncthreads();
   }
+  if (out.fence) __threadfence_system();
 }
 
+// local gradient rows of micro-batch mb (NCCL / CE transports send them)
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) {
+  PeerRows out{};
+  out.base[0] = c.src_rows + s.src_base[mb] * c.D;
+  out.off[0] = 0;
+  out.off[1] = int32_t(s.info.mb_uniq[mb]);
+  out.n = 1;
+  out.fence = 0;
+  launch_segsum_to(c, s, mb, dout, out, st);
+}
+
+// R6 + R7 fused: the owner's gather writes every requested row straight into
+// the requester's receive rows (peer memory over NVLink; own rows locally)
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, const int64_t* __restrict__ recv,
+                                                           const int32_t* __restrict__ owner_inv,
+                                                           const int32_t* __restrict__ sendpos,
+                                                           const float* __restrict__ buffer, const PeerRows out) {
+  Grp<D> gp;
+  for (int64_t r = gp.g; r < R; r += gp.ng) {
+    if (!((uint64_t(__ldg(recv + r)) >> (56 + mb)) & 1u)) continue;
+    float* dst = map_row(out, __ldg(sendpos + r), D);
+    const float* src = buffer + int64_t(__ldg(owner_inv + r)) * D;
+#pragma unroll
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(dst + gp.col(v), ldg_f4(src + gp.col(v)));
+  }
+  __threadfence_system();
+}
+
+void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
+  const int64_t R = s.info.recv;
+  if (R == 0) return;
+  const int W = c.W, Nc = c.Nmax + 2;
+  PeerRows out{};
+  int64_t acc = 0;
+  for (int p = 0; p < W; ++p) {      // source-major send positions
+    int64_t dst = src_base_at(s, c, p, mb);
+    for (int o = 0; o < c.rank; ++o) dst += s.all[(size_t(p) * W + o) * Nc + 1 + mb];
+    out.base[p] = c.peer_src[p] + dst * c.D;
+    out.off[p] = int32_t(acc);
+    acc += s.all[(size_t(p) * W + c.rank) * Nc + 1 + mb];
+  }
+  out.off[W] = int32_t(acc);
+  out.n = W;
+  out.fence = 1;
+  const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    k_send_push<D><<<blocks_for_rows(R, rpb, 148 * 16), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
+                                                                              s.buffer, out);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st) {
   const int64_t Ui = s.info.mb_uniq[mb];
   const int64_t Ki = s.info.mb_nnz[mb];
   if (Ui == 0) return;
@@ -353,7 +418,6 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
   const int32_t* sval = s.sval + s.q0[mb];
   const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
   const uint32_t umask = (1u << s.ubits) - 1u;
-  float* g = c.src_rows + s.src_base[mb] * c.D;
   int32_t* seg = c.seg_start;
   k_seg_heads<<<blocks_for_rows(Ki, 256, 148 * 16), 256, 0, st>>>(Ki, skey, umask, pos, seg, Ui);
   // hot-segment bookkeeping: (is_hot, chunks) prefix -> hot_list, hot_ppos
@@ -380,10 +444,10 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
       c.scan_tmp_win, st);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_segsum_cold<D><<<blocks_for_rows(Ui, rpb, 148 * 16), kRowThreads, 0, st>>>(Ui, chunk, seg, sval, dout, g);
+    k_segsum_cold<D><<<blocks_for_rows(Ui, rpb, 148 * 16), kRowThreads, 0, st>>>(Ui, chunk, seg, sval, dout, out);
     k_segsum_hot_chunks<D><<<148 * 4, kRowThreads, 0, st>>>(chunk, tot, hot_list, hot_ppos, seg, sval, dout,
                                                             c.partial);
-    k_segsum_hot_final<D><<<148 * 2, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, g);
+    k_segsum_hot_final<D><<<148 * 2, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, out);
   });
   NEST_LAUNCH_CHECK();
   (void)skey;

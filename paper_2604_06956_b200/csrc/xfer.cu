@@ -42,11 +42,16 @@ static void load_driver_ops() {
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// NEST_A2A=nccl selects grouped ncclSend/ncclRecv instead (the baseline)
-bool xfer_wanted(int W) {
+// NEST_A2A = fused (default: gather / segment-sum kernels store straight into
+// peer memory), ce (copy engines), nccl (grouped ncclSend/ncclRecv, the baseline)
+int a2a_mode_wanted(int W) {
+  if (W <= 1) return A2A_NCCL;
   const char* e = std::getenv("NEST_A2A");
-  return W > 1 && !(e && std::strcmp(e, "nccl") == 0);
+  if (e && std::strcmp(e, "nccl") == 0) return A2A_NCCL;
+  if (e && std::strcmp(e, "ce") == 0) return A2A_CE;
+  return A2A_FUSED;
 }
+bool xfer_wanted(int W) { return a2a_mode_wanted(W) != A2A_NCCL; }
 
 // window layout: [src_rows MBcap*D f32 | own_rows OMBcap*D f32 | flags 2*Nmax*W u32]
 void xfer_setup(Ctx& c, cudaStream_t st) {
@@ -101,6 +106,7 @@ void xfer_setup(Ctx& c, cudaStream_t st) {
   // (no barrier needed: the first push happens after the first route's count
   // exchange, a collective every rank enters after this setup)
   c.xfer_ce = true;
+  c.a2a_mode = a2a_mode_wanted(c.W);
 }
 
 void xfer_destroy(Ctx& c) {
@@ -117,14 +123,14 @@ static inline size_t flag_index(const Ctx& c, int kind, int mb, int src) {
 
 // rows: [W][W][Nc] counts of the slot; base_of(p, i) = row base of micro-batch
 // i in rank p's requester (kind 0) / owner (kind 1) rows
-static int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb) {
+int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb) {
   const int Nc = c.Nmax + 2;
   int64_t b = 0;
   for (int i = 0; i < mb; ++i)
     for (int o = 0; o < c.W; ++o) b += s.all[(size_t(p) * c.W + o) * Nc + 1 + i];
   return b;
 }
-static int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb) {
+int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb) {
   const int Nc = c.Nmax + 2;
   int64_t b = 0;
   for (int i = 0; i < mb; ++i)
@@ -157,6 +163,18 @@ void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_s
     if (p == me) continue;
     CUresult r = g_write(reinterpret_cast<CUstream>(st),
                          reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, 0, mb, me)),
+                         cuuint32_t(s.epoch), 0);
+    NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+}
+
+// epoch flag of (kind, mb) written into every peer after the preceding work
+// on st (the fused kernels end with a system-scope fence)
+void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st) {
+  for (int p = 0; p < c.W; ++p) {
+    if (p == c.rank) continue;
+    CUresult r = g_write(reinterpret_cast<CUstream>(st),
+                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, kind, mb, c.rank)),
                          cuuint32_t(s.epoch), 0);
     NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWriteValue32 failed");
   }
