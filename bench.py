@@ -43,9 +43,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="dlrm", choices=["dlrm", "tiny", "dbp_stress"])
+    ap.add_argument("--config", default="dlrm", choices=["dlrm", "tiny", "dbp_stress", "genrec"])
+    ap.add_argument("--zipf", type=float, default=0.0, help="override the config's Zipf skew (FWP sweep)")
+    ap.add_argument("--reuse", type=float, default=0.0,
+                    help="DBP stress: batch t+1 reuses each key slot of batch t with this probability")
+    ap.add_argument("--correlated", default="", help="G,rho: correlated sample groups (FWP clustering sweep)")
     ap.add_argument("--micro-batches", type=int, default=0,
-                    help="FWP micro-batches N; 0 = auto: 1 at one GPU (no All2All to hide), 2 otherwise")
+                    help="FWP micro-batches N; 0 = auto (1; N = 2 is measured alongside)")
     ap.add_argument("--schedule", default="sequential", choices=["sequential", "clustered"])
     ap.add_argument("--variant", default="et", choices=["et", "e"],
                     help="et: embedding + stand-in tower (FWP overlap partner); e: embedding only")
@@ -118,7 +122,12 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- workload
-def rank_batches(cfg, seed, rank, P):
+def rank_batches(cfg, seed, rank, P, args=None):
+    if args is not None and args.reuse > 0:
+        return WL.gen_overlap_batches(cfg, seed, P, rank, args.reuse)
+    if args is not None and args.correlated:
+        g, rho = args.correlated.split(",")
+        return [WL.gen_correlated_batch(cfg, seed, t, rank, groups=int(g), rho=float(rho)) for t in range(P)]
     return [WL.gen_batch(cfg, seed, t, rank) for t in range(P)]
 
 
@@ -185,13 +194,20 @@ def config_json(args, cfg, world):
 def main():
     args = parse()
     cfg = WL.CONFIGS[args.config]
+    if args.zipf > 0:
+        cfg = cfg.with_(zipf=args.zipf)
+    if cfg.pooling == "none":
+        args.variant = "e"     # the stand-in tower is defined on pooled rows only
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and "RANK" in os.environ:
         pass  # torchrun decides
     if args.micro_batches <= 0:
-        args.micro_batches = 1 if world == 1 else 2
+        # measured best at W = 1, 2, 4 on B200: hiding the
+        # All2All behind the tower costs as much compute as it hides, so the
+        # default runs one micro-batch and reports N = 2 alongside
+        args.micro_batches = 1
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
@@ -208,19 +224,31 @@ def main():
 
     N = args.micro_batches
     B, F, d = cfg.batch_local, cfg.num_features, cfg.dim
-    batches = rank_batches(cfg, args.seed, rank, args.batches)
+    batches = rank_batches(cfg, args.seed, rank, args.batches, args)
     K = max(len(k) for k, _ in batches)
+    # capacities from the actual batches: unique keys per batch bound the
+    # received keys per owner (balanced by the row mod W rule) and the rows
+    # exchanged per micro-batch (sum_i U_{s,i} <= min(K, N * U_s))
+    U = max(len(np.unique(k)) for k, _ in batches)
+    if world > 1:
+        import torch.distributed as dist_
+        t = torch.tensor([U], device=dev)
+        dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
+        U = int(t.item())
+    Nctx = max(N, 2) if world > 1 else N      # room for the FWP comparison run
+    mb_rows = min(K, Nctx * U) + 1024
     uids = None
     if world > 1:
         obj = [unique_ids() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uids = obj[0]
     ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, pooling=cfg.pooling, max_keys=K + 1024,
-                      max_batch=B, max_micro_batches=N, seed=args.seed + 1, init_mode="uniform",
+                      max_batch=B, max_micro_batches=Nctx, seed=args.seed + 1, init_mode="uniform",
                       tower_layers=cfg.tower_layers if args.variant == "et" else 0,
                       tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev,
-                      max_recv_keys=(int(1.6 * K) if world > 1 else 0),
-                      max_owner_mb_rows=(int(1.6 * K) if world > 1 else 0))
+                      max_recv_keys=int(1.5 * U) + 1024 if world > 1 else U + 1024,
+                      max_mb_rows=mb_rows,
+                      max_owner_mb_rows=int(1.5 * mb_rows) if world > 1 else 0)
     torch.cuda.synchronize()
     # inputs resident in HBM (value) and pinned host copies (e2e)
     dev_b = [(torch.from_numpy(k).to(dev), torch.from_numpy(o).to(dev), B) for k, o in batches]
@@ -303,6 +331,11 @@ def main():
     ms, prof, _, _ = timed(runner, args.steps, args.warmup, profile=True)
     clk = clocks.stop()
     value = B * world * args.steps / (ms / 1e3)
+    # FWP payload of the last routed batch: sum_i |K(M_i)| vs |K(B)|
+    info = ctx.slot_info(runner.t % 2)
+    fwp_stats = {"N": N, "schedule": args.schedule, "uniq_keys": int(info.uniq),
+                 "sum_mb_uniq": int(sum(info.mb_uniq[i] for i in range(N))),
+                 "alpha": (sum(info.mb_uniq[i] for i in range(N)) / info.uniq) if info.uniq else None}
 
     # e2e through the public API with host inputs (copies inside the timed region)
     e2e = None
@@ -317,16 +350,21 @@ def main():
                "d2h_bytes_per_step": d2h // args.steps + counts_bytes,
                "ms_per_step": ms_e / args.steps}
 
-    # exposed All2All without FWP (N = 1) for comparison
-    no_fwp = None
-    if world > 1 and not args.no_fwp_compare and N > 1:
-        r1 = Runner(ctx, N=1, schedule="sequential", pipelined=True, lr_over_B=lr)
-        r1.t = runner.t + args.steps
-        timed(r1, 3, r1.t)
-        ms1, prof1, _, _ = timed(r1, max(5, args.steps // 2), r1.t, profile=True)
-        no_fwp = {"ms_per_step": ms1 / max(5, args.steps // 2),
-                  "a2a_exposed_ms_per_step": prof1["summary"]["a2a_exposed_ms"] / max(5, args.steps // 2),
-                  "a2a_ms_per_step": prof1["summary"]["a2a_ms"] / max(5, args.steps // 2)}
+    # exposed All2All with and without FWP: the same step at the other N
+    # (N = 2 micro-batches when the main run is N = 1, N = 1 otherwise)
+    other_fwp = None
+    if world > 1 and not args.no_fwp_compare:
+        N2 = 2 if N == 1 else 1
+        if N2 <= ctx.cfg.max_micro_batches:
+            r1 = Runner(ctx, N=N2, schedule=args.schedule if N2 > 1 else "sequential", pipelined=True,
+                        lr_over_B=lr)
+            r1.t = runner.t + args.steps
+            timed(r1, 3, r1.t)
+            k2 = max(5, args.steps // 2)
+            ms1, prof1, _, _ = timed(r1, k2, r1.t, profile=True)
+            other_fwp = {"N": N2, "ms_per_step": ms1 / k2, "samples_per_s": B * world * k2 / (ms1 / 1e3),
+                         "a2a_exposed_ms_per_step": prof1["summary"]["a2a_exposed_ms"] / k2,
+                         "a2a_ms_per_step": prof1["summary"]["a2a_ms"] / k2}
 
     if rank == 0:
         hbm_peak, bf16_peak, src = peaks()
@@ -374,7 +412,12 @@ def main():
                    "nvlink_gbs_per_gpu": a2a_bytes / (a2a_ms * 1e6) if a2a_ms else None,
                    "frac_of_peer_770": (a2a_bytes / (a2a_ms * 1e6)) / NVLINK_PEER_GBS if a2a_ms else None,
                    "frac_of_nominal_900": (a2a_bytes / (a2a_ms * 1e6)) / NVLINK_NOMINAL_GBS if a2a_ms else None,
-                   "without_fwp": no_fwp}
+                   # all-to-all ceiling measured by scripts/p2p_probe.cu (SM remote
+                   # stores, every GPU exchanging with every other): 691 GB/s at
+                   # 2 GPUs, 403 GB/s at 4 GPUs per GPU per direction
+                   "probe_all2all_ceiling_gbs": {2: 691.2, 4: 403.3}.get(world),
+                   "transport": os.environ.get("NEST_A2A", "fused"),
+                   "compare_other_N": other_fwp}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, args.seed)
@@ -385,7 +428,13 @@ def main():
                 "e2e": e2e, "gpu_launches": int(summ["launches"]), "clocks": clk, "a2a": a2a,
                 "stages": stages,
                 "trace": {"span_ms_per_step": summ["span_ms"] / steps,
-                          "compute_busy_ms_per_step": summ["compute_busy_ms"] / steps}}
+                          "compute_busy_ms_per_step": summ["compute_busy_ms"] / steps},
+                "dbp": {"refresh_ms_per_step": st["refresh"]["ms"] / max(1, st["refresh"]["records"]),
+                        "refreshed_rows_per_step": st["refresh"]["units"] / max(1, st["refresh"]["records"]),
+                        "owner_unique_per_step": st["gather"]["units"] / max(1, st["gather"]["records"]),
+                        "intersection_ratio": (st["refresh"]["units"] / st["gather"]["units"]
+                                               if st["gather"]["units"] else None)},
+                "fwp": fwp_stats}
         if args.trace:
             json.dump({"stages": st, "summary": summ}, open(args.trace, "w"), indent=1)
         print(json.dumps(line), flush=True)

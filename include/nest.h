@@ -88,8 +88,9 @@ typedef struct {
   int64_t max_keys;           /* K cap: key occurrences per rank per batch (< 2^28) */
   int64_t max_batch;          /* B cap: samples per rank per batch */
   int32_t max_micro_batches;  /* N cap, 1..NEST_MAX_MICRO_BATCHES */
-  int64_t max_recv_keys;      /* R_o cap: keys an owner receives per batch (default 2*max_keys, clamped to shard rows*W) */
-  int64_t max_owner_keys;     /* U_o cap: owner-unique keys (default min(max_recv_keys, shard rows)) */
+  int64_t max_recv_keys;      /* R_o cap: keys an owner receives per batch (default max_keys at W=1,
+                                 min(2, W) * max_keys otherwise); sizes the owner buffers */
+  int64_t max_owner_keys;     /* reserved (U_o cap is derived: min(max_recv_keys, shard rows)) */
   int64_t max_mb_rows;        /* cap of sum_i U_{s,i} (rows a source receives over all micro-batches; default max_keys) */
   int64_t max_owner_mb_rows;  /* cap of sum_i R_{o,i} (rows an owner sends over all micro-batches; default max_recv_keys*N clamped) */
   uint64_t seed;              /* PRF seed of the table initialisation */
@@ -266,6 +267,8 @@ typedef struct {
   double ms;            /* summed event-measured durations */
   double bytes;         /* summed algorithmic bytes; FLOPs for `tower`;
                            off-GPU bytes for the All2All stages */
+  double units;         /* summed device-side counts: refreshed rows I (refresh),
+                           owner-unique keys U_o (gather, update, owner_dedup) */
 } nest_profile_stage_t;
 
 typedef struct {

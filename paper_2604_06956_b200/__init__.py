@@ -162,7 +162,8 @@ class NestContext:
         out = {"stages": {}, "summary": {k: getattr(summ, k) for k, _ in L.ProfileSummary._fields_}}
         for s in stages:
             out["stages"][s.name.decode()] = {"stream": s.stream, "records": s.records,
-                                              "launches": s.launches, "ms": s.ms, "bytes": s.bytes}
+                                              "launches": s.launches, "ms": s.ms, "bytes": s.bytes,
+                                              "units": s.units}
         return out
 
     def route_view(self, slot: int) -> dict:

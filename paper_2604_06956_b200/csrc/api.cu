@@ -62,12 +62,12 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
   c.owords = (c.Vo + 31) / 32;
   c.Kcap = cfg->max_keys;
   c.Bcap = cfg->max_batch;
-  if (c.W == 1) {
-    c.Rcap = c.Kcap;
-  } else {
-    c.Rcap = cfg->max_recv_keys > 0 ? cfg->max_recv_keys : std::min<int64_t>(2 * c.Kcap, c.W * c.Kcap);
-  }
+  if (cfg->max_recv_keys > 0)
+    c.Rcap = cfg->max_recv_keys;
+  else
+    c.Rcap = c.W == 1 ? c.Kcap : std::min<int64_t>(2 * c.Kcap, c.W * c.Kcap);
   NEST_CHECK(c.Rcap < (int64_t(1) << 31) - 64, NEST_ERR_INVALID, "max_recv_keys too large");
+  // U_o <= R_o <= Rcap and U_o <= shard rows, so this never overflows
   c.Uocap = std::max<int64_t>(1, std::min<int64_t>(c.Rcap, c.Vo));
   c.MBcap = cfg->max_mb_rows > 0 ? cfg->max_mb_rows : c.Kcap;
   if (c.W == 1)

@@ -122,7 +122,10 @@ void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* 
     g.launches += r.launches;
     g.ms += double(t1) - double(t0);
     double bytes = r.bytes;
-    if (r.cidx >= 0) bytes += r.bytes_per_cnt * double(p.hcnt[r.cidx]);
+    if (r.cidx >= 0) {
+      bytes += r.bytes_per_cnt * double(p.hcnt[r.cidx]);
+      g.units += double(p.hcnt[r.cidx]);
+    }
     g.bytes += bytes;
     t_min = std::min(t_min, double(t0));
     t_max = std::max(t_max, double(t1));

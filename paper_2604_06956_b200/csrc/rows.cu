@@ -26,6 +26,20 @@ static inline int blocks_for_rows(int64_t rows, int rows_per_block, int max_bloc
 
 constexpr int kRowThreads = 256;
 
+// grid cap of the window's embedding-lane kernels (pool, segment-sum, send),
+// which FWP runs concurrently with the dense tower: NEST_EMB_MAX_BLOCKS
+static int emb_cap() {
+  static int cap = [] {
+    const char* e = std::getenv("NEST_EMB_MAX_BLOCKS");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 148 * 16;
+  }();
+  return cap;
+}
+static inline int emb_blocks(int64_t rows, int rows_per_block) {
+  return blocks_for_rows(rows, rows_per_block, emb_cap());
+}
+
 // group id / count helpers for grid-stride loops over rows
 template <int D>
 struct Grp {
@@ -113,7 +127,7 @@ void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st) {
   const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_send_gather<D><<<blocks_for_rows(R, rpb, 148 * 16), kRowThreads, 0, st>>>(
+    k_send_gather<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(
         R, mb, s.recv, s.owner_inv, sp, s.buffer, out);
   });
   NEST_LAUNCH_CHECK();
@@ -199,17 +213,17 @@ void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
     if (c.cfg.pooling == NEST_POOL_SUM) {
       const int64_t nrows = int64_t(s.cap) * c.F;
       if (w1)
-        k_pool<D, true><<<blocks_for_rows(nrows, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        k_pool<D, true><<<emb_blocks(nrows, rpb), kRowThreads, 0, st>>>(
             nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
       else
-        k_pool<D, false><<<blocks_for_rows(nrows, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        k_pool<D, false><<<emb_blocks(nrows, rpb), kRowThreads, 0, st>>>(
             nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
     } else {
       if (w1)
-        k_expand_rows<D, true><<<blocks_for_rows(s.cap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        k_expand_rows<D, true><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
             s.cap, c.F, perm_mb, s.bag_off, s.samp_base, s.inverse, pos, src, out);
       else
-        k_expand_rows<D, false><<<blocks_for_rows(s.cap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        k_expand_rows<D, false><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
             s.cap, c.F, perm_mb, s.bag_off, s.samp_base, s.inverse, pos, src, out);
     }
   });
@@ -404,7 +418,7 @@ void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
   const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_send_push<D><<<blocks_for_rows(R, rpb, 148 * 16), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
+    k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
                                                                               s.buffer, out);
   });
   NEST_LAUNCH_CHECK();
@@ -419,7 +433,7 @@ void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows
   const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
   const uint32_t umask = (1u << s.ubits) - 1u;
   int32_t* seg = c.seg_start;
-  k_seg_heads<<<blocks_for_rows(Ki, 256, 148 * 16), 256, 0, st>>>(Ki, skey, umask, pos, seg, Ui);
+  k_seg_heads<<<emb_blocks(Ki, 256), 256, 0, st>>>(Ki, skey, umask, pos, seg, Ui);
   // hot-segment bookkeeping: (is_hot, chunks) prefix -> hot_list, hot_ppos
   int32_t* hot_list = c.hot_list;
   int32_t* hot_ppos = c.seg_aux;
@@ -444,10 +458,10 @@ void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows
       c.scan_tmp_win, st);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_segsum_cold<D><<<blocks_for_rows(Ui, rpb, 148 * 16), kRowThreads, 0, st>>>(Ui, chunk, seg, sval, dout, out);
-    k_segsum_hot_chunks<D><<<148 * 4, kRowThreads, 0, st>>>(chunk, tot, hot_list, hot_ppos, seg, sval, dout,
+    k_segsum_cold<D><<<emb_blocks(Ui, rpb), kRowThreads, 0, st>>>(Ui, chunk, seg, sval, dout, out);
+    k_segsum_hot_chunks<D><<<std::min(148 * 4, emb_cap()), kRowThreads, 0, st>>>(chunk, tot, hot_list, hot_ppos, seg, sval, dout,
                                                             c.partial);
-    k_segsum_hot_final<D><<<148 * 2, kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, out);
+    k_segsum_hot_final<D><<<std::min(148 * 2, emb_cap()), kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, out);
   });
   NEST_LAUNCH_CHECK();
   (void)skey;

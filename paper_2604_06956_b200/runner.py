@@ -22,6 +22,39 @@ import torch
 from . import NestContext
 
 
+_GREEN = {}
+
+
+def _green_streams(dev, nsm: int, sparse_prios, dense_prios):
+    """Streams on two green contexts splitting the device's SMs: `nsm` SMs for
+    the sparse lanes, the remainder for the dense lane (CUDA >= 12.4)."""
+    from cuda.bindings import driver as cu
+
+    def ok(r):
+        err, *vals = r
+        if err != cu.CUresult.CUDA_SUCCESS:
+            raise RuntimeError(f"green context setup failed: {err}")
+        return vals[0] if len(vals) == 1 else tuple(vals)
+
+    key = (dev.index, nsm)
+    if key not in _GREEN:
+        torch.cuda.init()
+        cudev = ok(cu.cuDeviceGet(dev.index))
+        res = ok(cu.cuDeviceGetDevResource(cudev, cu.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM))
+        groups, _n, rem = ok(cu.cuDevSmResourceSplitByCount(1, res, 0, nsm))
+        ctxs = []
+        for r in (groups[0], rem):
+            desc = ok(cu.cuDevResourceGenerateDesc([r], 1))
+            ctxs.append(ok(cu.cuGreenCtxCreate(desc, cudev, cu.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM)))
+        _GREEN[key] = ctxs
+    sparse_ctx, dense_ctx = _GREEN[key]
+
+    def mk(gctx, prio):
+        s = ok(cu.cuGreenCtxStreamCreate(gctx, cu.CUstream_flags.CU_STREAM_NON_BLOCKING.value, prio))
+        return torch.cuda.ExternalStream(int(s), device=dev)
+    return [mk(sparse_ctx, p) for p in sparse_prios], [mk(dense_ctx, p) for p in dense_prios]
+
+
 class Runner:
     """Drives one rank through steps.  `dout_fn(t, i, pooled_i) -> dout_i`
     supplies the loss gradient of micro-batch i on the dense stream (LIN: a
@@ -33,11 +66,27 @@ class Runner:
         self.ctx, self.N, self.schedule, self.pipelined = ctx, N, schedule, pipelined
         self.lr = lr_over_B
         dev = ctx.device
-        self.compute = torch.cuda.Stream(device=dev)            # embedding lane
-        # comm lane at high priority: its kernels are scheduled first as SMs free up
-        self.comm = torch.cuda.Stream(device=dev, priority=-1) if ctx.world > 1 else self.compute
-        self.dense = torch.cuda.Stream(device=dev)              # tower lane
-        self.aux = torch.cuda.Stream(device=dev)                # DBP lookahead
+        import os
+        # block-scheduling priorities (lower = scheduled first as SMs free up):
+        # dense tower > comm > embedding, so the overlapped sparse work takes
+        # the SMs the GEMMs leave (NEST_LANE_PRIORITIES="dense,comm,emb")
+        pd, pc, pe = (int(x) for x in os.environ.get("NEST_LANE_PRIORITIES", "-2,-1,0").split(","))
+        # 3: dense / embedding / comm lanes; 2: the paper's computation +
+        # communication streams (NEST_LANES)
+        self.lanes = int(os.environ.get("NEST_LANES", "3"))
+        green = int(os.environ.get("NEST_GREEN_SMS", "0"))
+        if green > 0:
+            # hard SM partition (green contexts): the sparse lanes (embedding,
+            # comm, DBP lookahead) get `green` SMs, the dense tower the rest
+            sparse_s, dense_s = _green_streams(dev, green, [pe, pc, 0], [pd])
+            self.compute, comm, self.aux = sparse_s
+            self.comm = comm if ctx.world > 1 else self.compute
+            self.dense = dense_s[0]
+        else:
+            self.compute = torch.cuda.Stream(device=dev, priority=pe)            # embedding lane
+            self.comm = torch.cuda.Stream(device=dev, priority=pc) if ctx.world > 1 else self.compute
+            self.dense = torch.cuda.Stream(device=dev, priority=pd)              # tower lane
+            self.aux = torch.cuda.Stream(device=dev)                # DBP lookahead
         self.t = 0
         self.primed = False
         self.outs: List[torch.Tensor] = []
@@ -80,6 +129,8 @@ class Runner:
             self.primed = True
         outs = self.out_buffers(a)
         self.outs = outs if keep_outputs else []
+        if self.lanes == 2:
+            return self._step_two_lanes(a, p, outs, next_batch, dout_fn)
         # embedding lane: pool_0, pool_1, seg_0, pool_2, seg_1, ... (pool of
         # micro-batch i+1 is queued before the gradients of i); comm lane:
         # emb_0, emb_1, grad_0, emb_2, grad_1, ...; dense lane: tower_i
@@ -103,6 +154,34 @@ class Runner:
             ctx.grad_bwd_update(a, i, dout, self.lr, cs, ms)
         if self.pipelined and next_batch is not None:
             ctx.dbp_refresh(a, p, cs)
+        self.t += 1
+        return outs
+
+    def _step_two_lanes(self, a, p, outs, next_batch, dout_fn):
+        """The paper's two-stream plan: one computation stream runs
+        pool_i, tower_i, segsum_i back to back (each on the whole GPU); the
+        communication stream runs emb A2A_{i+1} and grad A2A_i as early as
+        possible, overlapping the computation of neighbouring micro-batches."""
+        ctx = self.ctx
+        cs, ms = self.dense, self.comm
+        cs.wait_stream(self.compute)          # batch uploads / primed route
+        ctx.lookup_prefetch(a, 0, cs, ms)
+        ctx.lookup_fwd(a, 0, outs[0], cs, ms)
+        for i in range(self.N):
+            if i + 1 < self.N:
+                ctx.lookup_prefetch(a, i + 1, cs, ms)
+            with torch.cuda.stream(cs):
+                dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
+            if i == self.N - 1 and self.pipelined and next_batch is not None:
+                nk, no, nB = next_batch
+                self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
+                self._route(p, nk, no, nB, self.aux)
+            ctx.grad_bwd_update(a, i, dout, self.lr, cs, ms)
+            if i + 1 < self.N:
+                ctx.lookup_fwd(a, i + 1, outs[i + 1], cs, ms)
+        if self.pipelined and next_batch is not None:
+            ctx.dbp_refresh(a, p, cs)
+        self.compute.wait_stream(cs)
         self.t += 1
         return outs
 

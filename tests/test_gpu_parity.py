@@ -269,6 +269,42 @@ def test_error_paths():
 
 
 # --------------------------------------------------------------------------- full size
+def test_genrec_full_tables_unpooled_sampled():
+    """BASELINE configs[2] (8 x 50M rows, d=64, seq 1,024 unpooled, Zipf 1.2) with
+    the full table sizes and a reduced batch: expanded rows and updated rows
+    checked one by one against the oracle's PRF rows and per-key gradients."""
+    cfg = WL.CONFIGS["genrec"]
+    B, N, F, d = 128, 2, cfg.num_features, cfg.dim
+    keys, offs = WL.gen_batch(cfg, 0, 0, 0, batch=B)
+    U = len(np.unique(keys))
+    ctx = NestContext(cfg.table_rows, d, pooling="none", max_keys=len(keys), max_batch=B,
+                      max_micro_batches=N, max_recv_keys=U + 16, max_mb_rows=2 * U + 16,
+                      seed=9, init_mode="uniform", device=DEV)
+    run = Runner(ctx, N=N, pipelined=False, lr_over_B=0.25)
+    kd, od = to_dev(keys, torch.int64), to_dev(offs, torch.int32)
+    dout_all = torch.randn(len(keys), d, device=DEV, generator=torch.Generator(DEV).manual_seed(1))
+    cap = B // N
+    mb_occ = [(int(offs[i * cap * F]), int(offs[(i + 1) * cap * F])) for i in range(N)]
+    outs = run.step((kd, od, B), None, lambda t, i, p: dout_all[mb_occ[i][0]:mb_occ[i][1]])
+    torch.cuda.synchronize()
+    v = ctx.route_view(0)
+    assert v["info"].uniq == U and np.array_equal(v["uniq"][v["inverse"]], keys)
+    rng = np.random.default_rng(2)
+    for j in rng.integers(0, len(keys), size=64):      # expanded occurrence rows
+        i = 0 if j < mb_occ[0][1] else 1
+        got = outs[i][j - mb_occ[i][0]].cpu().numpy()
+        assert np.array_equal(got, OPRF.init_rows(9, keys[j:j + 1], d)[0])
+    dnp = dout_all.cpu().numpy().astype(np.float64)
+    sample = rng.choice(np.unique(keys), size=48, replace=False)
+    got = ctx.read_rows(to_dev(sample, torch.int64)).cpu().numpy()
+    for k, row in zip(sample, got):
+        occ = np.nonzero(keys == k)[0]
+        ref = OS.sgd_rows(OPRF.init_rows(9, np.array([k]), d), dnp[occ].sum(axis=0)[None], 0.25)[0]
+        scale = np.abs(dnp[occ]).sum(axis=0) * 0.25 + np.abs(ref)
+        assert np.all(np.abs(row - ref) <= 1e-5 * scale + 1e-7)
+    ctx.close()
+
+
 def test_dlrm_full_size_w1_sampled():
     """BASELINE configs[1] at W=1 (the bench launch configuration): routing
     invariants at full size, sampled pooled rows and sampled updated rows
