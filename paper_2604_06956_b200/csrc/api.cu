@@ -524,6 +524,22 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
     cudaStream_t cs = S(compute), ms = S(comm);
     Slot& other = c->slot[1 - slot];
     const double row = double(c->D) * sizeof(float);
+    if (c->W == 1 && s.N == 1) {
+      // one rank, one micro-batch: the segment-sum applies Eq. 2 itself
+      NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
+      {
+        ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
+        launch_segsum_sgd(*c, s, dout, lr_over_B, cs);
+        ps.launches = s.info.mb_uniq[0] > 0 ? 7 : 0;
+        // N7 + N8 without the gradient-row round trip: gradient rows read +
+        // 4 K + frozen rows read + rows written back
+        ps.bytes = row * double(s.info.mb_out_rows[0]) + 4.0 * double(s.info.mb_nnz[0]) +
+                   2.0 * row * double(s.info.mb_uniq[0]);
+      }
+      NEST_CUDA(cudaEventRecord(s.ev_update, cs));
+      s.updated = true;
+      return;
+    }
     const bool fused = c->a2a_mode == A2A_FUSED;
     {
       ProfScope ps(*c, fused ? ST_GRAD_A2A : ST_SEGSUM, SK_COMPUTE, cs);

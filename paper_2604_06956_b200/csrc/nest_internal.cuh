@@ -472,6 +472,12 @@ struct PeerRows {
   int32_t off[NEST_MAX_WORLD + 1];
   int32_t n;          // number of segments (W, or 1 for a purely local map)
   int32_t fence;      // 1: writes go to peer memory (system fence at the end)
+  // fused SGD (W == 1, N == 1: every key has exactly one contribution): row k
+  // is applied as shard[owner_rows[k]] = fma(-lr, g, buffer[k]) instead of stored
+  const float* sgd_buffer;
+  const int32_t* sgd_rows;
+  float* sgd_shard;
+  float sgd_lr;
 };
 enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
 int a2a_mode_wanted(int W);
@@ -479,6 +485,7 @@ int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb);
 int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb);
 void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st);
 void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st);
+void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, float lr, cudaStream_t st);
 void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st);
 // copy-engine transport (xfer.cu)
 bool xfer_wanted(int W);

@@ -288,6 +288,21 @@ __device__ __forceinline__ float* map_row(const PeerRows& m, int64_t p, int D) {
   return m.base[s] + (p - m.off[s]) * D;
 }
 
+// store gradient row k (one float4 per call) or, in fused-SGD mode, apply it:
+// shard[owner_rows[k]] = fma(-lr, g, frozen buffer row k)  (Eq. 2)
+__device__ __forceinline__ void put_grad(const PeerRows& m, int64_t k, int D, int col, float4 g) {
+  if (m.sgd_shard) {
+    float4 e = ldg_f4(m.sgd_buffer + k * D + col);
+    e.x = __fmaf_rn(-m.sgd_lr, g.x, e.x);
+    e.y = __fmaf_rn(-m.sgd_lr, g.y, e.y);
+    e.z = __fmaf_rn(-m.sgd_lr, g.z, e.z);
+    e.w = __fmaf_rn(-m.sgd_lr, g.w, e.w);
+    st_f4_cs(m.sgd_shard + int64_t(__ldg(m.sgd_rows + k)) * D + col, e);
+  } else {
+    st_f4(map_row(m, k, D) + col, g);
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, int chunk,
                                                              const int32_t* __restrict__ seg_start,
@@ -300,9 +315,8 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, int chu
     if (b - a > chunk) continue;
     float4 acc[RowGeom<D>::VPL];
     sum_rows<D>(sval, a, b, dout, gp, acc);
-    float* g = map_row(out, k, D);
 #pragma unroll
-    for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(g + gp.col(v), acc[v]);
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) put_grad(out, k, D, gp.col(v), acc[v]);
   }
   if (out.fence) __threadfence_system();
 }
@@ -357,12 +371,11 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
     for (int v = 0; v < G::VPL; ++v) red[grp][v * G::L + l] = acc[v];
     __syncthreads();
     if (grp == 0) {
-      float* g = map_row(out, k, D);
 #pragma unroll
       for (int v = 0; v < G::VPL; ++v) {
         float4 s = red[0][v * G::L + l];
         for (int q = 1; q < NG; ++q) s = f4add(s, red[q][v * G::L + l]);
-        st_f4(g + (v * G::L + l) * 4, s);
+        put_grad(out, k, D, (v * G::L + l) * 4, s);
       }
     }
     __syncthreads();
@@ -379,6 +392,22 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
   out.n = 1;
   out.fence = 0;
   launch_segsum_to(c, s, mb, dout, out, st);
+}
+
+// R10 + R12 fused for W == 1, N == 1: each key's gradient is its only
+// contribution, so the segment-sum applies the SGD update and writes the row
+// back directly (no gradient rows stored and re-read)
+void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, float lr, cudaStream_t st) {
+  PeerRows out{};
+  out.base[0] = c.src_rows;
+  out.off[0] = 0;
+  out.off[1] = int32_t(s.info.mb_uniq[0]);
+  out.n = 1;
+  out.sgd_buffer = s.buffer;
+  out.sgd_rows = s.owner_rows;
+  out.sgd_shard = c.shard;
+  out.sgd_lr = lr;
+  launch_segsum_to(c, s, 0, dout, out, st);
 }
 
 // R6 + R7 fused: the owner's gather writes every requested row straight into
