@@ -242,7 +242,8 @@ def main():
         obj = [unique_ids() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uids = obj[0]
-    ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, pooling=cfg.pooling, max_keys=K + 1024,
+    ctx = NestContext(cfg.table_rows, d, num_features=F, world=world, rank=rank, pooling=cfg.pooling,
+                      max_keys=K + 1024,
                       max_batch=B, max_micro_batches=Nctx, seed=args.seed + 1, init_mode="uniform",
                       tower_layers=cfg.tower_layers if args.variant == "et" else 0,
                       tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev,

@@ -119,8 +119,9 @@ typedef struct {
   const int32_t* inverse;     /* [K] uniq[inverse[j]] == keys[j] */
   const uint32_t* mask;       /* [U_s] bit i set iff the key occurs in micro-batch i */
   const int32_t* pos;         /* [N][U_s+1] index of u among mask-bit-i keys */
-  const int32_t* send_counts; /* [W][N+2] per owner: {U, U_1..U_N, err} */
-  const int32_t* all_counts;  /* [W][W][N+2] every rank's send_counts (count exchange) */
+  const int32_t* send_counts; /* [W][Nm+2], Nm = max_micro_batches: per owner
+                                 {U, U_1..U_N, (unused up to Nm), err} */
+  const int32_t* all_counts;  /* [W][W][Nm+2] every rank's send_counts (count exchange) */
   const int64_t* recv_keys;   /* [R_o] received keys | mask << 56, sources concatenated */
   const int32_t* owner_rows;  /* [U_o] shard row of every owner-unique key, ascending */
   const int32_t* owner_inv;   /* [R_o] owner-unique index of every received key */

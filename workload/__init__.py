@@ -43,6 +43,7 @@ class WorkloadConfig:
     micro_batches: int = 1        # default FWP N
     tower_layers: int = 4         # stand-in tower depth (timing only)
     tower_hidden: int = 1024
+    feature_table: Tuple[int, ...] = ()   # table of every feature (default: feature f -> table f)
 
     @property
     def num_tables(self) -> int:
@@ -50,7 +51,10 @@ class WorkloadConfig:
 
     @property
     def num_features(self) -> int:
-        return len(self.table_rows)
+        return len(self.feature_table) if self.feature_table else len(self.table_rows)
+
+    def table_of_feature(self, f: int) -> int:
+        return self.feature_table[f] if self.feature_table else f
 
     def with_(self, **kw) -> "WorkloadConfig":
         return replace(self, **kw)
@@ -74,7 +78,7 @@ CONFIGS = {
                              (1024, 1024), True, 1.2, pooling="none", world=8),
     # configs[3]: 1 table x 100M rows, dim 128, 26 bags per sample
     "dbp_stress": WorkloadConfig("dbp_stress", (100_000_000,), 128, 65536,
-                                 (1, 3), True, 1.05, world=8),
+                                 (1, 3), True, 1.05, world=8, feature_table=(0,) * 26),
 }
 
 
@@ -138,8 +142,9 @@ def unpack_keys(keys: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
 
 def _draw_table_keys(rng, cfg: WorkloadConfig, f: int, lengths: np.ndarray,
                      salt: int) -> np.ndarray:
-    """Rows for every bag of table f, concatenated in bag order."""
-    rows_t = cfg.table_rows[f]
+    """Rows for every bag of feature f, concatenated in bag order."""
+    tab = cfg.table_of_feature(f)
+    rows_t = cfg.table_rows[tab]
     n = int(lengths.sum())
     ranks = zipf_ranks(rng, cfg.zipf, rows_t, n)
     if not cfg.bag_repeats:
@@ -158,7 +163,7 @@ def _draw_table_keys(rng, cfg: WorkloadConfig, f: int, lengths: np.ndarray,
         else:  # pragma: no cover
             raise RuntimeError("could not draw distinct bag keys")
         del starts
-    return pack_keys(f, ranks_to_rows(ranks, rows_t, salt=f + 1))
+    return pack_keys(tab, ranks_to_rows(ranks, rows_t, salt=tab + 1))
 
 
 def gen_batch(cfg: WorkloadConfig, seed: int, step: int, rank: int,
@@ -244,7 +249,8 @@ def gen_correlated_batch(cfg: WorkloadConfig, seed: int, step: int, rank: int,
     np.cumsum(lengths.reshape(-1), out=bag_offsets[1:])
     keys = np.empty(int(bag_offsets[-1]), dtype=np.int64)
     for f in range(F):
-        rows_t = cfg.table_rows[f]
+        tab = cfg.table_of_feature(f)
+        rows_t = cfg.table_rows[tab]
         ln = lengths[:, f]
         n = int(ln.sum())
         r2 = rng_for(seed, 6, step, rank, f)
@@ -257,5 +263,5 @@ def gen_correlated_batch(cfg: WorkloadConfig, seed: int, step: int, rank: int,
             rows[sel] = ranks_to_rows(ranks[sel], rows_t, salt=f + 1000 * (1 + int(g)))
         starts = bag_offsets[np.arange(B) * F + f]
         dst = np.repeat(starts, ln) + (np.arange(n) - np.repeat(np.cumsum(ln) - ln, ln))
-        keys[dst] = pack_keys(f, rows)
+        keys[dst] = pack_keys(tab, rows)
     return keys, bag_offsets.astype(np.int32)
