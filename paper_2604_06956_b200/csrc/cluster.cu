@@ -77,7 +77,8 @@ __global__ void k_cl_first(int64_t nnz, const uint32_t* __restrict__ sk, const i
 
 // warp per sample: size (distinct keys), init assignment
 __global__ void k_cl_size(int B, int F, const int32_t* __restrict__ bag_off, const int32_t* __restrict__ cl_u,
-                          int32_t* __restrict__ size, int32_t* __restrict__ grp, int32_t* __restrict__ maxsz) {
+                          int32_t* __restrict__ size, int32_t* __restrict__ grp, int32_t* __restrict__ maxsz,
+                          int32_t* __restrict__ err) {
   const int lane = lane_id();
   const int64_t nw = int64_t(gridDim.x) * blockDim.x / 32;
   for (int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < B; s += nw) {
@@ -88,7 +89,8 @@ __global__ void k_cl_size(int B, int F, const int32_t* __restrict__ bag_off, con
     if (lane == 0) {
       size[s] = n;
       grp[s] = -1;
-      atomicMax(maxsz, n);
+      if (n > kMaxSize) atomicOr(err, kErrSampleSize);   // rank keys need (smax+1)^2 <= 2^28
+      atomicMax(maxsz, min(n, kMaxSize));
     }
   }
 }
@@ -133,14 +135,25 @@ __global__ void k_cl_seed_apply(int F, int g, const int32_t* __restrict__ bag_of
   }
 }
 
-// round snapshot: S[g][s] for every unassigned sample (warp per sample)
+constexpr uint32_t kTaken = 0xffffffffu;   // rank key of a sample no longer a candidate
+
+// round snapshot (warp per sample): S = |keys(s) & union(g)| folded into one
+// rank key per (g, s), ck = (smax - S) * (smax + 1) + (size - S), so that
+// "S desc, size - S asc" is "ck asc"; assigned samples get kTaken.
 __global__ void k_cl_S(int B, int F, int N, const int32_t* __restrict__ bag_off,
                        const int32_t* __restrict__ cl_u, const uint32_t* __restrict__ inmask,
-                       const int32_t* __restrict__ grp, int32_t* __restrict__ S) {
+                       const int32_t* __restrict__ grp, const int32_t* __restrict__ size,
+                       const int32_t* __restrict__ maxsz, uint32_t* __restrict__ ck) {
   const int lane = lane_id();
+  const int smax = *maxsz;
+  const uint32_t nb = uint32_t(smax) + 1;
   const int64_t nw = int64_t(gridDim.x) * blockDim.x / 32;
   for (int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < B; s += nw) {
-    if (grp[s] >= 0) continue;
+    if (grp[s] >= 0) {
+      if (lane < N) ck[int64_t(lane) * B + s] = kTaken;
+      continue;
+    }
+    const int sz = size[s];
     const int j0 = bag_off[s * F], j1 = bag_off[(s + 1) * F];
     int cnt[NEST_MAX_MICRO_BATCHES] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = j0 + lane; j < j1; j += 32) {
@@ -154,7 +167,7 @@ __global__ void k_cl_S(int B, int F, int N, const int32_t* __restrict__ bag_off,
     for (int g = 0; g < NEST_MAX_MICRO_BATCHES; ++g) {
       int v = cnt[g];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && g < N) S[int64_t(g) * B + s] = v;
+      if (lane == g && g < N) ck[int64_t(g) * B + s] = uint32_t(smax - v) * nb + uint32_t(sz - v);
     }
   }
 }
@@ -205,66 +218,107 @@ __device__ void find_bin(const int* hist, int nbins, int k, int* ws, int* out) {
   __syncthreads();
 }
 
-// one round: groups 0..N-1 take their samples in order (single block)
+// one round: groups 0..N-1 take their samples in order (single block).
+// Group g takes the k samples of least rank key ck (ties: lowest id): a radix
+// select on ck finds the threshold T and how many T-ties to take (one
+// histogram level when (smax+1)^2 <= kHistBins, else two), then every warp
+// walks its own contiguous id range in order, ranking the T-ties by id.
+// A sample taken by g is struck from the later groups' keys (ck = kTaken).
+constexpr int kHistLog = 14, kHistBins = 1 << kHistLog, kSelUnroll = 8;
+
 __global__ void __launch_bounds__(kSelThreads) k_cl_select(int B, int N, Takes takes,
-                                                           const int32_t* __restrict__ S,
-                                                           const int32_t* __restrict__ size,
                                                            const int32_t* __restrict__ maxsz,
-                                                           int32_t* __restrict__ grp,
+                                                           uint32_t* ck, int32_t* __restrict__ grp,
                                                            int32_t* __restrict__ newlist,
                                                            int32_t* __restrict__ nnew) {
-  extern __shared__ int hist[];            // [kMaxSize + 1]
+  extern __shared__ int hist[];            // [kHistBins]
   __shared__ int ws[33];
   __shared__ int sel[2];
-  const int smax = *maxsz;
-  const int nb = smax + 1;
-  const int per = (B + kSelThreads - 1) / kSelThreads;
-  const int s0 = threadIdx.x * per, s1 = min(B, s0 + per);
-  if (threadIdx.x == 0) *nnew = 0;
+  __shared__ int wcnt[32];
+  __shared__ int nnew_s;
+  const uint32_t nb = uint32_t(*maxsz) + 1;
+  const uint32_t nkeys = nb * nb;          // ck < nb^2 <= 2^28
+  int nbits = 0;
+  while ((1u << nbits) < nkeys) ++nbits;
+  const int lo = nbits > kHistLog ? nbits - kHistLog : 0;
+  const int nb1 = lo ? kHistBins : int(nkeys);
+  const uint32_t lomask = (1u << lo) - 1u;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const int R = ((B + kSelThreads - 1) / kSelThreads) * 32;   // ids per warp, multiple of 32
+  const int w0 = min(B, warp * R), w1 = min(B, w0 + R);
+  if (threadIdx.x == 0) nnew_s = 0;
+  // warp-aggregated histogram increment (most candidates share a bin)
+  auto hist_add = [&](int bin) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && (peers & lt) == 0) atomicAdd(&hist[bin], __popc(peers));
+  };
+  // the warp's range in id order, kSelUnroll loads in flight per lane
+  auto walk = [&](const uint32_t* ckg, auto&& f) {
+    for (int s0 = w0; s0 < w1; s0 += 32 * kSelUnroll) {
+      uint32_t v[kSelUnroll];
+#pragma unroll
+      for (int u = 0; u < kSelUnroll; ++u) {
+        const int s = s0 + u * 32 + lane;
+        v[u] = s < w1 ? ckg[s] : kTaken;
+      }
+#pragma unroll
+      for (int u = 0; u < kSelUnroll; ++u)
+        if (s0 + u * 32 < w1) f(s0 + u * 32 + lane, v[u]);
+    }
+  };
   for (int g = 0; g < N; ++g) {
     const int k = takes.v[g];
     if (k <= 0) continue;
-    const int32_t* Sg = S + int64_t(g) * B;
-    // pass 1: key1 = smax - S
-    for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
+    const uint32_t* ckg = ck + int64_t(g) * B;
+    // level 1: bins of ck >> lo
+    for (int b = threadIdx.x; b < nb1; b += kSelThreads) hist[b] = 0;
     __syncthreads();
-    for (int s = s0; s < s1; ++s)
-      if (grp[s] < 0) atomicAdd(&hist[smax - Sg[s]], 1);
+    walk(ckg, [&](int, uint32_t c) { hist_add(c != kTaken ? int(c >> lo) : -1); });
     __syncthreads();
-    find_bin(hist, nb, k, ws, sel);
-    const int b1 = sel[0], k1 = k - sel[1];
+    find_bin(hist, nb1, k, ws, sel);
+    uint32_t T = uint32_t(sel[0]);
+    int kk = k - sel[1];
+    int cnt = hist[sel[0]];
     __syncthreads();
-    // pass 2: growth = size - S among key1 == b1
-    for (int b = threadIdx.x; b < nb; b += kSelThreads) hist[b] = 0;
-    __syncthreads();
-    for (int s = s0; s < s1; ++s)
-      if (grp[s] < 0 && smax - Sg[s] == b1) atomicAdd(&hist[size[s] - Sg[s]], 1);
-    __syncthreads();
-    find_bin(hist, nb, k1, ws, sel);
-    const int b2 = sel[0], k2 = k1 - sel[1];
-    __syncthreads();
-    // pass 3: lowest ids in (b1, b2), then assign
-    int mine = 0;
-    for (int s = s0; s < s1; ++s)
-      mine += grp[s] < 0 && smax - Sg[s] == b1 && size[s] - Sg[s] == b2;
-    int tot;
-    int rank = block_excl_scan(mine, ws, tot);
-    for (int s = s0; s < s1; ++s) {
-      if (grp[s] >= 0) continue;
-      const int key1 = smax - Sg[s];
-      bool take = key1 < b1;
-      if (key1 == b1) {
-        const int gr = size[s] - Sg[s];
-        if (gr < b2) take = true;
-        else if (gr == b2) take = rank++ < k2;
-      }
+    if (lo) {   // level 2: low bits inside the chosen bin
+      const uint32_t hi = T;
+      for (int b = threadIdx.x; b < (1 << lo); b += kSelThreads) hist[b] = 0;
+      __syncthreads();
+      walk(ckg, [&](int, uint32_t c) { hist_add(c != kTaken && (c >> lo) == hi ? int(c & lomask) : -1); });
+      __syncthreads();
+      find_bin(hist, 1 << lo, kk, ws, sel);
+      T = (hi << lo) | uint32_t(sel[0]);
+      kk -= sel[1];
+      cnt = hist[sel[0]];
+      __syncthreads();
+    }
+    const bool partial = kk < cnt;   // only then do the T-ties need ranking by id
+    int running = 0;
+    if (partial) {
+      int n = 0;
+      walk(ckg, [&](int, uint32_t c) { n += __popc(__ballot_sync(0xffffffffu, c == T)); });
+      if (lane == 0) wcnt[warp] = n;
+      __syncthreads();
+      for (int w = 0; w < warp; ++w) running += wcnt[w];
+    }
+    walk(ckg, [&](int s, uint32_t c) {
+      const uint32_t tie = __ballot_sync(0xffffffffu, c == T);
+      const bool take = c < T || (c == T && (!partial || running + __popc(tie & lt) < kk));
+      running += __popc(tie);
       if (take) {
         grp[s] = g;
-        newlist[atomicAdd(nnew, 1)] = s;
+        for (int g2 = g + 1; g2 < N; ++g2) ck[int64_t(g2) * B + s] = kTaken;
       }
-    }
+      const uint32_t m = __ballot_sync(0xffffffffu, take);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&nnew_s, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (take) newlist[base + __popc(m & lt)] = s;
+    });
     __syncthreads();
   }
+  if (threadIdx.x == 0) *nnew = nnew_s;
 }
 
 // union(g) grows by the keys of the samples taken this round (warp per sample)
@@ -335,7 +389,8 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
   int32_t* maxsz = reinterpret_cast<int32_t*>(c.cl_small);
   unsigned long long* best = reinterpret_cast<unsigned long long*>(c.cl_small + 1);
   int32_t* nnew = reinterpret_cast<int32_t*>(c.cl_small + 2);
-  k_cl_size<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(B, F, bag_offsets, c.cl_u, c.cl_size, c.cl_grp, maxsz);
+  k_cl_size<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(B, F, bag_offsets, c.cl_u, c.cl_size, c.cl_grp, maxsz,
+                                                        c.d_err);
   NEST_CUDA(cudaMemsetAsync(c.cl_inmask, 0, sizeof(uint32_t) * c.Kcap, st));
   // seeds
   for (int g = 0; g < N; ++g) {
@@ -349,7 +404,8 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
   std::vector<int64_t> have(N, 1);
   int64_t assigned = N;
   uint64_t Q = uint64_t(1) << 32;
-  const size_t smem = sizeof(int) * (kMaxSize + 1);
+  const size_t smem = sizeof(int) * kHistBins;
+  uint32_t* ck = reinterpret_cast<uint32_t*>(c.cl_S);
   static bool attr = false;
   if (!attr) {
     NEST_CUDA(cudaFuncSetAttribute(k_cl_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -364,8 +420,9 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
       have[g] += tk.v[g];
       assigned += tk.v[g];
     }
-    k_cl_S<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(B, F, N, bag_offsets, c.cl_u, c.cl_inmask, c.cl_grp, c.cl_S);
-    k_cl_select<<<1, kSelThreads, smem, st>>>(B, N, tk, c.cl_S, c.cl_size, maxsz, c.cl_grp, c.cl_new, nnew);
+    k_cl_S<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(B, F, N, bag_offsets, c.cl_u, c.cl_inmask, c.cl_grp,
+                                                      c.cl_size, maxsz, ck);
+    k_cl_select<<<1, kSelThreads, smem, st>>>(B, N, tk, maxsz, ck, c.cl_grp, c.cl_new, nnew);
     k_cl_update<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(F, c.cl_new, nnew, bag_offsets, c.cl_u, c.cl_grp,
                                                            c.cl_inmask);
   }

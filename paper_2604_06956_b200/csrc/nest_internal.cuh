@@ -50,7 +50,7 @@ struct Error {
 #define NEST_LAUNCH_CHECK() NEST_CUDA(cudaGetLastError())
 
 // device error bits (OR-ed into ctx->d_err)
-enum : int32_t { kErrKeyRange = 1, kErrShard = 2 };
+enum : int32_t { kErrKeyRange = 1, kErrShard = 2, kErrSampleSize = 4 };
 
 constexpr int kRowBits = 40;
 constexpr uint64_t kRowMask = (uint64_t(1) << kRowBits) - 1;

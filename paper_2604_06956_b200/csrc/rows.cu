@@ -239,7 +239,6 @@ void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
 //   partials in a fixed strided order + fixed tree.  No float atomics, so
 //   the result is bitwise reproducible run to run.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 32;
 
 __global__ void k_seg_heads(int64_t Ki, const uint32_t* __restrict__ skey, uint32_t umask,
                             const int32_t* __restrict__ pos, int32_t* __restrict__ seg_start,

@@ -247,6 +247,61 @@ def test_train_w1_clustered_p1_bit_exact():
     assert np.array_equal(ctx.read_rows(to_dev(allk, torch.int64)).cpu().numpy(), tab_ref.get(allk))
 
 
+# --------------------------------------------------------------------------- edge cases
+def _p1_check(cfg, batches, N, pipelined=True, lr=2.0 ** -10, seed=5):
+    """Run the given per-step batches (W=1) and compare pooled rows of every
+    step and the final rows bit-exactly against the oracle (P1)."""
+    F, d = cfg.num_features, cfg.dim
+    T = len(batches)
+    douts = [WL.gen_dout(seed, t, 0, (len(o) - 1), d, "dyadic") for t, (k, o) in enumerate(batches)]
+    B = (len(batches[0][1]) - 1) // F
+    K = max(1, max(len(k) for k, _ in batches))
+    ctx = make_ctx(cfg, B, N=N, K=K, init="dyadic", seed=seed)
+    run = Runner(ctx, N=N, pipelined=pipelined, lr_over_B=lr)
+    db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), B) for k, o in batches]
+    cap = B // N
+    tab = OS.LazyTable(seed, d, "dyadic")
+    for t in range(T):
+        outs = run.step(db[t], db[t + 1] if t + 1 < T else None,
+                        lambda tt, i, p, t=t: to_dev(douts[t][i * cap * F:(i + 1) * cap * F], torch.float32))
+        torch.cuda.synchronize()
+        res = OS.sync_step(tab, [batches[t]], [douts[t]], lr)
+        assert np.array_equal(np.concatenate([o.cpu().numpy() for o in outs]), res.pooled[0]), t
+    allk = np.unique(np.concatenate([k for k, _ in batches] + [np.zeros(1, np.int64)]))
+    assert np.array_equal(ctx.read_rows(to_dev(allk, torch.int64)).cpu().numpy(), tab.get(allk))
+
+
+def test_edge_empty_bags_empty_samples_and_single_sample_microbatches():
+    """Empty bags pool to zero (reading Q5), an all-empty sample, micro-batches
+    of one sample (N = B), and a step whose batch has no keys at all."""
+    cfg = WL.CONFIGS["tiny"]
+    F, B = cfg.num_features, 8
+    batches = []
+    for t in range(3):
+        keys, offs = WL.gen_batch(cfg, 40 + t, t, 0, batch=B)
+        lens = np.diff(offs).astype(np.int64)
+        lens[::3] = 0                      # every third bag empty
+        lens[F:2 * F] = 0                  # sample 1 has no keys
+        new_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        new_keys = np.concatenate([keys[offs[b]:offs[b] + lens[b]] for b in range(B * F)])
+        batches.append((new_keys.astype(np.int64), new_off))
+    batches.append((np.zeros(0, np.int64), np.zeros(B * F + 1, np.int32)))   # no keys
+    batches.append(batches[0])
+    _p1_check(cfg, batches, N=8)
+    _p1_check(cfg, batches, N=2, pipelined=False)
+
+
+def test_edge_single_key_everywhere_hot():
+    """Degenerate skew: every occurrence is the same key (one hot segment of
+    B*F rows, split into chunks) plus the table-boundary rows."""
+    cfg = WL.CONFIGS["tiny"].with_(bag_repeats=True)
+    F, B = cfg.num_features, 64
+    offs = np.arange(B * F + 1, dtype=np.int32) * 2
+    keys = np.full(B * F * 2, (2 << 40) | 999, dtype=np.int64)
+    keys[1::7] = (3 << 40) | 0
+    _p1_check(cfg, [(keys, offs), (keys[::-1].copy(), offs)], N=4)
+
+
 # --------------------------------------------------------------------------- errors
 def test_error_paths():
     cfg = WL.CONFIGS["tiny"]
