@@ -377,7 +377,7 @@ def main():
                 continue
             e = {"ms_per_step": s["ms"] / steps, "launches_per_step": s["launches"] / steps,
                  "records_per_step": s["records"] / steps}
-            if name == "tower":
+            if name in ("tower", "tower_dw"):
                 e["tflops"] = s["bytes"] / (s["ms"] * 1e9) if s["ms"] else None
             elif name in ("emb_a2a", "grad_a2a", "key_a2a"):
                 e["nvlink_gbs"] = s["bytes"] / (s["ms"] * 1e6) if s["ms"] else None

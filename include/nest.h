@@ -222,9 +222,16 @@ NEST_API nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32
 /* Stand-in dense tower (the FWP overlap partner, not the product):
  * fixed bf16 MLP forward + backward on `stream` via cuBLAS, input = the pooled
  * rows of a micro-batch viewed as [rows/F, F*d]; writes its input gradient
- * into dout (fp32, same layout).  Requires tower_layers > 0. */
+ * into dout (fp32, same layout).  Requires tower_layers > 0.  dout is
+ * complete when `stream` reaches it; the weight-gradient GEMMs may still run
+ * on a library-internal stream (the next call, nest_join and nest_destroy
+ * wait for them). */
 NEST_API nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t rows,
                                  float* dout, void* stream);
+
+/* Make `stream` wait for all work the library queued on its internal streams
+ * (the tower's deferred weight-gradient GEMMs).  Host-side enqueue only. */
+NEST_API nest_status_t nest_join(nest_ctx_t* ctx, void* stream);
 
 /* Host-known counts of a slot (valid after nest_route). */
 NEST_API nest_status_t nest_slot_info(const nest_ctx_t* ctx, int32_t slot, nest_slot_info_t* info);
@@ -257,16 +264,17 @@ NEST_API nest_status_t nest_exchange_plan(const nest_config_t* cfg, int32_t N,
                                           const int32_t* all_counts, nest_exchange_plan_t* plan);
 
 /* ---- tracing: CUDA events around every stage of the path ---- */
-enum { NEST_PROFILE_STAGES = 14 };
+enum { NEST_PROFILE_STAGES = 15 };
 typedef struct {
   char name[24];        /* stage: schedule, route, sort, key_a2a, owner_dedup, gather, refresh,
-                           send_gather, emb_a2a, pool, tower, segsum, grad_a2a, update */
+                           send_gather, emb_a2a, pool, tower, segsum, grad_a2a, update,
+                           tower_dw (the tower's deferred weight gradients, internal stream) */
   int32_t stream;       /* 0 compute, 1 comm, 2 aux */
   int32_t records;      /* instrumented calls */
   int32_t launches;     /* libnest kernels launched by those calls (NCCL / cuBLAS not counted) */
   int32_t pad;
   double ms;            /* summed event-measured durations */
-  double bytes;         /* summed algorithmic bytes; FLOPs for `tower`;
+  double bytes;         /* summed algorithmic bytes; FLOPs for tower / tower_dw;
                            off-GPU bytes for the All2All stages */
   double units;         /* summed device-side counts: refreshed rows I (refresh),
                            owner-unique keys U_o (gather, update, owner_dedup) */

@@ -137,6 +137,10 @@ class NestContext:
         self._check(self.lib.nest_tower_fwd_bwd(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout),
                                                 _stream(stream)))
 
+    def join(self, stream=None) -> None:
+        """`stream` waits for the library's internal streams (nest_join)."""
+        self._check(self.lib.nest_join(self.ctx, _stream(stream)))
+
     def slot_info(self, slot: int) -> L.SlotInfo:
         info = L.SlotInfo()
         self._check(self.lib.nest_slot_info(self.ctx, slot, C.byref(info)))

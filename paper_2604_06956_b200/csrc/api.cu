@@ -634,12 +634,15 @@ nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t r
     NEST_CHECK(c->tower != nullptr, NEST_ERR_INVALID, "tower_layers == 0");
     NEST_CHECK(rows % c->F == 0, NEST_ERR_INVALID, "rows must be a multiple of F");
     ProfScope ps(*c, ST_TOWER, SK_COMPUTE, S(stream));
-    tower_run(*c, pooled, rows, dout, S(stream));
-    const double M = double(rows / c->F), in0 = double(c->F) * c->D, H = c->cfg.tower_hidden;
-    const int L = c->cfg.tower_layers;
-    ps.bytes = 3.0 * 2.0 * M * (in0 * H + double(L - 1) * H * H);  // FLOPs (fwd + dW + dX)
+    ps.bytes = tower_run(*c, pooled, rows, dout, S(stream));  // FLOPs on this stream
     ps.launches = 1;  // the cast kernel (the GEMMs are cuBLAS)
   });
+}
+
+nest_status_t nest_join(nest_ctx_t* ctx, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { tower_join(*c, S(stream)); });
 }
 
 nest_status_t nest_slot_info(const nest_ctx_t* ctx, int32_t slot, nest_slot_info_t* info) {

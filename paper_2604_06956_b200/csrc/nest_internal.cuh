@@ -106,7 +106,7 @@ struct Slot {
 // ----------------------------------------------------------------------------
 enum Stage : int {
   ST_SCHEDULE = 0, ST_ROUTE, ST_SORT, ST_KEY_A2A, ST_OWNER_DEDUP, ST_GATHER, ST_REFRESH,
-  ST_SEND_GATHER, ST_EMB_A2A, ST_POOL, ST_TOWER, ST_SEGSUM, ST_GRAD_A2A, ST_UPDATE, ST_COUNT
+  ST_SEND_GATHER, ST_EMB_A2A, ST_POOL, ST_TOWER, ST_SEGSUM, ST_GRAD_A2A, ST_UPDATE, ST_TOWER_DW, ST_COUNT
 };
 enum StreamKind : int { SK_COMPUTE = 0, SK_COMM = 1, SK_AUX = 2 };
 
@@ -497,6 +497,7 @@ void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st);
 void xfer_wait_grads(Ctx& c, Slot& s, cudaStream_t st);
 void tower_create(Ctx& c);
 void tower_destroy(Ctx& c);
-void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st);
+double tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st);
+void tower_join(Ctx& c, cudaStream_t st);
 
 }  // namespace nest

@@ -9,9 +9,10 @@
 
 namespace nest {
 
+static_assert(int(ST_COUNT) == int(NEST_PROFILE_STAGES), "stage table out of sync with include/nest.h");
 static const char* kStageName[ST_COUNT] = {"schedule", "route", "sort", "key_a2a", "owner_dedup",
                                            "gather", "refresh", "send_gather", "emb_a2a", "pool",
-                                           "tower", "segsum", "grad_a2a", "update"};
+                                           "tower", "segsum", "grad_a2a", "update", "tower_dw"};
 
 static cudaEvent_t take_event(Profiler& p) {
   if (p.next_ev == p.pool.size()) {

@@ -40,6 +40,26 @@ static inline int emb_blocks(int64_t rows, int rows_per_block) {
   return blocks_for_rows(rows, rows_per_block, emb_cap());
 }
 
+// independent segments / bags each lane group walks at once (their index
+// chains and row loads overlap; every sum stays in its own sequential order):
+// NEST_ROW_ILP = 1 (default), 2 or 4.  Measured on DLRM W=1:
+// 2 and 4 are slower -- the extra registers halve occupancy and the random
+// 512-byte row reads are bound by DRAM access efficiency, not by latency.
+static int row_ilp() {
+  static int v = [] {
+    const char* e = std::getenv("NEST_ROW_ILP");
+    const int x = e ? std::atoi(e) : 1;
+    return x == 2 || x == 4 ? x : 1;
+  }();
+  return v;
+}
+#define NEST_DISPATCH_ILP(...)                                           \
+  switch (row_ilp()) {                                                   \
+    case 2: { constexpr int IL = 2; __VA_ARGS__; } break;                \
+    case 4: { constexpr int IL = 4; __VA_ARGS__; } break;                \
+    default: { constexpr int IL = 1; __VA_ARGS__; } break;               \
+  }
+
 // group id / count helpers for grid-stride loops over rows
 template <int D>
 struct Grp {
@@ -136,7 +156,9 @@ void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // R8: pool (sum per bag, left to right) or expand (one row per occurrence)
 // ---------------------------------------------------------------------------
-template <int D, bool W1>
+// IL bags per lane group at once (bags q, q + ng, ...), two rows of each in
+// flight per pass, each bag summed left to right
+template <int D, bool W1, int IL>
 __global__ void __launch_bounds__(kRowThreads) k_pool(int64_t nrows, int F,
                                                       const int32_t* __restrict__ perm_mb,
                                                       const int32_t* __restrict__ bag_off,
@@ -146,35 +168,61 @@ __global__ void __launch_bounds__(kRowThreads) k_pool(int64_t nrows, int F,
                                                       float* __restrict__ out) {
   Grp<D> gp;
   constexpr int VPL = RowGeom<D>::VPL;
-  for (int64_t q = gp.g; q < nrows; q += gp.ng) {
-    const int p = int(q / F), f = int(q - int64_t(p) * F);
-    const int b = __ldg(perm_mb + p);
-    const int64_t bag = int64_t(b) * F + f;
-    const int j0 = __ldg(bag_off + bag), j1 = __ldg(bag_off + bag + 1);
-    float4 acc[VPL];
+  for (int64_t q0 = gp.g; q0 < nrows; q0 += IL * gp.ng) {
+    int j[IL], e[IL];
+    int len = 0;
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    int j = j0;
-    for (; j + 1 < j1; j += 2) {  // two rows in flight, summed in order
-      const int u0 = __ldg(inverse + j), u1 = __ldg(inverse + j + 1);
-      const int64_t i0 = W1 ? u0 : __ldg(pos + u0), i1 = W1 ? u1 : __ldg(pos + u1);
-      float4 a[VPL], bb[VPL];
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        a[v] = ldg_f4(src + i0 * D + gp.col(v));
-        bb[v] = ldg_f4(src + i1 * D + gp.col(v));
+    for (int i = 0; i < IL; ++i) {
+      const int64_t q = q0 + i * gp.ng;
+      j[i] = e[i] = 0;
+      if (q < nrows) {
+        const int p = int(q / F), f = int(q - int64_t(p) * F);
+        const int64_t bag = int64_t(__ldg(perm_mb + p)) * F + f;
+        j[i] = __ldg(bag_off + bag);
+        e[i] = __ldg(bag_off + bag + 1);
+        len = max(len, e[i] - j[i]);
       }
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) acc[v] = f4add(f4add(acc[v], a[v]), bb[v]);
     }
-    if (j < j1) {
-      const int u0 = __ldg(inverse + j);
-      const int64_t i0 = W1 ? u0 : __ldg(pos + u0);
+    float4 acc[IL][VPL];
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(src + i0 * D + gp.col(v)));
+    for (int i = 0; i < IL; ++i)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) acc[i][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int o = 0; o < len; o += 2) {
+      int64_t r[IL][2];
+#pragma unroll
+      for (int i = 0; i < IL; ++i)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          r[i][t] = -1;
+          if (j[i] + o + t < e[i]) {
+            const int u = __ldg(inverse + j[i] + o + t);
+            r[i][t] = W1 ? u : __ldg(pos + u);
+          }
+        }
+      float4 x[IL][2][VPL];
+#pragma unroll
+      for (int i = 0; i < IL; ++i)
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (r[i][t] >= 0) x[i][t][v] = ldg_f4(src + r[i][t] * D + gp.col(v));
+#pragma unroll
+      for (int i = 0; i < IL; ++i)
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (r[i][t] >= 0) acc[i][v] = f4add(acc[i][v], x[i][t][v]);
     }
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) st_f4_cs(out + q * D + gp.col(v), acc[v]);
+    for (int i = 0; i < IL; ++i) {
+      const int64_t q = q0 + i * gp.ng;
+      if (q < nrows)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) st_f4_cs(out + q * D + gp.col(v), acc[i][v]);
+    }
   }
 }
 
@@ -212,12 +260,14 @@ void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
     if (c.cfg.pooling == NEST_POOL_SUM) {
       const int64_t nrows = int64_t(s.cap) * c.F;
-      if (w1)
-        k_pool<D, true><<<emb_blocks(nrows, rpb), kRowThreads, 0, st>>>(
-            nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
-      else
-        k_pool<D, false><<<emb_blocks(nrows, rpb), kRowThreads, 0, st>>>(
-            nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+      NEST_DISPATCH_ILP({
+        if (w1)
+          k_pool<D, true, IL><<<emb_blocks((nrows + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
+              nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+        else
+          k_pool<D, false, IL><<<emb_blocks((nrows + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
+              nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+      });
     } else {
       if (w1)
         k_expand_rows<D, true><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
@@ -302,20 +352,64 @@ __device__ __forceinline__ void put_grad(const PeerRows& m, int64_t k, int D, in
   }
 }
 
-template <int D>
+// IL cold segments per lane group at once (k, k + ng, ...), two rows of each
+// in flight per pass, each segment summed in occurrence order
+template <int D, int IL>
 __global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, int chunk,
                                                              const int32_t* __restrict__ seg_start,
                                                              const int32_t* __restrict__ sval,
                                                              const float* __restrict__ dout,
                                                              const PeerRows out) {
   Grp<D> gp;
-  for (int64_t k = gp.g; k < Ui; k += gp.ng) {
-    const int64_t a = seg_start[k], b = seg_start[k + 1];
-    if (b - a > chunk) continue;
-    float4 acc[RowGeom<D>::VPL];
-    sum_rows<D>(sval, a, b, dout, gp, acc);
+  constexpr int VPL = RowGeom<D>::VPL;
+  for (int64_t k0 = gp.g; k0 < Ui; k0 += IL * gp.ng) {
+    int a[IL], b[IL];
+    int len = 0;
 #pragma unroll
-    for (int v = 0; v < RowGeom<D>::VPL; ++v) put_grad(out, k, D, gp.col(v), acc[v]);
+    for (int i = 0; i < IL; ++i) {
+      const int64_t k = k0 + i * gp.ng;
+      a[i] = b[i] = 0;
+      if (k < Ui) {
+        a[i] = seg_start[k];
+        b[i] = seg_start[k + 1];
+        if (b[i] - a[i] > chunk) b[i] = a[i] - 1;   // hot: the chunked kernels own it
+        len = max(len, b[i] - a[i]);
+      }
+    }
+    float4 acc[IL][VPL];
+#pragma unroll
+    for (int i = 0; i < IL; ++i)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) acc[i][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int o = 0; o < len; o += 2) {
+      int32_t r[IL][2];
+#pragma unroll
+      for (int i = 0; i < IL; ++i)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) r[i][t] = a[i] + o + t < b[i] ? __ldg(sval + a[i] + o + t) : -1;
+      float4 x[IL][2][VPL];
+#pragma unroll
+      for (int i = 0; i < IL; ++i)
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (r[i][t] >= 0) x[i][t][v] = ldg_f4(dout + int64_t(r[i][t]) * D + gp.col(v));
+#pragma unroll
+      for (int i = 0; i < IL; ++i)
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (r[i][t] >= 0) acc[i][v] = f4add(acc[i][v], x[i][t][v]);
+    }
+#pragma unroll
+    for (int i = 0; i < IL; ++i) {
+      const int64_t k = k0 + i * gp.ng;
+      if (k < Ui && b[i] >= a[i])
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) put_grad(out, k, D, gp.col(v), acc[i][v]);
+    }
   }
   if (out.fence) __threadfence_system();
 }
@@ -486,7 +580,8 @@ void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows
       c.scan_tmp_win, st);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_segsum_cold<D><<<emb_blocks(Ui, rpb), kRowThreads, 0, st>>>(Ui, chunk, seg, sval, dout, out);
+    NEST_DISPATCH_ILP(k_segsum_cold<D, IL><<<emb_blocks((Ui + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
+                          Ui, chunk, seg, sval, dout, out));
     k_segsum_hot_chunks<D><<<std::min(148 * 4, emb_cap()), kRowThreads, 0, st>>>(chunk, tot, hot_list, hot_ppos, seg, sval, dout,
                                                             c.partial);
     k_segsum_hot_final<D><<<std::min(148 * 2, emb_cap()), kRowThreads, 0, st>>>(tot, hot_list, hot_ppos, c.partial, out);

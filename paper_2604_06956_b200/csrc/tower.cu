@@ -5,6 +5,10 @@
 // fixed top gradient G, backward dW_l = dY_l^T X_{l-1} and dX_{l-1} = dY_l W_l,
 // with the input gradient dX_0 written as fp32 `dout`.  GEMMs run on the
 // tensor cores through cuBLAS (library GEMMs, allowed for the plain tower).
+// Only the dX chain feeds the embedding backward, so by default the dW GEMMs
+// run on an internal low-priority stream behind it (overlapping segment-sum,
+// update, refresh and the next pool); the next forward waits for them, as it
+// would for a dense optimizer step (NEST_TOWER_DEFER_DW=0: all on one stream).
 #include <cublasLt.h>
 #include <cublas_v2.h>
 
@@ -32,11 +36,16 @@ struct Tower {
   std::vector<int64_t> woff;
   __nv_bfloat16* x = nullptr;       // activations X_0..X_{L-1}, X_l at xoff[l]
   std::vector<int64_t> xoff;
-  __nv_bfloat16* dy[2] = {nullptr, nullptr};  // [bmax, max(H, in0)]
+  __nv_bfloat16* dy = nullptr;      // dY_l for l = 0..L-2 (layer l's output), [L-1][bmax, H]
   __nv_bfloat16* dw = nullptr;      // [H, max in]
-  __nv_bfloat16* gtop = nullptr;    // [bmax, H] fixed top gradient
-  void* ws = nullptr;
+  __nv_bfloat16* gtop = nullptr;    // [bmax, H] fixed top gradient dY_{L-1}
+  void* ws = nullptr;               // cuBLASLt workspace of the caller's stream
+  void* ws_dw = nullptr;            // ... and of the dW stream
   size_t ws_bytes = 32u << 20;
+  bool defer_dw = true;
+  cudaStream_t side = nullptr;      // dW GEMMs
+  cudaEvent_t ev_dx = nullptr, ev_dw = nullptr;
+  bool dw_pending = false;
   char* mem = nullptr;
 };
 
@@ -53,10 +62,10 @@ size_t tower_workspace_bytes(const Ctx& c) {
   const int64_t in0 = int64_t(c.F) * c.D, bmax = c.Bcap;
   int64_t elems = H * in0 + int64_t(L - 1) * H * H;   // weights
   elems += bmax * in0 + int64_t(L - 1) * bmax * H;   // activations
-  elems += 2 * bmax * std::max<int64_t>(H, in0);     // dy ping-pong
+  elems += int64_t(std::max(L - 1, 1)) * bmax * H;   // dY of layers 0..L-2 (>= 1: forward scratch)
   elems += int64_t(H) * std::max<int64_t>(H, in0);   // dw
   elems += bmax * H;                                 // top gradient
-  return size_t(elems) * 2 + (32u << 20) + 8 * 256;
+  return size_t(elems) * 2 + 2 * (32u << 20) + 8 * 256;
 }
 
 void tower_bind(Ctx& c, char* mem) {
@@ -103,11 +112,20 @@ void tower_create(Ctx& c) {
   t->xoff.assign(L + 1, 0);
   for (int l = 0; l < L; ++l) t->xoff[l + 1] = t->xoff[l] + bmax * (l == 0 ? in0 : H);
   t->x = w.take<__nv_bfloat16>(t->xoff[L]);
-  t->dy[0] = w.take<__nv_bfloat16>(bmax * std::max<int64_t>(H, in0));
-  t->dy[1] = w.take<__nv_bfloat16>(bmax * std::max<int64_t>(H, in0));
+  t->dy = w.take<__nv_bfloat16>(int64_t(std::max(L - 1, 1)) * bmax * H);
   t->dw = w.take<__nv_bfloat16>(int64_t(H) * std::max<int64_t>(H, in0));
   t->gtop = w.take<__nv_bfloat16>(bmax * H);
   t->ws = w.take<char>(int64_t(t->ws_bytes));
+  t->ws_dw = w.take<char>(int64_t(t->ws_bytes));
+  {
+    const char* dv = std::getenv("NEST_TOWER_DEFER_DW");
+    t->defer_dw = !(dv && std::atoi(dv) == 0);
+    int lo = 0, hi = 0;
+    NEST_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    NEST_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, lo));   // lowest priority
+    NEST_CUDA(cudaEventCreateWithFlags(&t->ev_dx, cudaEventDisableTiming));
+    NEST_CUDA(cudaEventCreateWithFlags(&t->ev_dw, cudaEventDisableTiming));
+  }
   NEST_CUBLAS(cublasCreate(&t->h));
   NEST_CUBLAS(cublasSetWorkspace(t->h, t->ws, t->ws_bytes));
   NEST_CUBLAS(cublasSetMathMode(t->h, CUBLAS_DEFAULT_MATH));
@@ -137,6 +155,12 @@ void tower_destroy(Ctx& c) {
   Tower* t = reinterpret_cast<Tower*>(c.tower);
   if (!t) return;
   if (t->h) cublasDestroy(t->h);
+  if (t->side) {
+    cudaStreamSynchronize(t->side);
+    cudaStreamDestroy(t->side);
+  }
+  if (t->ev_dx) cudaEventDestroy(t->ev_dx);
+  if (t->ev_dw) cudaEventDestroy(t->ev_dw);
   for (auto& kv : t->plans) {
     cublasLtMatmulDescDestroy(kv.second.op);
     cublasLtMatrixLayoutDestroy(kv.second.a);
@@ -174,7 +198,8 @@ static GemmPlan& plan_for(Tower* t, bool ta, bool tb, int M, int N, int K, int l
 }
 
 static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void* A, int lda,
-                    const void* B, int ldb, void* C, int ldc, cudaDataType ctype, cudaStream_t st) {
+                    const void* B, int ldb, void* C, int ldc, cudaDataType ctype, cudaStream_t st,
+                    void* ws) {
   const float alpha = 1.f, beta = 0.f;
   GemmPlan& p = plan_for(t, ta, tb, M, N, K, lda, ldb, ldc, ctype);
   if (!p.have_algo) {
@@ -197,7 +222,7 @@ static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void*
       bool ok = true;
       for (int rep = 0; rep < 3 && ok; ++rep) {  // warm + 2 timed
         if (rep == 1) cudaEventRecord(e0, st);
-        ok = cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &res[i].algo, t->ws,
+        ok = cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &res[i].algo, ws,
                             t->ws_bytes, st) == CUBLAS_STATUS_SUCCESS;
       }
       if (!ok) continue;
@@ -216,44 +241,61 @@ static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void*
     p.algo = res[bi].algo;
     p.have_algo = true;
   }
-  NEST_CUBLAS(cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, t->ws,
+  NEST_CUBLAS(cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &p.algo, ws,
                              t->ws_bytes, st));
 }
 
-void tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st) {
+double tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st) {
   Tower* t = reinterpret_cast<Tower*>(c.tower);
   const int64_t bm = rows / c.F;
-  if (bm == 0) return;
+  if (bm == 0) return 0.0;
   NEST_CHECK(bm <= t->bmax, NEST_ERR_CAPACITY, "tower batch exceeds max_batch");
-  NEST_CUBLAS(cublasSetStream(t->h, st));
   const int L = t->L, H = t->H, in0 = t->in0, M = int(bm);
+  auto X = [&](int l) { return t->x + t->xoff[l]; };                     // input of layer l
+  auto W = [&](int l) { return t->w + t->woff[l]; };
+  auto DY = [&](int l) { return l == L - 1 ? t->gtop : t->dy + int64_t(l) * t->bmax * H; };
+  auto IN = [&](int l) { return l == 0 ? in0 : H; };
+  // the previous call's dW GEMMs still read X and dY
+  if (t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
+  t->dw_pending = false;
   k_cast_bf16<<<148 * 8, 256, 0, st>>>(pooled, t->x, bm * in0 / 4);
   NEST_LAUNCH_CHECK();
-  // forward: X_l = X_{l-1} W_l^T  (the last layer's output Y_L is not needed)
-  for (int l = 0; l < L - 1; ++l) {
-    const int in = l == 0 ? in0 : H;
-    gemm_rm(t, false, true, M, H, in, t->x + t->xoff[l], in, t->w + t->woff[l], in, t->x + t->xoff[l + 1], H,
-            CUDA_R_16BF, st);
+  // forward: X_{l+1} = X_l W_l^T (the last layer's output is not needed:
+  // its gradient is the fixed gtop); the scratch dY_0 takes it
+  for (int l = 0; l < L; ++l)
+    gemm_rm(t, false, true, M, H, IN(l), X(l), IN(l), W(l), IN(l), l + 1 < L ? X(l + 1) : t->dy, H, CUDA_R_16BF,
+            st, t->ws);
+  // backward, input-gradient chain: dY_{l-1} = dY_l W_l, dX_0 = dY_0 W_0 (fp32)
+  for (int l = L - 1; l >= 1; --l)
+    gemm_rm(t, false, false, M, H, H, DY(l), H, W(l), H, DY(l - 1), H, CUDA_R_16BF, st, t->ws);
+  gemm_rm(t, false, false, M, in0, H, DY(0), H, W(0), in0, dout, in0, CUDA_R_32F, st, t->ws);
+  // weight gradients dW_l = dY_l^T X_l
+  cudaStream_t ws = st;
+  if (t->defer_dw) {
+    NEST_CUDA(cudaEventRecord(t->ev_dx, st));
+    NEST_CUDA(cudaStreamWaitEvent(t->side, t->ev_dx, 0));
+    ws = t->side;
   }
-  {  // last layer forward (output discarded: dY_L is the fixed gradient)
-    const int in = L == 1 ? in0 : H;
-    gemm_rm(t, false, true, M, H, in, t->x + t->xoff[L - 1], in, t->w + t->woff[L - 1], in, t->dy[1], H,
-            CUDA_R_16BF, st);
+  const double flops_dw = 2.0 * M * (double(in0) * H + double(L - 1) * H * H);
+  {
+    ProfScope ps(c, ST_TOWER_DW, SK_AUX, ws);
+    for (int l = L - 1; l >= 0; --l)
+      gemm_rm(t, true, false, H, IN(l), M, DY(l), H, X(l), IN(l), t->dw, IN(l), CUDA_R_16BF, ws,
+              t->defer_dw ? t->ws_dw : t->ws);
+    ps.bytes = flops_dw;
+    ps.launches = 0;
   }
-  // backward
-  const __nv_bfloat16* dy = t->gtop;
-  int cur = 0;
-  for (int l = L - 1; l >= 0; --l) {
-    const int in = l == 0 ? in0 : H;
-    gemm_rm(t, true, false, H, in, M, dy, H, t->x + t->xoff[l], in, t->dw, in, CUDA_R_16BF, st);  // dW_l
-    if (l == 0) {
-      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, dout, in, CUDA_R_32F, st);  // dX_0 (fp32)
-    } else {
-      gemm_rm(t, false, false, M, in, H, dy, H, t->w + t->woff[l], in, t->dy[cur], in, CUDA_R_16BF, st);
-      dy = t->dy[cur];
-      cur ^= 1;
-    }
+  if (t->defer_dw) {
+    NEST_CUDA(cudaEventRecord(t->ev_dw, t->side));
+    t->dw_pending = true;
   }
+  return t->defer_dw ? 2.0 * flops_dw : 3.0 * flops_dw;   // FLOPs on `st` (fwd + dX [+ dW])
+}
+
+// make `st` wait for outstanding dW GEMMs (context teardown / host reads)
+void tower_join(Ctx& c, cudaStream_t st) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  if (t && t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
 }
 
 }  // namespace nest

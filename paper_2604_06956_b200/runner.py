@@ -191,4 +191,5 @@ class Runner:
         for other in (self.comm, self.dense, self.aux):
             if other is not s:
                 s.wait_stream(other)
+        self.ctx.join(s)
         return s
