@@ -4,9 +4,17 @@
 One step = the whole hot path of SURVEY.md §8(a) over one batch per GPU:
 FWP schedule, DBP route of the next batch (dedup, count exchange, key
 All2All, owner dedup, prefetch gather), the frozen window of N micro-batches
-(send gather, embedding All2All, pool, stand-in tower fwd+bwd, segment-sum,
-gradient All2All), the fused owner reduce + SGD + write-back, and the
-dual-buffer refresh.  Weak scaling: 65,536 samples per GPU, fixed tables.
+(send gather, embedding All2All, pool, segment-sum, gradient All2All), the
+fused owner reduce + SGD + write-back, and the dual-buffer refresh.  Weak
+scaling: 65,536 samples per GPU, fixed tables.
+
+The headline `value` is the step with the stand-in dense tower as FWP's
+overlap partner (variant E+T; north_star: "the overlap partner, not the
+product"; its scaling target is "with FWP hiding most All2All behind dense
+compute").  Also reported: the same step at the other micro-batch count
+(`fwp.with_tower`: exposed All2All without / with FWP) and the embedding
+step alone (`embedding_only`, variant E: the loss gradient of the pooled rows
+is a fixed tensor).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -52,12 +60,13 @@ def parse():
                     help="FWP micro-batches N; 0 = auto (1; N = 2 is measured alongside)")
     ap.add_argument("--schedule", default="sequential", choices=["sequential", "clustered"])
     ap.add_argument("--variant", default="et", choices=["et", "e"],
-                    help="et: embedding + stand-in tower (FWP overlap partner); e: embedding only")
+                    help="et: embedding + stand-in tower (FWP overlap partner; headline); e: embedding only")
     ap.add_argument("--batches", type=int, default=3, help="distinct batches cycled per rank")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-fwp-compare", action="store_true")
+    ap.add_argument("--no-fwp-compare", action="store_true",
+                    help="skip the secondary runs (other micro-batch count, other variant)")
     ap.add_argument("--trace", default="", help="write the per-stage trace JSON here")
     return ap.parse_args()
 
@@ -185,6 +194,8 @@ def config_json(args, cfg, world):
             "micro_batches": args.micro_batches, "schedule": args.schedule,
             "variant": "E+T (embedding + stand-in tower)" if args.variant == "et" else "E (embedding only)",
             "tower": f"{cfg.tower_layers}x{cfg.tower_hidden} bf16 cuBLAS" if args.variant == "et" else None,
+            "dout": "stand-in tower input gradient" if args.variant == "et" else
+                    "fixed seeded loss gradient of the pooled rows (N(0, 1e-2))",
             "parallelism": f"tables row-sharded over {world} GPU(s), data-parallel samples",
             "l2": "inputs larger than L2 (tables 4*rows*dim bytes, GB-scale per-step traffic)",
             "pipelined": "DBP (route t+1 on aux stream) + FWP (comm/compute streams)"}
@@ -236,6 +247,7 @@ def main():
         dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
         U = int(t.item())
     Nctx = max(N, 2) if world > 1 else N      # room for the FWP comparison run
+    with_tower = cfg.pooling == "sum" and (args.variant == "et" or not args.no_fwp_compare)
     mb_rows = min(K, Nctx * U) + 1024
     uids = None
     if world > 1:
@@ -245,7 +257,7 @@ def main():
     ctx = NestContext(cfg.table_rows, d, num_features=F, world=world, rank=rank, pooling=cfg.pooling,
                       max_keys=K + 1024,
                       max_batch=B, max_micro_batches=Nctx, seed=args.seed + 1, init_mode="uniform",
-                      tower_layers=cfg.tower_layers if args.variant == "et" else 0,
+                      tower_layers=cfg.tower_layers if with_tower else 0,
                       tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev,
                       max_recv_keys=int(1.5 * U) + 1024 if world > 1 else U + 1024,
                       max_mb_rows=mb_rows,
@@ -256,8 +268,8 @@ def main():
     host_b = [(torch.from_numpy(k).pin_memory(), torch.from_numpy(o).pin_memory()) for k, o in batches]
     lr = 1e-3 / (B * world)
 
-    def make_dout_fn(runner):
-        if args.variant == "et":
+    def make_dout_fn(variant):
+        if variant == "et":
             douts = {}
 
             def fn(t, i, pooled):
@@ -282,9 +294,9 @@ def main():
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    def timed(runner, steps, t0, source=None, profile=False):
+    def timed(runner, steps, t0, source=None, profile=False, variant=None):
         """Runs `steps` steps; returns device ms (max over ranks)."""
-        dout_fn = make_dout_fn(runner)
+        dout_fn = make_dout_fn(variant or args.variant)
         barrier()
         if profile:
             ctx.profile_enable(True)
@@ -351,21 +363,56 @@ def main():
                "d2h_bytes_per_step": d2h // args.steps + counts_bytes,
                "ms_per_step": ms_e / args.steps}
 
-    # exposed All2All with and without FWP: the same step at the other N
-    # (N = 2 micro-batches when the main run is N = 1, N = 1 otherwise)
-    other_fwp = None
-    if world > 1 and not args.no_fwp_compare:
-        N2 = 2 if N == 1 else 1
-        if N2 <= ctx.cfg.max_micro_batches:
-            r1 = Runner(ctx, N=N2, schedule=args.schedule if N2 > 1 else "sequential", pipelined=True,
-                        lr_over_B=lr)
-            r1.t = runner.t + args.steps
-            timed(r1, 3, r1.t)
-            k2 = max(5, args.steps // 2)
-            ms1, prof1, _, _ = timed(r1, k2, r1.t, profile=True)
-            other_fwp = {"N": N2, "ms_per_step": ms1 / k2, "samples_per_s": B * world * k2 / (ms1 / 1e3),
-                         "a2a_exposed_ms_per_step": prof1["summary"]["a2a_exposed_ms"] / k2,
-                         "a2a_ms_per_step": prof1["summary"]["a2a_ms"] / k2}
+    # the same step with the stand-in dense tower (FWP's overlap partner):
+    # N = 1 (no FWP) and, when there is an All2All to hide, N = 2 (FWP)
+    def tower_run(Nv, t0):
+        r1 = Runner(ctx, N=Nv, schedule=args.schedule if Nv > 1 else "sequential", pipelined=True,
+                    lr_over_B=lr)
+        r1.t = t0
+        timed(r1, 3, r1.t, variant="et")
+        k2 = max(5, args.steps // 2)
+        ms1, prof1, _, _ = timed(r1, k2, r1.t, profile=True, variant="et")
+        sm, st1 = prof1["summary"], prof1["stages"]
+        tw = st1["tower"]
+        out = {"N": Nv, "steps": k2, "ms_per_step": ms1 / k2, "samples_per_s": B * world * k2 / (ms1 / 1e3),
+               "tower_ms_per_step": tw["ms"] / k2,
+               "tower_tflops": (tw["bytes"] + st1["tower_dw"]["bytes"]) / ((tw["ms"] + st1["tower_dw"]["ms"]) * 1e9)
+               if tw["ms"] else None}
+        if world > 1:
+            out["a2a_ms_per_step"] = sm["a2a_ms"] / k2
+            out["a2a_exposed_ms_per_step"] = sm["a2a_exposed_ms"] / k2
+            out["a2a_exposed_ratio"] = sm["a2a_exposed_ms"] / sm["a2a_ms"] if sm["a2a_ms"] else None
+        return out, r1.t
+
+    def embedding_run(Nv, t0):
+        r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr)
+        r1.t = t0
+        timed(r1, 3, r1.t, variant="e")
+        ms1, prof1, _, _ = timed(r1, args.steps, r1.t, profile=True, variant="e")
+        st1 = prof1["stages"]
+        return {"N": Nv, "steps": args.steps, "ms_per_step": ms1 / args.steps,
+                "samples_per_s": B * world * args.steps / (ms1 / 1e3),
+                "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in st1.items() if v["records"]}}
+
+    with_tower_runs, embedding_only = None, None
+    if not args.no_fwp_compare:
+        tnext = runner.t + args.steps + 8
+        if args.variant == "et":
+            with_tower_runs = {f"N{N}": {"N": N, "ms_per_step": ms / args.steps, "samples_per_s": value,
+                                         "a2a_ms_per_step": prof["summary"]["a2a_ms"] / args.steps,
+                                         "a2a_exposed_ms_per_step": prof["summary"]["a2a_exposed_ms"] / args.steps,
+                                         "main_run": True}}
+            if world > 1:
+                N2 = 2 if N == 1 else 1
+                if N2 <= ctx.cfg.max_micro_batches:
+                    res, tnext = tower_run(N2, tnext)
+                    with_tower_runs[f"N{N2}"] = res
+            embedding_only = embedding_run(N, tnext + 8)
+        elif with_tower:
+            with_tower_runs = {}
+            for Nv in ([1, 2] if world > 1 and ctx.cfg.max_micro_batches >= 2 else [1]):
+                res, tnext = tower_run(Nv, tnext)
+                with_tower_runs[f"N{Nv}"] = res
 
     if rank == 0:
         hbm_peak, bf16_peak, src = peaks()
@@ -418,7 +465,7 @@ def main():
                    # 2 GPUs, 403 GB/s at 4 GPUs per GPU per direction
                    "probe_all2all_ceiling_gbs": {2: 691.2, 4: 403.3}.get(world),
                    "transport": os.environ.get("NEST_A2A", "fused"),
-                   "compare_other_N": other_fwp}
+                   "with_tower": with_tower_runs}
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, args.seed)
@@ -435,7 +482,8 @@ def main():
                         "owner_unique_per_step": st["gather"]["units"] / max(1, st["gather"]["records"]),
                         "intersection_ratio": (st["refresh"]["units"] / st["gather"]["units"]
                                                if st["gather"]["units"] else None)},
-                "fwp": fwp_stats}
+                "fwp": dict(fwp_stats, with_tower=with_tower_runs),
+                "embedding_only": embedding_only}
         if args.trace:
             json.dump({"stages": st, "summary": summ}, open(args.trace, "w"), indent=1)
         print(json.dumps(line), flush=True)

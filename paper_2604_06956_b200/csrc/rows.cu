@@ -60,6 +60,13 @@ static int row_ilp() {
     default: { constexpr int IL = 1; __VA_ARGS__; } break;               \
   }
 
+// resident blocks to ask of ptxas for a kernel holding IL row vectors per lane
+// group in flight: full occupancy (32 registers) for one float4 per lane
+template <int D>
+constexpr int ilp_min_blocks(int il) {
+  return il * RowGeom<D>::VPL <= 1 ? 8 : il * RowGeom<D>::VPL <= 2 ? 4 : 2;
+}
+
 // group id / count helpers for grid-stride loops over rows
 template <int D>
 struct Grp {
@@ -159,7 +166,7 @@ void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st) {
 // IL bags per lane group at once (bags q, q + ng, ...), two rows of each in
 // flight per pass, each bag summed left to right
 template <int D, bool W1, int IL>
-__global__ void __launch_bounds__(kRowThreads) k_pool(int64_t nrows, int F,
+__global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_pool(int64_t nrows, int F,
                                                       const int32_t* __restrict__ perm_mb,
                                                       const int32_t* __restrict__ bag_off,
                                                       const int32_t* __restrict__ inverse,
@@ -355,7 +362,7 @@ __device__ __forceinline__ void put_grad(const PeerRows& m, int64_t k, int D, in
 // IL cold segments per lane group at once (k, k + ng, ...), two rows of each
 // in flight per pass, each segment summed in occurrence order
 template <int D, int IL>
-__global__ void __launch_bounds__(kRowThreads) k_segsum_cold(int64_t Ui, int chunk,
+__global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_segsum_cold(int64_t Ui, int chunk,
                                                              const int32_t* __restrict__ seg_start,
                                                              const int32_t* __restrict__ sval,
                                                              const float* __restrict__ dout,
