@@ -466,6 +466,9 @@ def main():
                    "probe_all2all_ceiling_gbs": {2: 691.2, 4: 403.3}.get(world),
                    "transport": os.environ.get("NEST_A2A", "fused"),
                    "with_tower": with_tower_runs}
+        # the dual-buffer refresh (fused with the re-push under the early push)
+        rname = "emb_repush" if st["emb_repush"]["records"] else "refresh"
+        rs = st[rname]
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, args.seed)
@@ -477,10 +480,11 @@ def main():
                 "stages": stages,
                 "trace": {"span_ms_per_step": summ["span_ms"] / steps,
                           "compute_busy_ms_per_step": summ["compute_busy_ms"] / steps},
-                "dbp": {"refresh_ms_per_step": st["refresh"]["ms"] / max(1, st["refresh"]["records"]),
-                        "refreshed_rows_per_step": st["refresh"]["units"] / max(1, st["refresh"]["records"]),
+                "dbp": {"refresh_ms_per_step": rs["ms"] / max(1, rs["records"]),
+                        "refresh_stage": rname,
+                        "refreshed_rows_per_step": rs["units"] / max(1, rs["records"]),
                         "owner_unique_per_step": st["gather"]["units"] / max(1, st["gather"]["records"]),
-                        "intersection_ratio": (st["refresh"]["units"] / st["gather"]["units"]
+                        "intersection_ratio": (rs["units"] / st["gather"]["units"]
                                                if st["gather"]["units"] else None)},
                 "fwp": dict(fwp_stats, with_tower=with_tower_runs),
                 "embedding_only": embedding_only}

@@ -177,7 +177,11 @@ NEST_API nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys,
  * shard into the slot's HBM buffer.  keys/bag_offsets: the local batch (nnz
  * occurrences, B samples).  perm/mb_offsets from nest_fwp_schedule (NULL =
  * one micro-batch, N must be 1).  The gather is ordered after the previous
- * update's write-back (events inside the library, reading Q8). */
+ * update's write-back (events inside the library, reading Q8).  With the
+ * fused NVLink transport (world > 1, NEST_A2A unset, NEST_EARLY_PUSH != 0)
+ * the owner then pushes every requested row of the buffer into the
+ * requesters' receive rows of this slot (the embedding All2All, issued here
+ * on `stream` instead of inside the window). */
 NEST_API nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys,
                          const int32_t* bag_offsets, int64_t nnz, int32_t B,
                          const int32_t* perm, const int32_t* mb_offsets, int32_t N,
@@ -186,7 +190,10 @@ NEST_API nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* 
 /* Dual-buffer synchronization: for every key k in both
  * the active slot's and the prefetch slot's owner key sets, copy the active
  * (already updated) row over the prefetch row.  Waits inside for the active
- * slot's update and the prefetch slot's gather. */
+ * slot's update and the prefetch slot's gather.  After an early push (see
+ * nest_route) the same rows are re-pushed to the requesters that hold stale
+ * copies.  Collective in the early-push mode: every rank calls it for the
+ * same slots. */
 NEST_API nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot,
                                int32_t prefetch_slot, void* stream);
 
@@ -264,11 +271,12 @@ NEST_API nest_status_t nest_exchange_plan(const nest_config_t* cfg, int32_t N,
                                           const int32_t* all_counts, nest_exchange_plan_t* plan);
 
 /* ---- tracing: CUDA events around every stage of the path ---- */
-enum { NEST_PROFILE_STAGES = 15 };
+enum { NEST_PROFILE_STAGES = 16 };
 typedef struct {
   char name[24];        /* stage: schedule, route, sort, key_a2a, owner_dedup, gather, refresh,
                            send_gather, emb_a2a, pool, tower, segsum, grad_a2a, update,
-                           tower_dw (the tower's deferred weight gradients, internal stream) */
+                           tower_dw (the tower's deferred weight gradients, internal stream),
+                           emb_repush (early-push transport: rows the refresh re-sent) */
   int32_t stream;       /* 0 compute, 1 comm, 2 aux */
   int32_t records;      /* instrumented calls */
   int32_t launches;     /* libnest kernels launched by those calls (NCCL / cuBLAS not counted) */

@@ -26,7 +26,7 @@ SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_s
            "nest_tower_fwd_bwd", "nest_join",
            "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
            "nest_profile_read", "nest_last_error"]
-PROFILE_STAGES = 15
+PROFILE_STAGES = 16
 
 
 class NestError(RuntimeError):

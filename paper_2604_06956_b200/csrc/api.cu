@@ -330,7 +330,8 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       NEST_CUDA(cudaMallocHost(&s.h_xfer, sizeof(int32_t) * (int64_t(c->W) * c->W * Nc + c->Nmax + 1)));
       NEST_CUDA(cudaMemsetAsync(s.n_owner, 0, sizeof(int32_t), st0));
       NEST_CUDA(cudaMemsetAsync(s.off, 0, sizeof(int32_t) * (c->W + 1), st0));
-      cudaEvent_t* evs[] = {&s.ev_gather, &s.ev_update, &s.ev_free, &s.ev_ready, &s.ev_sync};
+      cudaEvent_t* evs[] = {&s.ev_gather, &s.ev_update, &s.ev_free, &s.ev_ready, &s.ev_sync, &s.ev_early,
+                            &s.ev_repush};
       for (auto* e : evs) NEST_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
       for (int i = 0; i < NEST_MAX_MICRO_BATCHES; ++i) {
         NEST_CUDA(cudaEventCreateWithFlags(&s.ev_emb[i], cudaEventDisableTiming));
@@ -374,7 +375,7 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
   for (auto& s : c->slot) {
     if (s.h_xfer) cudaFreeHost(s.h_xfer);
-    cudaEvent_t evs[] = {s.ev_gather, s.ev_update, s.ev_free, s.ev_ready, s.ev_sync};
+    cudaEvent_t evs[] = {s.ev_gather, s.ev_update, s.ev_free, s.ev_ready, s.ev_sync, s.ev_early, s.ev_repush};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
     for (int i = 0; i < NEST_MAX_MICRO_BATCHES; ++i) {
@@ -445,6 +446,37 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
     s.updated = false;
     s.prefetched = 0;
     s.epoch = ++c->epoch;
+    s.early = s.repushed = false;
+    if (c->early_push) {
+      // early push: every requested row of the prefetch buffer goes to its
+      // requester now, overlapping the current window; rows the current
+      // window updates are re-pushed by nest_dbp_refresh
+      const double row = double(c->D) * sizeof(float);
+      for (int mb = 0; mb < N; ++mb) {
+        const int64_t self = s.all[(size_t(c->rank) * c->W + c->rank) * (c->Nmax + 2) + 1 + mb];
+        if (c->early_push == EP_CE) {
+          // send rows gathered locally, then copy-engine DMA per requester
+          // (no SM time while the window's kernels run)
+          {
+            ProfScope ps(*c, ST_SEND_GATHER, SK_AUX, st);
+            launch_send_gather(*c, s, mb, st, c->send_stage);
+            ps.bytes = 2.0 * row * double(s.info.mb_recv[mb]) + 12.0 * double(s.info.recv);
+          }
+          ProfScope ps(*c, ST_EMB_A2A, SK_AUX, st);
+          xfer_push_emb(*c, s, mb, st, s.ev_emb[mb], c->send_stage);   // signals XK_EMB
+          ps.launches = 0;
+          ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+        } else {
+          ProfScope ps(*c, ST_EMB_A2A, SK_AUX, st);
+          launch_send_push(*c, s, mb, st);
+          ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+          xfer_signal(*c, s, XK_EMB, mb, st);
+        }
+      }
+      NEST_CUDA(cudaEventRecord(s.ev_early, st));
+      s.early = true;
+      s.prefetched = (1u << N) - 1u;
+    }
   });
 }
 
@@ -460,12 +492,31 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
     cudaStream_t st = S(stream);
     NEST_CUDA(cudaStreamWaitEvent(st, a.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, p.ev_gather, 0));
-    ProfScope ps(*c, ST_REFRESH, SK_COMPUTE, st);
-    launch_refresh(*c, a, p, st);
-    // 8 (U_o + U_o') key reads + 2 I rows (I counted on the device)
-    ps.bytes = 8.0 * double(std::min(p.info.recv, c->Uocap));  // U_o' keys + bit tests
-    ps.dcount = c->n_refreshed;
-    ps.bpc = 2.0 * c->D * sizeof(float);
+    if (p.early) {
+      // the requesters' early copies of the intersection are stale too: the
+      // refresh re-pushes exactly those rows (after the early push landed)
+      NEST_CUDA(cudaStreamWaitEvent(st, p.ev_early, 0));
+      {
+        ProfScope ps(*c, ST_EMB_REPUSH, SK_COMPUTE, st);
+        for (int mb = 0; mb < p.N; ++mb) launch_refresh_push(*c, a, p, mb, st);
+        ps.launches = p.N + 1;
+        // N4 (8 U_o' keys + 2 I rows) + the re-pushed rows (not counted: the
+        // requester fan-out of I is known on the device only)
+        ps.bytes = 8.0 * double(std::min(p.info.recv, c->Uocap));
+        ps.dcount = c->n_refreshed;
+        ps.bpc = 2.0 * c->D * sizeof(float);
+      }
+      for (int mb = 0; mb < p.N; ++mb) xfer_signal(*c, p, XK_REPUSH, mb, st);
+      NEST_CUDA(cudaEventRecord(p.ev_repush, st));
+      p.repushed = true;
+    } else {
+      ProfScope ps(*c, ST_REFRESH, SK_COMPUTE, st);
+      launch_refresh(*c, a, p, st);
+      // 8 (U_o + U_o') key reads + 2 I rows (I counted on the device)
+      ps.bytes = 8.0 * double(std::min(p.info.recv, c->Uocap));  // U_o' keys + bit tests
+      ps.dcount = c->n_refreshed;
+      ps.bpc = 2.0 * c->D * sizeof(float);
+    }
     NEST_CUDA(cudaEventRecord(a.ev_free, st));
   });
 }
@@ -478,6 +529,7 @@ nest_status_t nest_lookup_prefetch(nest_ctx_t* ctx, int32_t slot, int32_t mb, vo
     NEST_CHECK(s.routed, NEST_ERR_ORDER, "prefetch before route");
     NEST_CHECK(!s.updated, NEST_ERR_ORDER, "prefetch after the window closed (S:568)");
     NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
+    if (s.early) return;   // pushed at route time
     NEST_CHECK(!((s.prefetched >> mb) & 1u), NEST_ERR_ORDER, "micro-batch already prefetched");
     if (c->W > 1) lookup_comm(*c, s, mb, S(compute), S(comm));
   });
@@ -494,7 +546,15 @@ nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* 
     NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
     NEST_CHECK(out != nullptr, NEST_ERR_INVALID, "null out");
     cudaStream_t cs = S(compute), ms = S(comm);
-    if (c->W > 1) {
+    if (c->W > 1 && s.early) {
+      // rows pushed at route time (+ the refresh's re-push) by every owner
+      NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_early, 0));
+      xfer_wait_emb(*c, s, mb, cs, XK_EMB);
+      if (s.repushed) {
+        NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_repush, 0));
+        xfer_wait_emb(*c, s, mb, cs, XK_REPUSH);
+      }
+    } else if (c->W > 1) {
       if (!((s.prefetched >> mb) & 1u)) lookup_comm(*c, s, mb, cs, ms);
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_emb[mb], 0));
       if (c->xfer_ce) xfer_wait_emb(*c, s, mb, cs);   // every owner's rows have landed

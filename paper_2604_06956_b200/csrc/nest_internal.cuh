@@ -96,6 +96,11 @@ struct Slot {
   uint32_t epoch = 0;              // window sequence number (same on every rank)
   uint32_t prefetched = 0;         // micro-batches whose embedding All2All is issued
   bool routed = false, updated = false;
+  // early push (fused transport, W > 1): the owner pushed every requested row
+  // right after the prefetch gather (`early`); the dual-buffer refresh re-pushed
+  // the rows the previous window updated (`repushed`)
+  bool early = false, repushed = false;
+  cudaEvent_t ev_early = nullptr, ev_repush = nullptr;
   cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
               ev_grad[NEST_MAX_MICRO_BATCHES] = {}, ev_ready = nullptr, ev_sync = nullptr;
 };
@@ -106,7 +111,8 @@ struct Slot {
 // ----------------------------------------------------------------------------
 enum Stage : int {
   ST_SCHEDULE = 0, ST_ROUTE, ST_SORT, ST_KEY_A2A, ST_OWNER_DEDUP, ST_GATHER, ST_REFRESH,
-  ST_SEND_GATHER, ST_EMB_A2A, ST_POOL, ST_TOWER, ST_SEGSUM, ST_GRAD_A2A, ST_UPDATE, ST_TOWER_DW, ST_COUNT
+  ST_SEND_GATHER, ST_EMB_A2A, ST_POOL, ST_TOWER, ST_SEGSUM, ST_GRAD_A2A, ST_UPDATE, ST_TOWER_DW,
+  ST_EMB_REPUSH, ST_COUNT
 };
 enum StreamKind : int { SK_COMPUTE = 0, SK_COMM = 1, SK_AUX = 2 };
 
@@ -168,7 +174,7 @@ struct Ctx {
   float* own_rows = nullptr;       // [OMBcap][d] (== src_rows when W == 1)
   int32_t* d_err = nullptr;        // [1]
   int32_t* d_cnt_scratch = nullptr; // [W*(Nmax)] mb counts scratch
-  int32_t* n_refreshed = nullptr;  // [1] rows copied by the last refresh
+  int32_t* n_refreshed = nullptr;  // [4] rows copied by the last refresh | rows re-pushed off-GPU
   // FWP clustering scratch (cluster.cu)
   uint32_t* cl_bm = nullptr;       // [words+2]
   int32_t* cl_wr = nullptr;        // [words+2]
@@ -190,9 +196,13 @@ struct Ctx {
   int a2a_mode = 0;                // A2AMode
   void* xwin = nullptr;            // library-owned, IPC-exported exchange window
   size_t xwin_bytes = 0, xoff_own = 0, xoff_flags = 0;
-  uint32_t* xflags = nullptr;      // [2][Nmax][W] epoch flags written by peers
+  uint32_t* xflags = nullptr;      // [2 slots][3 kinds][Nmax][W] epoch flags written by peers
+  int early_push = 0;              // EarlyPush: embedding rows pushed at route time (fused transport)
+  float* send_stage = nullptr;     // [OMBcap][d] early push send rows (copy-engine early push)
+  int64_t src_slot_stride = 0;     // floats between the two slots' receive windows (0: shared)
   std::vector<void*> peer_win;
   std::vector<float*> peer_src, peer_own;
+  std::vector<float*> peer_src_slot[2];  // each peer's receive rows of slot 0 / 1
   std::vector<uint32_t*> peer_flags;
   ncclComm_t comm = nullptr, comm_aux = nullptr;
   nest_status_t sticky = NEST_OK;
@@ -200,6 +210,13 @@ struct Ctx {
   // tower (cuBLAS), see tower.cu
   void* tower = nullptr;
 };
+
+// receive rows of a slot (this rank / peer p's window)
+inline int slot_index(const Ctx& c, const Slot& s) { return int(&s - c.slot); }
+inline float* src_rows_of(const Ctx& c, const Slot& s) {
+  return c.src_rows + slot_index(c, s) * c.src_slot_stride;
+}
+inline float* peer_src_of(const Ctx& c, const Slot& s, int p) { return c.peer_src_slot[slot_index(c, s)][p]; }
 
 // bump allocator over a caller-owned buffer (base == nullptr: size only)
 struct Carver {
@@ -438,7 +455,7 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
 void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p);
 void launch_init_tables(Ctx& c, cudaStream_t st);
 void launch_gather(Ctx& c, Slot& s, cudaStream_t st);
-void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_rows = nullptr);
 void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st);
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st);
 void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st);
@@ -480,10 +497,14 @@ struct PeerRows {
   float sgd_lr;
 };
 enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
+enum EarlyPush : int { EP_OFF = 0, EP_CE = 1, EP_SM = 2 };
 int a2a_mode_wanted(int W);
 int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb);
 int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb);
 void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st);
+// dual-buffer refresh a -> p fused with the re-push of the refreshed rows to
+// every requester of micro-batch mb of slot p (early push)
+void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st);
 void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st);
 void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, float lr, cudaStream_t st);
 void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st);
@@ -491,8 +512,11 @@ void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st);
 bool xfer_wanted(int W);
 void xfer_setup(Ctx& c, cudaStream_t st);
 void xfer_destroy(Ctx& c);
-void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_self);
-void xfer_wait_emb(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_self,
+                   const float* send_rows = nullptr);
+// flag kinds: 0 embedding rows, 1 gradient rows, 2 re-pushed embedding rows
+enum XferKind : int { XK_EMB = 0, XK_GRAD = 1, XK_REPUSH = 2, XK_COUNT = 3 };
+void xfer_wait_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, int kind = XK_EMB);
 void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st);
 void xfer_wait_grads(Ctx& c, Slot& s, cudaStream_t st);
 void tower_create(Ctx& c);

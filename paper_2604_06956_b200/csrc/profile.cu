@@ -12,7 +12,8 @@ namespace nest {
 static_assert(int(ST_COUNT) == int(NEST_PROFILE_STAGES), "stage table out of sync with include/nest.h");
 static const char* kStageName[ST_COUNT] = {"schedule", "route", "sort", "key_a2a", "owner_dedup",
                                            "gather", "refresh", "send_gather", "emb_a2a", "pool",
-                                           "tower", "segsum", "grad_a2a", "update", "tower_dw"};
+                                           "tower", "segsum", "grad_a2a", "update", "tower_dw",
+                                           "emb_repush"};
 
 static cudaEvent_t take_event(Profiler& p) {
   if (p.next_ev == p.pool.size()) {
@@ -130,10 +131,10 @@ void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* 
     g.bytes += bytes;
     t_min = std::min(t_min, double(t0));
     t_max = std::max(t_max, double(t1));
-    if (r.stage == ST_EMB_A2A || r.stage == ST_GRAD_A2A) {
+    if (r.stage == ST_EMB_A2A || r.stage == ST_GRAD_A2A || r.stage == ST_EMB_REPUSH) {
       a2a.emplace_back(t0, t1);
       a2a_ms += double(t1) - double(t0);
-    } else if (r.stage == ST_POOL || r.stage == ST_TOWER || r.stage == ST_SEGSUM) {
+    } else if (r.stage == ST_POOL || r.stage == ST_TOWER || r.stage == ST_SEGSUM || r.stage == ST_TOWER_DW) {
       // the compute lane: dense forward/backward of the window
       comp.emplace_back(t0, t1);
     }

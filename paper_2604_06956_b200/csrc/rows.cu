@@ -147,10 +147,10 @@ __global__ void __launch_bounds__(kRowThreads) k_send_gather(int64_t R, int mb,
   }
 }
 
-void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st) {
+void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_rows) {
   const int64_t R = s.info.recv;
   if (R == 0) return;
-  float* out = c.own_rows + s.own_base[mb] * c.D;
+  float* out = (out_rows ? out_rows : c.own_rows) + s.own_base[mb] * c.D;
   const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(int nsamp, int F,
 
 void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
   const bool w1 = c.W == 1;
-  const float* src = w1 ? s.buffer : c.src_rows + s.src_base[mb] * c.D;
+  const float* src = w1 ? s.buffer : src_rows_of(c, s) + s.src_base[mb] * c.D;
   const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
   const int32_t* perm_mb = s.perm + int64_t(mb) * s.cap;
   NEST_DISPATCH_D(c.D, {
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
 // local gradient rows of micro-batch mb (NCCL / CE transports send them)
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) {
   PeerRows out{};
-  out.base[0] = c.src_rows + s.src_base[mb] * c.D;
+  out.base[0] = src_rows_of(c, s) + s.src_base[mb] * c.D;
   out.off[0] = 0;
   out.off[1] = int32_t(s.info.mb_uniq[mb]);
   out.n = 1;
@@ -528,27 +528,84 @@ __global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, co
   __threadfence_system();
 }
 
-void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
-  const int64_t R = s.info.recv;
-  if (R == 0) return;
+// R5 + re-push (early push): for every owner key u of slot p whose shard row
+// the active slot wrote back (bit in bm_a), copy the row into p's buffer
+// (mb == 0 only) and store it into the receive row of every requester s that
+// asked for u in micro-batch mb: src_tab[u][s] = r, row sendpos[r] of s's
+// range.  The row is read once for all its requesters.
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_refresh_push(
+    const int32_t* __restrict__ n_p, const int32_t* __restrict__ rows_p, const uint32_t* __restrict__ bm_a,
+    const float* __restrict__ shard, float* __restrict__ buf_p, const int32_t* __restrict__ src_tab, int W,
+    int mb, const int64_t* __restrict__ recv, const int32_t* __restrict__ sendpos, const PeerRows out,
+    int32_t* __restrict__ count) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL;
+  const int64_t n = *n_p;
+  int32_t local = 0;
+  for (int64_t u = gp.g; u < n; u += gp.ng) {
+    const uint32_t ld = uint32_t(__ldg(rows_p + u));
+    if (!bit_test(bm_a, ld)) continue;
+    float4 v[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) v[q] = ldg_f4(shard + int64_t(ld) * D + gp.col(q));
+    if (mb == 0) {
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) st_f4(buf_p + u * D + gp.col(q), v[q]);
+      if (gp.l == 0) ++local;
+    }
+    for (int s = 0; s < W; ++s) {
+      const int32_t r = __ldg(src_tab + u * W + s);
+      if (r < 0 || !((uint64_t(__ldg(recv + r)) >> (56 + mb)) & 1u)) continue;
+      float* dst = out.base[s] + int64_t(__ldg(sendpos + r) - out.off[s]) * D;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) st_f4(dst + gp.col(q), v[q]);
+    }
+  }
+  if (local) atomicAdd(count, local);
+  __threadfence_system();
+}
+
+// destination map of micro-batch mb's rows: requester p's range of the
+// owner's source-major send positions -> p's receive rows of the slot
+static PeerRows send_map(Ctx& c, Slot& s, int mb) {
   const int W = c.W, Nc = c.Nmax + 2;
   PeerRows out{};
   int64_t acc = 0;
-  for (int p = 0; p < W; ++p) {      // source-major send positions
+  for (int p = 0; p < W; ++p) {
     int64_t dst = src_base_at(s, c, p, mb);
     for (int o = 0; o < c.rank; ++o) dst += s.all[(size_t(p) * W + o) * Nc + 1 + mb];
-    out.base[p] = c.peer_src[p] + dst * c.D;
+    out.base[p] = peer_src_of(c, s, p) + dst * c.D;
     out.off[p] = int32_t(acc);
     acc += s.all[(size_t(p) * W + c.rank) * Nc + 1 + mb];
   }
   out.off[W] = int32_t(acc);
   out.n = W;
   out.fence = 1;
+  return out;
+}
+
+void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
+  const int64_t R = s.info.recv;
+  if (R == 0) return;
+  const PeerRows out = send_map(c, s, mb);
   const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
-                                                                              s.buffer, out);
+    k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp, s.buffer, out);
+  });
+  NEST_LAUNCH_CHECK();
+}
+
+void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st) {
+  if (mb == 0) NEST_CUDA(cudaMemsetAsync(c.n_refreshed, 0, sizeof(int32_t), st));
+  if (p.info.recv == 0) return;
+  const PeerRows out = send_map(c, p, mb);
+  const int32_t* sp = p.sendpos + int64_t(mb) * (c.Rcap + 1);
+  NEST_DISPATCH_D(c.D, {
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    k_refresh_push<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
+        p.n_owner, p.owner_rows, a.obm, c.shard, p.buffer, p.src_tab, c.W, mb, p.recv, sp, out, c.n_refreshed);
   });
   NEST_LAUNCH_CHECK();
 }
@@ -663,7 +720,7 @@ void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st) {
     if (w1)
       k_reduce_sgd<D, true><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, 1, lr, b, s.mask, s.pos, c.Kcap + 1, nullptr, nullptr, nullptr, 0,
-          c.src_rows, s.owner_rows, s.buffer, c.shard);
+          src_rows_of(c, s), s.owner_rows, s.buffer, c.shard);
     else
       k_reduce_sgd<D, false><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, c.W, lr, b, nullptr, nullptr, 0, s.src_tab, s.recv, s.sendpos, c.Rcap + 1,

@@ -14,6 +14,16 @@
 // need resetting.  Buffer reuse is safe by causality: an owner pushes batch
 // t+1's rows only after its update(t), which waited for every requester's
 // gradient push of batch t, i.e. after every requester stopped using its rows.
+//
+// Early push (fused transport; NEST_EARLY_PUSH = sm (default) | ce | 0): the
+// owner pushes batch t+1's rows at the end of its route (right after the
+// prefetch gather, during window t) into a second receive window, one per
+// slot -- by copy engine from a send-staging buffer (ce) or by SM remote
+// stores (sm) -- and after update(t) the dual-buffer refresh re-pushes only
+// the rows update(t) wrote back (P:363-380's intersection, applied to the
+// requesters' copies) from the same kernel that refreshes the owner's buffer.  The same causality argument holds per slot: route(t+1) on the
+// owner follows update(t-1) of that slot, after every requester stopped
+// reading the slot's window.
 #include <cuda.h>
 
 #include <cstring>
@@ -53,12 +63,26 @@ int a2a_mode_wanted(int W) {
 }
 bool xfer_wanted(int W) { return a2a_mode_wanted(W) != A2A_NCCL; }
 
-// window layout: [src_rows MBcap*D f32 | own_rows OMBcap*D f32 | flags 2*Nmax*W u32]
+static int early_push_wanted() {
+  const char* e = std::getenv("NEST_EARLY_PUSH");
+  if (e && std::strcmp(e, "0") == 0) return EP_OFF;
+  if (e && std::strcmp(e, "ce") == 0) return EP_CE;
+  return EP_SM;   // measured best at W = 2: sm 4.57, off 4.61, ce 4.92 ms/step
+}
+
+// window layout: [src_rows of slot 0 (| slot 1 with early push) MBcap*D f32 |
+//                 own_rows OMBcap*D f32 | flags [2][3][Nmax][W] u32]
 void xfer_setup(Ctx& c, cudaStream_t st) {
   load_driver_ops();
-  const size_t src_b = align_up(size_t(c.MBcap) * c.D * sizeof(float), 4096);
+  c.a2a_mode = a2a_mode_wanted(c.W);
+  c.early_push = c.a2a_mode == A2A_FUSED ? early_push_wanted() : EP_OFF;
+  if (c.early_push == EP_CE)
+    NEST_CUDA(cudaMalloc(&c.send_stage, std::max<size_t>(size_t(c.OMBcap) * c.D * sizeof(float), 256)));
+  const size_t src1 = align_up(size_t(c.MBcap) * c.D * sizeof(float), 4096);
+  const size_t src_b = c.early_push ? 2 * src1 : src1;
   const size_t own_b = align_up(size_t(c.OMBcap) * c.D * sizeof(float), 4096);
-  const size_t flg_b = align_up(size_t(2) * c.Nmax * c.W * sizeof(uint32_t), 4096);
+  const size_t flg_b = align_up(size_t(2) * XK_COUNT * c.Nmax * c.W * sizeof(uint32_t), 4096);
+  c.src_slot_stride = c.early_push ? int64_t(src1 / sizeof(float)) : 0;
   c.xwin_bytes = src_b + own_b + flg_b;
   NEST_CUDA(cudaMalloc(&c.xwin, c.xwin_bytes));
   NEST_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(c.xwin) + src_b + own_b, 0, flg_b, st));
@@ -70,10 +94,11 @@ void xfer_setup(Ctx& c, cudaStream_t st) {
   // exchange IPC handles (+ window geometry) through the aux communicator
   struct Rec {
     cudaIpcMemHandle_t h;
-    uint64_t own, flags, bytes;
+    uint64_t own, flags, bytes, src_stride;
   };
   Rec mine{};
   NEST_CUDA(cudaIpcGetMemHandle(&mine.h, c.xwin));
+  mine.src_stride = uint64_t(c.src_slot_stride);
   mine.own = c.xoff_own;
   mine.flags = c.xoff_flags;
   mine.bytes = c.xwin_bytes;
@@ -89,6 +114,8 @@ void xfer_setup(Ctx& c, cudaStream_t st) {
   c.peer_src.assign(c.W, nullptr);
   c.peer_own.assign(c.W, nullptr);
   c.peer_flags.assign(c.W, nullptr);
+  c.peer_src_slot[0].assign(c.W, nullptr);
+  c.peer_src_slot[1].assign(c.W, nullptr);
   for (int p = 0; p < c.W; ++p) {
     char* base;
     if (p == c.rank) {
@@ -100,13 +127,14 @@ void xfer_setup(Ctx& c, cudaStream_t st) {
       c.peer_win[p] = ptr;
     }
     c.peer_src[p] = reinterpret_cast<float*>(base);
+    c.peer_src_slot[0][p] = c.peer_src[p];
+    c.peer_src_slot[1][p] = c.peer_src[p] + all[p].src_stride;
     c.peer_own[p] = reinterpret_cast<float*>(base + all[p].own);
     c.peer_flags[p] = reinterpret_cast<uint32_t*>(base + all[p].flags);
   }
   // (no barrier needed: the first push happens after the first route's count
   // exchange, a collective every rank enters after this setup)
   c.xfer_ce = true;
-  c.a2a_mode = a2a_mode_wanted(c.W);
 }
 
 void xfer_destroy(Ctx& c) {
@@ -115,10 +143,12 @@ void xfer_destroy(Ctx& c) {
   c.peer_win.clear();
   if (c.xwin) cudaFree(c.xwin);
   c.xwin = nullptr;
+  if (c.send_stage) cudaFree(c.send_stage);
+  c.send_stage = nullptr;
 }
 
-static inline size_t flag_index(const Ctx& c, int kind, int mb, int src) {
-  return (size_t(kind) * c.Nmax + mb) * c.W + src;
+static inline size_t flag_index(const Ctx& c, const Slot& s, int kind, int mb, int src) {
+  return ((size_t(slot_index(c, s)) * XK_COUNT + kind) * c.Nmax + mb) * c.W + src;
 }
 
 // rows: [W][W][Nc] counts of the slot; base_of(p, i) = row base of micro-batch
@@ -141,7 +171,8 @@ int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb) {
 // R7: owner `rank` pushes micro-batch mb's rows to every requester (on st)
 // (self rows first; `after_self` is recorded between the self copy and the
 // remote pushes so the local pool does not wait for the outgoing DMA)
-void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_self) {
+void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_self, const float* send_rows) {
+  if (!send_rows) send_rows = c.own_rows;
   const int W = c.W, Nc = c.Nmax + 2, me = c.rank;
   const size_t row = size_t(c.D) * sizeof(float);
   for (int pass = 0; pass < 2; ++pass) {
@@ -151,8 +182,8 @@ void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_s
     if (cnt > 0 && (pass == 0) == (p == me)) {
       int64_t dst = src_base_at(s, c, p, mb);
       for (int o = 0; o < me; ++o) dst += s.all[(size_t(p) * W + o) * Nc + 1 + mb];
-      NEST_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(c.peer_src[p]) + dst * row,
-                                reinterpret_cast<const char*>(c.own_rows) + so * row, cnt * row,
+      NEST_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(peer_src_of(c, s, p)) + dst * row,
+                                reinterpret_cast<const char*>(send_rows) + so * row, cnt * row,
                                 cudaMemcpyDeviceToDevice, st));
     }
     so += cnt;
@@ -162,7 +193,7 @@ void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_s
   for (int p = 0; p < W; ++p) {
     if (p == me) continue;
     CUresult r = g_write(reinterpret_cast<CUstream>(st),
-                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, 0, mb, me)),
+                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, s, XK_EMB, mb, me)),
                          cuuint32_t(s.epoch), 0);
     NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWriteValue32 failed");
   }
@@ -174,18 +205,19 @@ void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st) {
   for (int p = 0; p < c.W; ++p) {
     if (p == c.rank) continue;
     CUresult r = g_write(reinterpret_cast<CUstream>(st),
-                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, kind, mb, c.rank)),
+                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, s, kind, mb, c.rank)),
                          cuuint32_t(s.epoch), 0);
     NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWriteValue32 failed");
   }
 }
 
 // the requester's stream waits for every owner's rows of micro-batch mb
-void xfer_wait_emb(Ctx& c, Slot& s, int mb, cudaStream_t st) {
+// (kind XK_EMB) or for every owner's re-pushed rows (XK_REPUSH)
+void xfer_wait_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, int kind) {
   for (int o = 0; o < c.W; ++o) {
     if (o == c.rank) continue;
     CUresult r = g_wait(reinterpret_cast<CUstream>(st),
-                        reinterpret_cast<CUdeviceptr>(c.xflags + flag_index(c, 0, mb, o)),
+                        reinterpret_cast<CUdeviceptr>(c.xflags + flag_index(c, s, kind, mb, o)),
                         cuuint32_t(s.epoch), CU_STREAM_WAIT_VALUE_GEQ);
     NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWaitValue32 failed");
   }
@@ -202,7 +234,7 @@ void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st) {
       int64_t dst = own_base_at(s, c, p, mb);
       for (int r = 0; r < me; ++r) dst += s.all[(size_t(r) * W + p) * Nc + 1 + mb];
       NEST_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(c.peer_own[p]) + dst * row,
-                                reinterpret_cast<const char*>(c.src_rows) + so * row, cnt * row,
+                                reinterpret_cast<const char*>(src_rows_of(c, s)) + so * row, cnt * row,
                                 cudaMemcpyDeviceToDevice, st));
     }
     so += cnt;
@@ -210,7 +242,7 @@ void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st) {
   for (int p = 0; p < W; ++p) {
     if (p == me) continue;
     CUresult r = g_write(reinterpret_cast<CUstream>(st),
-                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, 1, mb, me)),
+                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_index(c, s, XK_GRAD, mb, me)),
                          cuuint32_t(s.epoch), 0);
     NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWriteValue32 failed");
   }
@@ -222,7 +254,7 @@ void xfer_wait_grads(Ctx& c, Slot& s, cudaStream_t st) {
     for (int r = 0; r < c.W; ++r) {
       if (r == c.rank) continue;
       CUresult res = g_wait(reinterpret_cast<CUstream>(st),
-                            reinterpret_cast<CUdeviceptr>(c.xflags + flag_index(c, 1, mb, r)),
+                            reinterpret_cast<CUdeviceptr>(c.xflags + flag_index(c, s, XK_GRAD, mb, r)),
                             cuuint32_t(s.epoch), CU_STREAM_WAIT_VALUE_GEQ);
       NEST_CHECK(res == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWaitValue32 failed");
     }

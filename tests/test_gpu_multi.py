@@ -20,12 +20,25 @@ def _port():
     return p
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs >= 2 CUDA devices")
-def test_world2_parity_nccl():
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+def _ndev():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+# transports: fused NVLink stores with the early push (default), fused with
+# the embedding push inside the window, copy engines, NCCL send/recv
+TRANSPORTS = {"fused-early": {}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
+              "fused-window": {"NEST_EARLY_PUSH": "0"}, "ce": {"NEST_A2A": "ce"},
+              "nccl": {"NEST_A2A": "nccl"}}
+
+
+@pytest.mark.parametrize("world,transport", [(2, t) for t in TRANSPORTS] + [(4, "fused-early")])
+def test_multi_rank_parity(world, transport):
+    if _ndev() < world:
+        pytest.skip(f"needs >= {world} CUDA devices")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    env = dict(os.environ, **TRANSPORTS[transport])
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "MGPU ALL OK" in r.stdout
