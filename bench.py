@@ -268,6 +268,14 @@ def main():
     host_b = [(torch.from_numpy(k).pin_memory(), torch.from_numpy(o).pin_memory()) for k, o in batches]
     lr = 1e-3 / (B * world)
 
+    def pooled_dtype(variant):
+        # the bf16 tower takes bf16 pooled rows straight from the pool kernel
+        # (same values as casting the fp32 rows; NEST_BENCH_POOLED_BF16=0: fp32
+        # rows + the tower's cast)
+        if variant == "et" and os.environ.get("NEST_BENCH_POOLED_BF16", "1") != "0":
+            return torch.bfloat16
+        return torch.float32
+
     def make_dout_fn(variant):
         if variant == "et":
             douts = {}
@@ -275,7 +283,7 @@ def main():
             def fn(t, i, pooled):
                 key = (i, pooled.shape[0])
                 if key not in douts:
-                    douts[key] = torch.empty_like(pooled)
+                    douts[key] = torch.empty(pooled.shape, dtype=torch.float32, device=dev)
                 ctx.tower_fwd_bwd(pooled, douts[key], stream=torch.cuda.current_stream())  # dense lane
                 return douts[key]
             return fn
@@ -323,7 +331,7 @@ def main():
             outs = runner.step(dev_b[cur], nb, dout_fn, keep_outputs=True)
             if source == "host":
                 res = outs[-1][0].to("cpu", non_blocking=False)   # the step's result row
-                d2h += res.numel() * 4
+                d2h += res.numel() * res.element_size()
         end.record(runner.join())
         torch.cuda.synchronize()
         ms = start.elapsed_time(end)
@@ -337,7 +345,8 @@ def main():
             ms = float(tt.item())
         return ms, prof, h2d, d2h
 
-    runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr)
+    runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr,
+                    pooled_dtype=pooled_dtype(args.variant))
     timed(runner, args.warmup, 0)
     clocks = Clocks(local)
     clocks.start()
@@ -353,7 +362,8 @@ def main():
     # e2e through the public API with host inputs (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
-        r2 = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr)
+        r2 = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr,
+                    pooled_dtype=pooled_dtype(args.variant))
         r2.t = runner.t
         timed(r2, 2, runner.t, source="host")
         ms_e, _, h2d, d2h = timed(r2, args.steps, r2.t, source="host")
@@ -367,7 +377,7 @@ def main():
     # N = 1 (no FWP) and, when there is an All2All to hide, N = 2 (FWP)
     def tower_run(Nv, t0):
         r1 = Runner(ctx, N=Nv, schedule=args.schedule if Nv > 1 else "sequential", pipelined=True,
-                    lr_over_B=lr)
+                    lr_over_B=lr, pooled_dtype=pooled_dtype("et"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="et")
         k2 = max(5, args.steps // 2)
@@ -385,7 +395,8 @@ def main():
         return out, r1.t
 
     def embedding_run(Nv, t0):
-        r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr)
+        r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr,
+                    pooled_dtype=pooled_dtype("e"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="e")
         ms1, prof1, _, _ = timed(r1, args.steps, r1.t, profile=True, variant="e")

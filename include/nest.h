@@ -205,6 +205,13 @@ NEST_API nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot,
 NEST_API nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out,
                               void* compute, void* comm);
 
+/* nest_lookup_fwd with bf16 output for a bf16 dense consumer: the same fp32
+ * sum per bag, rounded once to bf16 (round to nearest even) when stored, so
+ * out == bf16(nest_lookup_fwd's rows) bit for bit.  out: bf16 (uint16 bit
+ * patterns) [mb_out_rows, d].  Pooling SUM only (else NEST_ERR_INVALID). */
+NEST_API nest_status_t nest_lookup_fwd_bf16(nest_ctx_t* ctx, int32_t slot, int32_t mb, void* out,
+                                            void* compute, void* comm);
+
 /* The communication half of nest_lookup_fwd for micro-batch mb, issued early
  * (FWP stream scheduling: "communication should be launched as
  * early as possible within the frozen window"): owner send gather + embedding
@@ -235,6 +242,14 @@ NEST_API nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32
  * wait for them). */
 NEST_API nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t rows,
                                  float* dout, void* stream);
+
+/* The same tower on bf16 pooled rows (nest_lookup_fwd_bf16), read in place
+ * without the fp32 -> bf16 cast: dout is bit-identical to
+ * nest_tower_fwd_bwd(pooled_fp32) whenever pooled == bf16(pooled_fp32).
+ * `pooled` must stay unmodified until the deferred weight-gradient GEMMs that
+ * read it finish (the next tower call, nest_join or nest_destroy). */
+NEST_API nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pooled, int64_t rows,
+                                               float* dout, void* stream);
 
 /* Make `stream` wait for all work the library queued on its internal streams
  * (the tower's deferred weight-gradient GEMMs).  Host-side enqueue only. */

@@ -125,8 +125,10 @@ class NestContext:
                                                   _stream(comm if comm is not None else compute)))
 
     def lookup_fwd(self, slot: int, mb: int, out, compute=None, comm=None) -> None:
-        self._check(self.lib.nest_lookup_fwd(self.ctx, slot, mb, _ptr(out), _stream(compute),
-                                             _stream(comm if comm is not None else compute)))
+        """Pool micro-batch mb into `out` (fp32, or bf16 -> nest_lookup_fwd_bf16)."""
+        fn = self.lib.nest_lookup_fwd_bf16 if str(out.dtype) == "torch.bfloat16" else self.lib.nest_lookup_fwd
+        self._check(fn(self.ctx, slot, mb, _ptr(out), _stream(compute),
+                       _stream(comm if comm is not None else compute)))
 
     def grad_bwd_update(self, slot: int, mb: int, dout, lr_over_B: float, compute=None, comm=None) -> None:
         self._check(self.lib.nest_grad_bwd_update(self.ctx, slot, mb, _ptr(dout), float(lr_over_B),
@@ -134,8 +136,9 @@ class NestContext:
                                                   _stream(comm if comm is not None else compute)))
 
     def tower_fwd_bwd(self, pooled, dout, stream=None) -> None:
-        self._check(self.lib.nest_tower_fwd_bwd(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout),
-                                                _stream(stream)))
+        """Stand-in tower on fp32 or bf16 pooled rows (-> nest_tower_fwd_bwd_bf16)."""
+        fn = self.lib.nest_tower_fwd_bwd_bf16 if str(pooled.dtype) == "torch.bfloat16" else self.lib.nest_tower_fwd_bwd
+        self._check(fn(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout), _stream(stream)))
 
     def join(self, stream=None) -> None:
         """`stream` waits for the library's internal streams (nest_join)."""

@@ -22,8 +22,8 @@ MAX_MICRO_BATCHES = 8
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
            "nest_create", "nest_destroy", "nest_init_tables", "nest_fwp_schedule", "nest_route",
-           "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_grad_bwd_update",
-           "nest_tower_fwd_bwd", "nest_join",
+           "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_lookup_fwd_bf16",
+           "nest_grad_bwd_update", "nest_tower_fwd_bwd", "nest_tower_fwd_bwd_bf16", "nest_join",
            "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
            "nest_profile_read", "nest_last_error"]
 PROFILE_STAGES = 16
@@ -109,8 +109,10 @@ def load() -> C.CDLL:
         "nest_dbp_refresh": ([vp, i32, i32, vp], i32),
         "nest_lookup_prefetch": ([vp, i32, i32, vp, vp], i32),
         "nest_lookup_fwd": ([vp, i32, i32, vp, vp, vp], i32),
+        "nest_lookup_fwd_bf16": ([vp, i32, i32, vp, vp, vp], i32),
         "nest_grad_bwd_update": ([vp, i32, i32, vp, f32, vp, vp], i32),
         "nest_tower_fwd_bwd": ([vp, vp, i64, vp, vp], i32),
+        "nest_tower_fwd_bwd_bf16": ([vp, vp, i64, vp, vp], i32),
         "nest_join": ([vp, vp], i32),
         "nest_slot_info": ([vp, i32, C.POINTER(SlotInfo)], i32),
         "nest_route_view": ([vp, i32, C.POINTER(RouteView)], i32),

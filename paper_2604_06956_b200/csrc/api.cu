@@ -87,7 +87,7 @@ static size_t layout(Ctx& c, char* base) {
   const int64_t K = c.Kcap, B = c.Bcap, R = c.Rcap, Uo = c.Uocap, D = c.D, W = c.W, Nm = c.Nmax;
   const int Nc = c.Nmax + 2;
   int64_t maxn = std::max<int64_t>({c.words + 2, c.owords + 2, K + 2, R + 2, B + 2,
-                                    int64_t(256) * radix_blocks(K) + 2});
+                                    int64_t(1 << kRadixMaxDigit) * radix_blocks(K) + 2});
   const int64_t scan_bytes = (scan_blocks(maxn) + 4) * int64_t(sizeof(I2));
   c.d_rows = w.take<int64_t>(c.T);
   c.d_seg_base = w.take<int64_t>(W * c.T + 1);
@@ -100,7 +100,7 @@ static size_t layout(Ctx& c, char* base) {
     c.tkey[i] = w.take<uint32_t>(K);
     c.tval[i] = w.take<int32_t>(K);
   }
-  c.hist = w.take<uint32_t>(int64_t(256) * radix_blocks(K) + 2);
+  c.hist = w.take<uint32_t>(int64_t(1 << kRadixMaxDigit) * radix_blocks(K) + 2);
   c.scan_tmp = w.take<char>(scan_bytes);
   c.scan_tmp_win = w.take<char>(scan_bytes);
   c.samp_scratch = w.take<int32_t>(B + 2);
@@ -535,11 +535,11 @@ nest_status_t nest_lookup_prefetch(nest_ctx_t* ctx, int32_t slot, int32_t mb, vo
   });
 }
 
-nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out, void* compute,
-                              void* comm) {
-  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+static nest_status_t lookup_fwd_impl(Ctx* c, int32_t slot, int32_t mb, void* out, bool bf16, void* compute,
+                                     void* comm) {
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] {
+    NEST_CHECK(!bf16 || c->cfg.pooling == NEST_POOL_SUM, NEST_ERR_INVALID, "bf16 output needs pooling = SUM");
     Slot& s = slot_of(*c, slot);
     NEST_CHECK(s.routed, NEST_ERR_ORDER, "lookup before route");
     NEST_CHECK(!s.updated, NEST_ERR_ORDER, "lookup after the window closed (S:568)");
@@ -562,14 +562,24 @@ nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* 
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));
     }
     ProfScope ps(*c, ST_POOL, SK_COMPUTE, cs);
-    launch_pool(*c, s, mb, out, cs);
+    launch_pool(*c, s, mb, out, bf16, cs);
     {
       // U_{s,i} rows + 4 K_i + output rows
       const double row = double(c->D) * sizeof(float);
       ps.bytes = row * double(s.info.mb_uniq[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
-                 row * double(s.info.mb_out_rows[mb]);
+                 (bf16 ? 0.5 : 1.0) * row * double(s.info.mb_out_rows[mb]);
     }
   });
+}
+
+nest_status_t nest_lookup_fwd(nest_ctx_t* ctx, int32_t slot, int32_t mb, float* out, void* compute,
+                              void* comm) {
+  return lookup_fwd_impl(reinterpret_cast<Ctx*>(ctx), slot, mb, out, false, compute, comm);
+}
+
+nest_status_t nest_lookup_fwd_bf16(nest_ctx_t* ctx, int32_t slot, int32_t mb, void* out, void* compute,
+                                   void* comm) {
+  return lookup_fwd_impl(reinterpret_cast<Ctx*>(ctx), slot, mb, out, true, compute, comm);
 }
 
 nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, const float* dout,
@@ -686,17 +696,26 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
   });
 }
 
-nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t rows, float* dout,
-                                 void* stream) {
-  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+static nest_status_t tower_impl(Ctx* c, const void* pooled, bool bf16, int64_t rows, float* dout, void* stream) {
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] {
     NEST_CHECK(c->tower != nullptr, NEST_ERR_INVALID, "tower_layers == 0");
     NEST_CHECK(rows % c->F == 0, NEST_ERR_INVALID, "rows must be a multiple of F");
+    NEST_CHECK(pooled != nullptr && dout != nullptr, NEST_ERR_INVALID, "null pooled / dout");
     ProfScope ps(*c, ST_TOWER, SK_COMPUTE, S(stream));
-    ps.bytes = tower_run(*c, pooled, rows, dout, S(stream));  // FLOPs on this stream
-    ps.launches = 1;  // the cast kernel (the GEMMs are cuBLAS)
+    ps.bytes = tower_run(*c, pooled, bf16, rows, dout, S(stream));  // FLOPs on this stream
+    ps.launches = bf16 ? 0 : 1;  // the cast kernel (the GEMMs are cuBLAS)
   });
+}
+
+nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t rows, float* dout,
+                                 void* stream) {
+  return tower_impl(reinterpret_cast<Ctx*>(ctx), pooled, false, rows, dout, stream);
+}
+
+nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pooled, int64_t rows, float* dout,
+                                      void* stream) {
+  return tower_impl(reinterpret_cast<Ctx*>(ctx), pooled, true, rows, dout, stream);
 }
 
 nest_status_t nest_join(nest_ctx_t* ctx, void* stream) {

@@ -159,7 +159,7 @@ struct Ctx {
   int32_t* occ_mbrow = nullptr;    // [Kcap]
   uint32_t* tkey[2] = {nullptr, nullptr};  // radix ping-pong [Kcap]
   int32_t* tval[2] = {nullptr, nullptr};
-  uint32_t* hist = nullptr;        // [256 * radix blocks + 1]
+  uint32_t* hist = nullptr;        // [2^kRadixMaxDigit * radix blocks + 2]
   void* scan_tmp = nullptr;        // scan block sums, route-side streams (bytes)
   void* scan_tmp_win = nullptr;    // scan block sums, window-side streams
   int32_t* samp_scratch = nullptr; // [Bcap+1] unpooled sample prefix (route)
@@ -264,6 +264,14 @@ __device__ __forceinline__ void st_f4_cs(float* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
                "f"(v.z), "f"(v.w)
                : "memory");
+}
+
+// streaming store of 4 consecutive outputs, fp32 or rounded to bf16 (RN)
+__device__ __forceinline__ void st_out4_cs(float* p, float4 v) { st_f4_cs(p, v); }
+__device__ __forceinline__ void st_out4_cs(__nv_bfloat16* p, float4 v) {
+  const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  const uint32_t lo = *reinterpret_cast<const uint32_t*>(&a), hi = *reinterpret_cast<const uint32_t*>(&b);
+  asm volatile("st.global.cs.v2.b32 [%0], {%1, %2};" ::"l"(p), "r"(lo), "r"(hi) : "memory");
 }
 
 // Row geometry for fp32 rows of D floats processed by groups of L lanes, each
@@ -440,11 +448,13 @@ constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;   // 4096
 constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixMaxDigit = 11;                        // widest digit (2048 bins)
 
 inline int radix_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kRadixTile - 1) / kRadixTile); }
 
 void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                       int32_t* vout, int64_t n, int bits, cudaStream_t st);
+int radix_digit_bits(int bits);
 
 // ----------------------------------------------------------------------------
 // stage launchers (route.cu / rows.cu / schedule.cu / tower.cu)
@@ -456,7 +466,8 @@ void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t
 void launch_init_tables(Ctx& c, cudaStream_t st);
 void launch_gather(Ctx& c, Slot& s, cudaStream_t st);
 void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_rows = nullptr);
-void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st);
+// out: fp32 rows, or bf16 rows (pooled sum only) when bf16
+void launch_pool(Ctx& c, Slot& s, int mb, void* out, bool bf16, cudaStream_t st);
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st);
 void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st);
 void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st);
@@ -521,7 +532,9 @@ void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st);
 void xfer_wait_grads(Ctx& c, Slot& s, cudaStream_t st);
 void tower_create(Ctx& c);
 void tower_destroy(Ctx& c);
-double tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st);
+// pooled: fp32 rows (cast to bf16 inside) or, with pooled_bf16, bf16 rows read
+// in place (they must stay unmodified until the deferred dW GEMMs finish)
+double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, float* dout, cudaStream_t st);
 void tower_join(Ctx& c, cudaStream_t st);
 
 }  // namespace nest

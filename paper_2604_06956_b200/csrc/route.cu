@@ -14,13 +14,17 @@
 namespace nest {
 
 // ---------------------------------------------------------------------------
-// radix sort (stable LSD, 8-bit digits): histogram -> scan -> ranked scatter
+// radix sort (stable LSD, DB = 8..11-bit digits): histogram -> scan -> ranked
+// scatter.  The digit width is chosen per sort so that keys of up to 22 bits
+// (the segment-sum keys of the DLRM batch) take two passes instead of three.
 // ---------------------------------------------------------------------------
+template <int DB>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys,
                                                               int64_t n, int shift,
                                                               uint32_t* __restrict__ hist, int nb) {
-  __shared__ uint32_t cnt[256];
-  cnt[threadIdx.x] = 0;
+  constexpr uint32_t NBIN = 1u << DB;
+  __shared__ uint32_t cnt[NBIN];
+  for (uint32_t d = threadIdx.x; d < NBIN; d += kRadixThreads) cnt[d] = 0;
   __syncthreads();
   const int64_t base = int64_t(blockIdx.x) * kRadixTile;
   const uint32_t lt = lanemask_lt();
@@ -28,33 +32,43 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __
   for (int k = 0; k < kRadixItems; ++k) {
     const int64_t i = base + k * kRadixThreads + threadIdx.x;
     const bool v = i < n;
-    const uint32_t d = v ? (keys[i] >> shift) & 255u : 256u;
+    const uint32_t d = v ? (keys[i] >> shift) & (NBIN - 1) : NBIN;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     if (v && (peers & lt) == 0) atomicAdd(&cnt[d], __popc(peers));
   }
   __syncthreads();
-  hist[int64_t(threadIdx.x) * nb + blockIdx.x] = cnt[threadIdx.x];
+  for (uint32_t d = threadIdx.x; d < NBIN; d += kRadixThreads) hist[int64_t(d) * nb + blockIdx.x] = cnt[d];
 }
 
+template <int DB>
+constexpr size_t radix_scatter_smem() {
+  return sizeof(uint32_t) * (size_t(kRadixWarps + 2) * (1u << DB) + 2 * size_t(kRadixTile));
+}
+
+template <int DB>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
     const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin, int64_t n, int shift,
     const uint32_t* __restrict__ offs, int nb, uint32_t* __restrict__ kout,
     int32_t* __restrict__ vout) {
-  __shared__ uint32_t wcnt[kRadixWarps][256];
-  __shared__ uint32_t dstart[256];
-  __shared__ uint32_t gbase[256];
-  __shared__ uint32_t skeys[kRadixTile];
-  __shared__ int32_t svals[kRadixTile];
+  constexpr uint32_t NBIN = 1u << DB;
+  constexpr int DPT = int(NBIN) / kRadixThreads;   // digits owned per thread in the digit scan
+  static_assert(DPT >= 1, "at least one digit per thread");
+  extern __shared__ uint32_t rsm[];
+  uint32_t* wcnt = rsm;                            // [kRadixWarps][NBIN]
+  uint32_t* dstart = wcnt + kRadixWarps * NBIN;    // [NBIN]
+  uint32_t* gbase = dstart + NBIN;                 // [NBIN]
+  uint32_t* skeys = gbase + NBIN;                  // [kRadixTile]
+  int32_t* svals = reinterpret_cast<int32_t*>(skeys + kRadixTile);
   __shared__ uint32_t wsum[kRadixWarps];
   const int warp = threadIdx.x >> 5, lane = lane_id();
-#pragma unroll
-  for (int w = 0; w < kRadixWarps; ++w) wcnt[w][threadIdx.x] = 0;
-  gbase[threadIdx.x] = offs[int64_t(threadIdx.x) * nb + blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < kRadixWarps * NBIN; i += kRadixThreads) wcnt[i] = 0;
+  for (uint32_t d = threadIdx.x; d < NBIN; d += kRadixThreads) gbase[d] = offs[int64_t(d) * nb + blockIdx.x];
   __syncthreads();
   // warp w owns the contiguous items [w*512, w*512+512) of the tile, visited
   // in rounds of 32: (warp, round, lane) order == input order -> stable
   const int64_t base = int64_t(blockIdx.x) * kRadixTile + warp * (32 * kRadixItems);
   const uint32_t lt = lanemask_lt();
+  uint32_t* wc = wcnt + warp * NBIN;
   uint32_t key[kRadixItems];
   int32_t val[kRadixItems];
   uint32_t lr[kRadixItems];
@@ -68,25 +82,34 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
 #pragma unroll
   for (int k = 0; k < kRadixItems; ++k) {
     const bool v = base + k * 32 + lane < n;
-    const uint32_t d = v ? (key[k] >> shift) & 255u : 256u;
+    const uint32_t d = v ? (key[k] >> shift) & (NBIN - 1) : NBIN;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = v ? wcnt[warp][d] : 0u;
+    const uint32_t before = v ? wc[d] : 0u;
     __syncwarp();
-    if (v && (peers & lt) == 0) wcnt[warp][d] = before + __popc(peers);
+    if (v && (peers & lt) == 0) wc[d] = before + __popc(peers);
     __syncwarp();
     lr[k] = before + __popc(peers & lt);
   }
   __syncthreads();
   {
-    const int d = threadIdx.x;
-    uint32_t run = 0;
+    // thread t owns digits [t*DPT, t*DPT + DPT): per digit an exclusive prefix
+    // over the warps, then a block-wide exclusive scan of the digit totals
+    uint32_t tot[DPT];
+    uint32_t mine = 0;
 #pragma unroll
-    for (int w = 0; w < kRadixWarps; ++w) {
-      const uint32_t cc = wcnt[w][d];
-      wcnt[w][d] = run;
-      run += cc;
+    for (int j = 0; j < DPT; ++j) {
+      const uint32_t d = threadIdx.x * DPT + j;
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < kRadixWarps; ++w) {
+        const uint32_t cc = wcnt[w * NBIN + d];
+        wcnt[w * NBIN + d] = run;
+        run += cc;
+      }
+      tot[j] = run;
+      mine += run;
     }
-    const uint32_t inc = warp_incl_scan(run);
+    const uint32_t inc = warp_incl_scan(mine);
     if (lane == 31) wsum[warp] = inc;
     __syncthreads();
     if (warp == 0) {
@@ -95,14 +118,19 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
       if (lane < kRadixWarps) wsum[lane] = xi - x;
     }
     __syncthreads();
-    dstart[d] = wsum[warp] + inc - run;
+    uint32_t start = wsum[warp] + inc - mine;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      dstart[threadIdx.x * DPT + j] = start;
+      start += tot[j];
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kRadixItems; ++k) {
     if (base + k * 32 + lane < n) {
-      const uint32_t d = (key[k] >> shift) & 255u;
-      const uint32_t s = dstart[d] + wcnt[warp][d] + lr[k];
+      const uint32_t d = (key[k] >> shift) & (NBIN - 1);
+      const uint32_t s = dstart[d] + wcnt[warp * NBIN + d] + lr[k];
       skeys[s] = key[k];
       svals[s] = val[k];
     }
@@ -112,17 +140,43 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
   const int nvalid = n - tb < kRadixTile ? int(n - tb) : kRadixTile;
   for (int s = threadIdx.x; s < nvalid; s += kRadixThreads) {
     const uint32_t k2 = skeys[s];
-    const uint32_t d = (k2 >> shift) & 255u;
+    const uint32_t d = (k2 >> shift) & (NBIN - 1);
     const uint32_t p = gbase[d] + (uint32_t(s) - dstart[d]);
     kout[p] = k2;
     vout[p] = svals[s];
   }
 }
 
+template <int DB>
+static void radix_pass(Ctx& c, const uint32_t* sk, const int32_t* sv, uint32_t* dk, int32_t* dv, int64_t n,
+                       int shift, int nb, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    NEST_CUDA(cudaFuncSetAttribute(k_radix_scatter<DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(radix_scatter_smem<DB>())));
+    attr = true;
+  }
+  k_radix_hist<DB><<<nb, kRadixThreads, 0, st>>>(sk, n, shift, c.hist, nb);
+  uint32_t* h = c.hist;
+  scan_exclusive<uint32_t>([=] __device__(int64_t i) { return h[i]; }, int64_t(1u << DB) * nb,
+                           [=] __device__(int64_t i, uint32_t v) { h[i] = v; }, c.scan_tmp, st);
+  k_radix_scatter<DB><<<nb, kRadixThreads, radix_scatter_smem<DB>(), st>>>(sk, sv, n, shift, c.hist, nb, dk, dv);
+  NEST_LAUNCH_CHECK();
+}
+
+// digit width of a sort of `bits`-bit keys: the fewest passes of <= 11 bits
+int radix_digit_bits(int bits) {
+  if (bits <= 8) return 8;
+  const int passes = (bits + kRadixMaxDigit - 1) / kRadixMaxDigit;
+  const int db = (bits + passes - 1) / passes;
+  return db < 8 ? 8 : db;
+}
+
 void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                       int32_t* vout, int64_t n, int bits, cudaStream_t st) {
   if (n <= 0) return;
-  const int passes = bits <= 8 ? 1 : (bits + 7) / 8;
+  const int db = radix_digit_bits(bits);
+  const int passes = bits <= db ? 1 : (bits + db - 1) / db;
   const int nb = radix_blocks(n);
   const uint32_t* sk = kin;
   const int32_t* sv = vin;
@@ -137,12 +191,12 @@ void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t*
       dk = c.tkey[t];
       dv = c.tval[t];
     }
-    k_radix_hist<<<nb, kRadixThreads, 0, st>>>(sk, n, 8 * p, c.hist, nb);
-    uint32_t* h = c.hist;
-    scan_exclusive<uint32_t>([=] __device__(int64_t i) { return h[i]; }, int64_t(256) * nb,
-                             [=] __device__(int64_t i, uint32_t v) { h[i] = v; }, c.scan_tmp, st);
-    k_radix_scatter<<<nb, kRadixThreads, 0, st>>>(sk, sv, n, 8 * p, c.hist, nb, dk, dv);
-    NEST_LAUNCH_CHECK();
+    switch (db) {
+      case 8: radix_pass<8>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
+      case 9: radix_pass<9>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
+      case 10: radix_pass<10>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
+      default: radix_pass<11>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
+    }
     sk = dk;
     sv = dv;
   }

@@ -165,14 +165,14 @@ void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_row
 // ---------------------------------------------------------------------------
 // IL bags per lane group at once (bags q, q + ng, ...), two rows of each in
 // flight per pass, each bag summed left to right
-template <int D, bool W1, int IL>
+template <int D, bool W1, int IL, typename OutT>
 __global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_pool(int64_t nrows, int F,
                                                       const int32_t* __restrict__ perm_mb,
                                                       const int32_t* __restrict__ bag_off,
                                                       const int32_t* __restrict__ inverse,
                                                       const int32_t* __restrict__ pos,
                                                       const float* __restrict__ src,
-                                                      float* __restrict__ out) {
+                                                      OutT* __restrict__ out) {
   Grp<D> gp;
   constexpr int VPL = RowGeom<D>::VPL;
   for (int64_t q0 = gp.g; q0 < nrows; q0 += IL * gp.ng) {
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_pool(int
       const int64_t q = q0 + i * gp.ng;
       if (q < nrows)
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) st_f4_cs(out + q * D + gp.col(v), acc[i][v]);
+        for (int v = 0; v < VPL; ++v) st_out4_cs(out + q * D + gp.col(v), acc[i][v]);
     }
   }
 }
@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(int nsamp, int F,
   }
 }
 
-void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
+void launch_pool(Ctx& c, Slot& s, int mb, void* out_v, bool bf16, cudaStream_t st) {
+  float* out = reinterpret_cast<float*>(out_v);
+  __nv_bfloat16* out_h = reinterpret_cast<__nv_bfloat16*>(out_v);
   const bool w1 = c.W == 1;
   const float* src = w1 ? s.buffer : src_rows_of(c, s) + s.src_base[mb] * c.D;
   const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
@@ -267,14 +269,24 @@ void launch_pool(Ctx& c, Slot& s, int mb, float* out, cudaStream_t st) {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
     if (c.cfg.pooling == NEST_POOL_SUM) {
       const int64_t nrows = int64_t(s.cap) * c.F;
-      NEST_DISPATCH_ILP({
+      const int grid = emb_blocks(nrows, rpb);
+      if (bf16) {
         if (w1)
-          k_pool<D, true, IL><<<emb_blocks((nrows + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
-              nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+          k_pool<D, true, 1><<<grid, kRowThreads, 0, st>>>(nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src,
+                                                            out_h);
         else
-          k_pool<D, false, IL><<<emb_blocks((nrows + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
-              nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
-      });
+          k_pool<D, false, 1><<<grid, kRowThreads, 0, st>>>(nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src,
+                                                             out_h);
+      } else {
+        NEST_DISPATCH_ILP({
+          if (w1)
+            k_pool<D, true, IL><<<emb_blocks((nrows + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
+                nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+          else
+            k_pool<D, false, IL><<<emb_blocks((nrows + IL - 1) / IL, rpb), kRowThreads, 0, st>>>(
+                nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+        });
+      }
     } else {
       if (w1)
         k_expand_rows<D, true><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(

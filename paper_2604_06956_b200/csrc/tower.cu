@@ -245,21 +245,26 @@ static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void*
                              t->ws_bytes, st));
 }
 
-double tower_run(Ctx& c, const float* pooled, int64_t rows, float* dout, cudaStream_t st) {
+double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, float* dout, cudaStream_t st) {
   Tower* t = reinterpret_cast<Tower*>(c.tower);
   const int64_t bm = rows / c.F;
   if (bm == 0) return 0.0;
   NEST_CHECK(bm <= t->bmax, NEST_ERR_CAPACITY, "tower batch exceeds max_batch");
   const int L = t->L, H = t->H, in0 = t->in0, M = int(bm);
-  auto X = [&](int l) { return t->x + t->xoff[l]; };                     // input of layer l
+  // input of layer l (X_0: the caller's bf16 rows in place, or the cast copy)
+  __nv_bfloat16* x0 = pooled_bf16 ? const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(pooled))
+                                  : t->x;
+  auto X = [&](int l) { return l == 0 ? x0 : t->x + t->xoff[l]; };
   auto W = [&](int l) { return t->w + t->woff[l]; };
   auto DY = [&](int l) { return l == L - 1 ? t->gtop : t->dy + int64_t(l) * t->bmax * H; };
   auto IN = [&](int l) { return l == 0 ? in0 : H; };
   // the previous call's dW GEMMs still read X and dY
   if (t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
   t->dw_pending = false;
-  k_cast_bf16<<<148 * 8, 256, 0, st>>>(pooled, t->x, bm * in0 / 4);
-  NEST_LAUNCH_CHECK();
+  if (!pooled_bf16) {
+    k_cast_bf16<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const float*>(pooled), t->x, bm * in0 / 4);
+    NEST_LAUNCH_CHECK();
+  }
   // forward: X_{l+1} = X_l W_l^T (the last layer's output is not needed:
   // its gradient is the fixed gtop); the scratch dY_0 takes it
   for (int l = 0; l < L; ++l)

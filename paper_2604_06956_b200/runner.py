@@ -62,9 +62,12 @@ class Runner:
     gradient)."""
 
     def __init__(self, ctx: NestContext, N: int = 1, schedule: str = "sequential",
-                 pipelined: bool = True, lr_over_B: float = 2.0 ** -10):
+                 pipelined: bool = True, lr_over_B: float = 2.0 ** -10, pooled_dtype=None):
         self.ctx, self.N, self.schedule, self.pipelined = ctx, N, schedule, pipelined
         self.lr = lr_over_B
+        # bf16: pooled rows for a bf16 dense consumer (nest_lookup_fwd_bf16)
+        self.pooled_dtype = pooled_dtype or torch.float32
+        self._hold: List[torch.Tensor] = []
         dev = ctx.device
         import os
         # block-scheduling priorities (lower = scheduled first as SMs free up):
@@ -110,7 +113,7 @@ class Runner:
         with torch.cuda.stream(self.compute):   # allocation stream = producing stream
             for i in range(self.N):
                 rows = int(info.mb_out_rows[i])
-                outs.append(torch.empty((rows, self.ctx.dim), dtype=torch.float32,
+                outs.append(torch.empty((rows, self.ctx.dim), dtype=self.pooled_dtype,
                                         device=self.ctx.device))
         return outs
 
@@ -129,6 +132,10 @@ class Runner:
             self.primed = True
         outs = self.out_buffers(a)
         self.outs = outs if keep_outputs else []
+        # a dense consumer may read the pooled rows after this call returns
+        # (the tower's deferred dW GEMMs): keep them allocated until the next
+        # step has enqueued its own tower calls, which wait for those GEMMs
+        prev, self._hold = self._hold, outs
         if self.lanes == 2:
             return self._step_two_lanes(a, p, outs, next_batch, dout_fn)
         # embedding lane: pool_0, pool_1, seg_0, pool_2, seg_1, ... (pool of

@@ -98,6 +98,36 @@ def test_route_mid_size_radix_tiles_and_ragged_tail():
     assert np.array_equal(v["pos"].astype(np.int64), rs.pos)
 
 
+# --------------------------------------------------------------------------- bf16 hand-off
+def test_lookup_bf16_and_tower_bf16_input_match_fp32_path():
+    """nest_lookup_fwd_bf16 == bf16(RN) of nest_lookup_fwd bit for bit, and the
+    tower's input gradient from the bf16 rows == the one from the fp32 rows
+    (cast inside) bit for bit; the fp32 rows meet the oracle's P2 bar."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(5000, 3000, 200, 77), zipf=1.3, bag_repeats=True, dim=64)
+    B = 512
+    keys, offs = WL.gen_batch(cfg, 9, 0, 0, batch=B)
+    ctx = make_ctx(cfg, B, K=len(keys), init="uniform", seed=4, tower_layers=2, tower_hidden=64)
+    ctx.route(0, to_dev(keys, torch.int64), to_dev(offs, torch.int32), B)
+    rows = B * cfg.num_features
+    out32 = torch.empty((rows, cfg.dim), dtype=torch.float32, device=DEV)
+    out16 = torch.empty((rows, cfg.dim), dtype=torch.bfloat16, device=DEV)
+    ctx.lookup_fwd(0, 0, out32)
+    ctx.lookup_fwd(0, 0, out16)
+    torch.cuda.synchronize()
+    assert torch.equal(out16.view(torch.int16), out32.to(torch.bfloat16).view(torch.int16))
+    tab = OS.LazyTable(4, cfg.dim, "uniform")
+    ref = OS.forward(tab, keys, offs, pooling="sum")
+    assert rel_rowwise_ok(out32.cpu().numpy(), ref)
+    d32 = torch.empty((rows, cfg.dim), dtype=torch.float32, device=DEV)
+    d16 = torch.empty_like(d32)
+    ctx.tower_fwd_bwd(out32, d32)
+    ctx.tower_fwd_bwd(out16, d16)
+    ctx.join()
+    torch.cuda.synchronize()
+    assert torch.isfinite(d32).all() and d32.abs().sum() > 0
+    assert torch.equal(d32, d16)
+
+
 # --------------------------------------------------------------------------- full steps
 def _run_w1(cfg, B, N, T, init, dmode, lr, pipelined, seed=3, grad_mode="lin"):
     F, d = cfg.num_features, cfg.dim
