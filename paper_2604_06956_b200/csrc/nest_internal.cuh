@@ -448,7 +448,10 @@ constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;   // 4096
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixMaxDigit = 11;                        // widest digit (2048 bins)
+// widest digit: 8 bits.  11-bit digits (2 passes for 22-bit keys) measured
+// slower on B200: scatter 81 vs 38 us, histogram 34 vs 23 us per pass at
+// 3.4M pairs (2 blocks/SM and strided per-block offset reads at 2048 bins)
+constexpr int kRadixMaxDigit = 8;
 
 inline int radix_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kRadixTile - 1) / kRadixTile); }
 

@@ -14,9 +14,8 @@
 namespace nest {
 
 // ---------------------------------------------------------------------------
-// radix sort (stable LSD, DB = 8..11-bit digits): histogram -> scan -> ranked
-// scatter.  The digit width is chosen per sort so that keys of up to 22 bits
-// (the segment-sum keys of the DLRM batch) take two passes instead of three.
+// radix sort (stable LSD, digits of DB <= kRadixMaxDigit bits): histogram ->
+// scan -> ranked scatter.
 // ---------------------------------------------------------------------------
 template <int DB>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys,
@@ -164,7 +163,7 @@ static void radix_pass(Ctx& c, const uint32_t* sk, const int32_t* sv, uint32_t* 
   NEST_LAUNCH_CHECK();
 }
 
-// digit width of a sort of `bits`-bit keys: the fewest passes of <= 11 bits
+// digit width of a sort of `bits`-bit keys: the fewest passes of <= kRadixMaxDigit bits
 int radix_digit_bits(int bits) {
   if (bits <= 8) return 8;
   const int passes = (bits + kRadixMaxDigit - 1) / kRadixMaxDigit;
@@ -191,12 +190,8 @@ void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t*
       dk = c.tkey[t];
       dv = c.tval[t];
     }
-    switch (db) {
-      case 8: radix_pass<8>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
-      case 9: radix_pass<9>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
-      case 10: radix_pass<10>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
-      default: radix_pass<11>(c, sk, sv, dk, dv, n, db * p, nb, st); break;
-    }
+    static_assert(kRadixMaxDigit == 8, "instantiate radix_pass for the wider digits");
+    radix_pass<8>(c, sk, sv, dk, dv, n, db * p, nb, st);
     sk = dk;
     sv = dv;
   }
@@ -265,7 +260,6 @@ __global__ void k_mark(const int64_t* __restrict__ keys, int64_t nnz, int T, int
                        uint32_t* __restrict__ occ_dom, uint32_t* __restrict__ bm,
                        int32_t* __restrict__ err) {
   const int lane = lane_id();
-  const uint32_t lt = lanemask_lt();
   const int64_t nth = int64_t(gridDim.x) * blockDim.x;
   for (int64_t j0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x - lane; j0 < nnz; j0 += nth) {
     const int64_t j = j0 + lane;
@@ -281,15 +275,16 @@ __global__ void k_mark(const int64_t* __restrict__ keys, int64_t nnz, int T, int
         atomicOr(err, kErrKeyRange);
       }
       occ_dom[j] = dom;
+      // test before the atomic: Zipf-hot keys find their bit already set
+      const uint32_t bit = 1u << (dom & 31u);
+      if (dom != 0xffffffffu && !(bm[dom >> 5] & bit)) atomicOr(&bm[dom >> 5], bit);
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, dom);
-    if (dom != 0xffffffffu && (peers & lt) == 0) atomicOr(&bm[dom >> 5], 1u << (dom & 31u));
   }
 }
 
 // per bitmap word: emit the set bits in ascending order
 __global__ void k_emit(int64_t words, const uint32_t* __restrict__ bm, const int32_t* __restrict__ wr,
-                       int T, int W, int nseg, const int64_t* __restrict__ seg_base,
+                       int T, int W, int nseg, uint32_t mask0, const int64_t* __restrict__ seg_base,
                        int64_t* __restrict__ uniq, uint32_t* __restrict__ mask,
                        int32_t* __restrict__ owner_rows) {
   for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < words;
@@ -310,7 +305,7 @@ __global__ void k_emit(int64_t words, const uint32_t* __restrict__ bm, const int
       const int o = lo / T, t = lo - o * T;
       const int64_t row = (dom - __ldg(seg_base + lo)) * W + o;
       uniq[r] = (int64_t(t) << kRowBits) | row;
-      mask[r] = 0u;
+      mask[r] = mask0;
       if (owner_rows) owner_rows[r] = int32_t(dom);
       ++r;
     }
@@ -326,6 +321,8 @@ __global__ void k_owner_offsets(int W, int T, const int64_t* __restrict__ seg_ba
 }
 
 // per occurrence: inverse, micro-batch mask, sort key/value
+// (one micro-batch: every key's mask is bit 0, written by k_emit; no OR pass)
+template <bool kOneMb>
 __global__ void k_inverse(int64_t nnz, const uint32_t* __restrict__ occ_dom,
                           const int32_t* __restrict__ occ_mbrow, const uint32_t* __restrict__ bm,
                           const int32_t* __restrict__ wr, int ubits, int32_t* __restrict__ inverse,
@@ -350,6 +347,7 @@ __global__ void k_inverse(int64_t nnz, const uint32_t* __restrict__ occ_dom,
       skey[j] = (mb << ubits) | uu;
       sval[j] = mr & int32_t(kRowFieldMask);
     }
+    if (kOneMb) continue;
     const uint32_t peers = __match_any_sync(0xffffffffu, u);
     const uint32_t bits = __reduce_or_sync(peers, bit);
     if (u != 0xffffffffu && (peers & lt) == 0) atomicOr(&mask[u], bits);
@@ -531,12 +529,17 @@ void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offs
                                              c.d_err);
   NEST_LAUNCH_CHECK();
   popc_scan(c, bm, wr, c.words + 1, nullptr, st);
-  k_emit<<<grid_for(c.words, 256), 256, 0, st>>>(c.words, bm, wr, c.T, W, W * c.T, c.d_seg_base,
+  k_emit<<<grid_for(c.words, 256), 256, 0, st>>>(c.words, bm, wr, c.T, W, W * c.T, N == 1 ? 1u : 0u,
+                                                 c.d_seg_base,
                                                  s.uniq, s.mask, W == 1 ? s.owner_rows : nullptr);
   k_owner_offsets<<<1, 128, 0, st>>>(W, c.T, c.d_seg_base, bm, wr, s.off);
   s.ubits = bits_for(c.Kcap);
-  k_inverse<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, c.occ_dom, c.occ_mbrow, bm, wr, s.ubits, s.inverse,
-                                                s.mask, c.tkey[0], c.tval[0]);
+  if (N == 1)
+    k_inverse<true><<<grid_for(nnz, 256), 256, 0, st>>>(nnz, c.occ_dom, c.occ_mbrow, bm, wr, s.ubits, s.inverse,
+                                                        s.mask, c.tkey[0], c.tval[0]);
+  else
+    k_inverse<false><<<grid_for(nnz, 256), 256, 0, st>>>(nnz, c.occ_dom, c.occ_mbrow, bm, wr, s.ubits, s.inverse,
+                                                         s.mask, c.tkey[0], c.tval[0]);
   k_mb_counts<<<grid_for(c.Kcap, 256, 148 * 4), 256, 0, st>>>(s.off, W, N, s.mask, c.d_cnt_scratch);
   k_finalize_counts<<<1, 64, 0, st>>>(W, N, Nc, s.off, c.d_cnt_scratch, c.d_err,
                                       xfer + int64_t(c.rank) * W * Nc);
