@@ -331,13 +331,14 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       NEST_CUDA(cudaMemsetAsync(s.n_owner, 0, sizeof(int32_t), st0));
       NEST_CUDA(cudaMemsetAsync(s.off, 0, sizeof(int32_t) * (c->W + 1), st0));
       cudaEvent_t* evs[] = {&s.ev_gather, &s.ev_update, &s.ev_free, &s.ev_ready, &s.ev_sync, &s.ev_early,
-                            &s.ev_repush};
+                            &s.ev_repush, &s.ev_sorted};
       for (auto* e : evs) NEST_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
       for (int i = 0; i < NEST_MAX_MICRO_BATCHES; ++i) {
         NEST_CUDA(cudaEventCreateWithFlags(&s.ev_emb[i], cudaEventDisableTiming));
         NEST_CUDA(cudaEventCreateWithFlags(&s.ev_grad[i], cudaEventDisableTiming));
       }
     }
+    NEST_CUDA(cudaEventCreateWithFlags(&c->ev_scratch, cudaEventDisableTiming));
     NEST_CUDA(cudaStreamSynchronize(st0));
     if (c->W > 1) {
       NEST_CHECK(nccl_uids != nullptr, NEST_ERR_INVALID, "world > 1 needs NCCL unique ids");
@@ -373,9 +374,11 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   xfer_destroy(*c);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
+  if (c->ev_scratch) cudaEventDestroy(c->ev_scratch);
   for (auto& s : c->slot) {
     if (s.h_xfer) cudaFreeHost(s.h_xfer);
-    cudaEvent_t evs[] = {s.ev_gather, s.ev_update, s.ev_free, s.ev_ready, s.ev_sync, s.ev_early, s.ev_repush};
+    cudaEvent_t evs[] = {s.ev_gather, s.ev_update, s.ev_free, s.ev_ready, s.ev_sync, s.ev_early, s.ev_repush,
+                         s.ev_sorted};
     for (auto e : evs)
       if (e) cudaEventDestroy(e);
     for (int i = 0; i < NEST_MAX_MICRO_BATCHES; ++i) {
@@ -409,8 +412,12 @@ nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int3
     NEST_CHECK(nnz >= 0 && nnz <= c->Kcap, NEST_ERR_CAPACITY, "nnz exceeds max_keys");
     NEST_CHECK(mode == NEST_SCHED_SEQUENTIAL || N == 1 || c->cl_u != nullptr, NEST_ERR_INVALID,
                "clustered schedule needs max_micro_batches > 1");
-    ProfScope ps(*c, ST_SCHEDULE, SK_AUX, S(stream));
-    launch_schedule(*c, keys, bag_offsets, nnz, B, N, mode, perm_out, mb_offsets_out, S(stream));
+    NEST_CUDA(cudaStreamWaitEvent(S(stream), c->ev_scratch, 0));
+    {
+      ProfScope ps(*c, ST_SCHEDULE, SK_AUX, S(stream));
+      launch_schedule(*c, keys, bag_offsets, nnz, B, N, mode, perm_out, mb_offsets_out, S(stream));
+    }
+    NEST_CUDA(cudaEventRecord(c->ev_scratch, S(stream)));
   });
 }
 
@@ -434,6 +441,7 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
     // its write-back done before this gather reads the shard (reading Q8)
     NEST_CUDA(cudaStreamWaitEvent(st, s.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, s.ev_free, 0));
+    NEST_CUDA(cudaStreamWaitEvent(st, c->ev_scratch, 0));
     int pid = prof_begin(*c, ST_ROUTE, SK_AUX, st);
     route_phase_a(*c, s, keys, bag_offsets, nnz, B, perm, N, st);
     prof_end(*c, pid, st, 0.0, nullptr, 0.0, c->cfg.pooling == NEST_POOL_SUM ? 12 : 15);
@@ -477,6 +485,9 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
       s.early = true;
       s.prefetched = (1u << N) - 1u;
     }
+    route_sort(*c, s, st);   // needed from this batch's backward on
+    NEST_CUDA(cudaEventRecord(s.ev_sorted, st));
+    NEST_CUDA(cudaEventRecord(c->ev_scratch, st));
   });
 }
 
@@ -594,6 +605,7 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
     cudaStream_t cs = S(compute), ms = S(comm);
     Slot& other = c->slot[1 - slot];
     const double row = double(c->D) * sizeof(float);
+    if (mb == 0) NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
     if (c->W == 1 && s.N == 1) {
       // one rank, one micro-batch: the segment-sum applies Eq. 2 itself
       NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));

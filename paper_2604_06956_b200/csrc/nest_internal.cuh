@@ -101,6 +101,7 @@ struct Slot {
   // the rows the previous window updated (`repushed`)
   bool early = false, repushed = false;
   cudaEvent_t ev_early = nullptr, ev_repush = nullptr;
+  cudaEvent_t ev_sorted = nullptr;  // occurrences sorted (the segment-sum's input)
   cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
               ev_grad[NEST_MAX_MICRO_BATCHES] = {}, ev_ready = nullptr, ev_sync = nullptr;
 };
@@ -190,6 +191,10 @@ struct Ctx {
   int64_t* cl_small = nullptr;     // [4]
   Slot slot[2];
   uint32_t epoch = 0;
+  // last use of the shared routing scratch (tkey/tval, hist, scan_tmp, occ_*,
+  // clustering): every nest_route / nest_fwp_schedule waits for it and
+  // records it, whatever stream the caller uses
+  cudaEvent_t ev_scratch = nullptr;
   int seg_chunk = 32;              // segment-sum: cold threshold = hot chunk length (>= 32)
   // copy-engine / fused All2All transports (xfer.cu)
   bool xfer_ce = false;            // peer windows mapped (CE or fused mode)
@@ -465,6 +470,7 @@ int radix_digit_bits(int bits);
 void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz,
                    int B, const int32_t* perm, int N, cudaStream_t st);
 void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
+void route_sort(Ctx& c, Slot& s, cudaStream_t st);
 void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p);
 void launch_init_tables(Ctx& c, cudaStream_t st);
 void launch_gather(Ctx& c, Slot& s, cudaStream_t st);

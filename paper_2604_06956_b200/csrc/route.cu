@@ -638,9 +638,8 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
   s.key_soff.assign(plan.key_send_off, plan.key_send_off + W + 1);
   s.key_roff.assign(plan.key_recv_off, plan.key_recv_off + W + 1);
 
-  // ---- R1 tail: per micro-batch positions among its keys, sorted occurrences ----
-  int mbbits = 0;
-  while ((1 << mbbits) < N) ++mbbits;
+  // ---- R1 tail: per micro-batch positions among its keys (the pool needs
+  // them); the occurrence sort follows the row traffic (route_sort) ----
   {
     ProfScope ps(c, ST_SORT, SK_AUX, st);
     for (int i = 0; i < N; ++i) {
@@ -649,11 +648,8 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
       scan_exclusive<int32_t>([=] __device__(int64_t u) { return int32_t((mk[u] >> i) & 1u); }, U,
                               [=] __device__(int64_t u, int32_t v) { pos[u] = v; }, c.scan_tmp, st);
     }
-    radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, s.ubits + mbbits, st);
-    const int passes = (s.ubits + mbbits) <= 8 ? 1 : (s.ubits + mbbits + 7) / 8;
-    ps.launches = 3 * N + (nnz > 0 ? 5 * passes : 0);
-    // pos scans read masks + write N positions; every pass reads + writes (key, value)
-    ps.bytes = double(U) * 4 * (1 + N) + double(nnz) * 16 * passes;
+    ps.launches = 3 * N;
+    ps.bytes = double(U) * 4 * (1 + N);   // masks read + N positions written
   }
 
   if (W == 1) {
@@ -712,6 +708,21 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     ps.bpc = 2.0 * c.D * sizeof(float);  // 2 U_o row
   }
   (void)D;
+}
+
+// R1 tail: occurrences sorted by (micro-batch, key) -- the grouping of the
+// deterministic segment-sum, first needed by the backward of this batch, so
+// it runs after everything the next window's forward waits for
+void route_sort(Ctx& c, Slot& s, cudaStream_t st) {
+  int mbbits = 0;
+  while ((1 << mbbits) < s.N) ++mbbits;
+  const int64_t nnz = s.info.nnz;
+  ProfScope ps(c, ST_SORT, SK_AUX, st);
+  radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, s.ubits + mbbits, st);
+  const int bits = s.ubits + mbbits, db = radix_digit_bits(bits);
+  const int passes = bits <= db ? 1 : (bits + db - 1) / db;
+  ps.launches = nnz > 0 ? 5 * passes : 0;
+  ps.bytes = double(nnz) * 16 * passes;   // every pass reads + writes (key, value)
 }
 
 }  // namespace nest
