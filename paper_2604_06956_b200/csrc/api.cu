@@ -622,7 +622,7 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
       s.updated = true;
       return;
     }
-    const bool fused = c->a2a_mode == A2A_FUSED;
+    const bool fused = c->a2a_mode == A2A_FUSED && !c->grad_ce;
     {
       ProfScope ps(*c, fused ? ST_GRAD_A2A : ST_SEGSUM, SK_COMPUTE, cs);
       if (fused) {

@@ -204,6 +204,7 @@ struct Ctx {
   uint32_t* xflags = nullptr;      // [2 slots][3 kinds][Nmax][W] epoch flags written by peers
   int early_push = 0;              // EarlyPush: embedding rows pushed at route time (fused transport)
   float* send_stage = nullptr;     // [OMBcap][d] early push send rows (copy-engine early push)
+  bool grad_ce = false;            // fused transport, gradients by copy engine (NEST_GRAD_PUSH=ce)
   int64_t src_slot_stride = 0;     // floats between the two slots' receive windows (0: shared)
   std::vector<void*> peer_win;
   std::vector<float*> peer_src, peer_own;

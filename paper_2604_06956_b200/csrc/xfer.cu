@@ -76,6 +76,12 @@ void xfer_setup(Ctx& c, cudaStream_t st) {
   load_driver_ops();
   c.a2a_mode = a2a_mode_wanted(c.W);
   c.early_push = c.a2a_mode == A2A_FUSED ? early_push_wanted() : EP_OFF;
+  {
+    // gradients under the fused transport: segment-sum stores into the
+    // owners' windows (sm, default) or local rows + copy-engine DMA (ce)
+    const char* g = std::getenv("NEST_GRAD_PUSH");
+    c.grad_ce = c.a2a_mode == A2A_FUSED && g && std::strcmp(g, "ce") == 0;
+  }
   if (c.early_push == EP_CE)
     NEST_CUDA(cudaMalloc(&c.send_stage, std::max<size_t>(size_t(c.OMBcap) * c.D * sizeof(float), 256)));
   const size_t src1 = align_up(size_t(c.MBcap) * c.D * sizeof(float), 4096);
