@@ -28,11 +28,31 @@ def rel_ok(a, b, tol=1e-5):
     return np.all(np.linalg.norm(a - b, axis=1) <= tol * np.maximum(np.linalg.norm(b, axis=1), 1e-30))
 
 
-def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids):
+def skewed_batches(cfg, B, T, world, seed=31):
+    """Edge case: every key owned by rank 0 (rows multiples of W), and the last
+    rank's batch empty (all bags empty) on odd steps."""
+    out = []
+    for t in range(T):
+        per = []
+        for r in range(world):
+            keys, offs = WL.gen_batch(cfg, seed, t, r, batch=B)
+            if r == world - 1 and t % 2 == 1:
+                keys, offs = keys[:0], np.zeros_like(offs)
+            else:
+                tab, row = WL.unpack_keys(keys)
+                row = (row // world) * world
+                keys = WL.pack_keys(tab, row)
+            per.append((keys, offs))
+        out.append(per)
+    return out
+
+
+def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=None):
     F, d = cfg.num_features, cfg.dim
-    batches = [[WL.gen_batch(cfg, 21, t, r, batch=B) for r in range(world)] for t in range(T)]
+    batches = gen(cfg, B, T, world) if gen else \
+        [[WL.gen_batch(cfg, 21, t, r, batch=B) for r in range(world)] for t in range(T)]
     douts = [[WL.gen_dout(21, t, r, B * F, d, dmode) for r in range(world)] for t in range(T)]
-    K = max(len(b[rank][0]) for b in batches)
+    K = max(1, max(len(b[rank][0]) for b in batches))
     ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, max_keys=K, max_batch=B,
                       max_micro_batches=N, seed=13, init_mode=init, nccl_uids=uids, device=dev)
     run = Runner(ctx, N=N, pipelined=True, lr_over_B=lr)
@@ -120,11 +140,15 @@ def main():
                                                 bag_repeats=True, dim=64), 2048, 4, 4, "uniform",
          "realistic", 0.02),
     ]
+    # (name, cfg, B, N, T, init, dout mode, lr, batch generator)
+    cases.append(("edge-owner0-empty-P1-N2", WL.CONFIGS["tiny"].with_(bag_repeats=True, table_rows=(4000, 800, 64, 9)),
+                  64, 2, 5, "dyadic", "dyadic", 2.0 ** -10, skewed_batches))
     all_ok = True
     for case in cases:
         obj = [unique_ids() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        all_ok &= run_case(*case, rank, world, dev, obj[0])
+        gen = case[8] if len(case) > 8 else None
+        all_ok &= run_case(*case[:8], rank, world, dev, obj[0], gen=gen)
     dist.barrier(device_ids=[local])
     dist.destroy_process_group()
     if rank == 0:
