@@ -124,7 +124,7 @@ static size_t layout(Ctx& c, char* base) {
     c.cl_bm = w.take<uint32_t>(c.words + 2);
     c.cl_wr = w.take<int32_t>(c.words + 2);
     c.cl_samp = w.take<int32_t>(K);
-    c.cl_sk = w.take<uint32_t>(K);
+    c.cl_sk = w.take<uint32_t>(K + 1);
     c.cl_sv = w.take<int32_t>(K);
     c.cl_u = w.take<int32_t>(K);
     c.cl_inmask = w.take<uint32_t>(K);
@@ -133,6 +133,13 @@ static size_t layout(Ctx& c, char* base) {
     c.cl_S = w.take<int32_t>(Nm * B);
     c.cl_new = w.take<int32_t>(B);
     c.cl_small = w.take<int64_t>(4);
+    c.cl_hist = w.take<int32_t>(int64_t(Nm + 1) * kClHistBins);
+    c.cl_sel = w.take<int32_t>(8 * Nm);
+    c.cl_bcnt = w.take<int32_t>(((B + kClIds - 1) / kClIds + 1) * Nm);
+    c.cl_boff = w.take<int32_t>(B * c.F + 1);
+    c.cl_Scnt = w.take<int32_t>(Nm * B);
+    c.cl_kstart = w.take<int32_t>(K + 2);
+    c.cl_newk = w.take<uint64_t>(K + K / 128 + 64);
   }
   for (int si = 0; si < 2; ++si) {
     Slot& s = c.slot[si];
@@ -339,6 +346,7 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       }
     }
     NEST_CUDA(cudaEventCreateWithFlags(&c->ev_scratch, cudaEventDisableTiming));
+    if (c->cl_u) NEST_CUDA(cudaMallocHost(&c->cl_hmax, sizeof(int32_t)));
     NEST_CUDA(cudaStreamSynchronize(st0));
     if (c->W > 1) {
       NEST_CHECK(nccl_uids != nullptr, NEST_ERR_INVALID, "world > 1 needs NCCL unique ids");
@@ -375,6 +383,8 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
   if (c->ev_scratch) cudaEventDestroy(c->ev_scratch);
+  if (c->cl_hmax) cudaFreeHost(c->cl_hmax);
+  for (auto& kv : c->cl_graphs) cudaGraphExecDestroy(kv.second);
   for (auto& s : c->slot) {
     if (s.h_xfer) cudaFreeHost(s.h_xfer);
     cudaEvent_t evs[] = {s.ev_gather, s.ev_update, s.ev_free, s.ev_ready, s.ev_sync, s.ev_early, s.ev_repush,

@@ -63,15 +63,20 @@ __global__ void k_cl_keyid(int64_t nnz, const int64_t* __restrict__ keys, int T,
   }
 }
 
-// after the stable sort by key id: first occurrence of (sample, key) -> cl_u[j] = u, else -1
+// after the stable sort by key id: first occurrence of (sample, key) -> cl_u[j] = u, else -1;
+// kstart[u] = first position of key id u in the sorted occurrences
 __global__ void k_cl_first(int64_t nnz, const uint32_t* __restrict__ sk, const int32_t* __restrict__ sv,
-                           const int32_t* __restrict__ samp, int32_t* __restrict__ cl_u) {
+                           const int32_t* __restrict__ samp, int32_t* __restrict__ cl_u,
+                           int32_t* __restrict__ kstart) {
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nnz;
        q += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t u = sk[q];
     const int32_t j = sv[q];
-    bool first = q == 0 || sk[q - 1] != u || samp[sv[q - 1]] != samp[j];
+    const bool key_first = q == 0 || sk[q - 1] != u;
+    bool first = key_first || samp[sv[q - 1]] != samp[j];
     cl_u[j] = first ? int32_t(u) : -1;
+    if (key_first) kstart[u] = int32_t(q);
+    if (q == nnz - 1) kstart[u + 1] = int32_t(nnz);
   }
 }
 
@@ -137,23 +142,14 @@ __global__ void k_cl_seed_apply(int F, int g, const int32_t* __restrict__ bag_of
 
 constexpr uint32_t kTaken = 0xffffffffu;   // rank key of a sample no longer a candidate
 
-// round snapshot (warp per sample): S = |keys(s) & union(g)| folded into one
-// rank key per (g, s), ck = (smax - S) * (smax + 1) + (size - S), so that
-// "S desc, size - S asc" is "ck asc"; assigned samples get kTaken.
-__global__ void k_cl_S(int B, int F, int N, const int32_t* __restrict__ bag_off,
-                       const int32_t* __restrict__ cl_u, const uint32_t* __restrict__ inmask,
-                       const int32_t* __restrict__ grp, const int32_t* __restrict__ size,
-                       const int32_t* __restrict__ maxsz, uint32_t* __restrict__ ck) {
+// S[g][s] = |keys(s) & union(g)| from scratch (warp per sample), once after
+// the seeds; the rounds then maintain it incrementally (k_cl_spread)
+__global__ void k_cl_S_full(int B, int F, int N, const int32_t* __restrict__ bag_off,
+                            const int32_t* __restrict__ cl_u, const uint32_t* __restrict__ inmask,
+                            int32_t* __restrict__ S) {
   const int lane = lane_id();
-  const int smax = *maxsz;
-  const uint32_t nb = uint32_t(smax) + 1;
   const int64_t nw = int64_t(gridDim.x) * blockDim.x / 32;
   for (int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; s < B; s += nw) {
-    if (grp[s] >= 0) {
-      if (lane < N) ck[int64_t(lane) * B + s] = kTaken;
-      continue;
-    }
-    const int sz = size[s];
     const int j0 = bag_off[s * F], j1 = bag_off[(s + 1) * F];
     int cnt[NEST_MAX_MICRO_BATCHES] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = j0 + lane; j < j1; j += 32) {
@@ -167,14 +163,41 @@ __global__ void k_cl_S(int B, int F, int N, const int32_t* __restrict__ bag_off,
     for (int g = 0; g < NEST_MAX_MICRO_BATCHES; ++g) {
       int v = cnt[g];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == g && g < N) ck[int64_t(g) * B + s] = uint32_t(smax - v) * nb + uint32_t(sz - v);
+      if (lane == g && g < N) S[int64_t(g) * B + s] = v;
     }
   }
 }
 
-struct Takes {
-  int32_t v[NEST_MAX_MICRO_BATCHES];
-};
+// round snapshot (thread per sample): S folded into one rank key per (g, s),
+// ck = (smax - S) * (smax + 1) + (size - S), so that "S desc, size - S asc"
+// is "ck asc"; assigned samples get kTaken.  Also the level-1 histogram of
+// every group's candidate keys (bins ck >> lo), warp-aggregated.
+__global__ void k_cl_rank(int B, int N, int lo, const int32_t* __restrict__ S, const int32_t* __restrict__ grp,
+                          const int32_t* __restrict__ size, const int32_t* __restrict__ maxsz,
+                          uint32_t* __restrict__ ck, int32_t* __restrict__ hist) {
+  const int smax = *maxsz;
+  const uint32_t nb = uint32_t(smax) + 1;
+  const uint32_t lt = lanemask_lt();
+  for (int s0 = blockIdx.x * blockDim.x; s0 < B; s0 += gridDim.x * blockDim.x) {
+    const int s = s0 + threadIdx.x;
+    const bool cand = s < B && grp[s] < 0;
+    const int sz = cand ? size[s] : 0;
+    for (int g = 0; g < N; ++g) {
+      int bin = -1;
+      if (s < B) {
+        uint32_t key = kTaken;
+        if (cand) {
+          const int v = S[int64_t(g) * B + s];
+          key = uint32_t(smax - v) * nb + uint32_t(sz - v);
+          bin = int(key >> lo);
+        }
+        ck[int64_t(g) * B + s] = key;
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      if (bin >= 0 && (peers & lt) == 0) atomicAdd(&hist[g * kClHistBins + bin], __popc(peers));
+    }
+  }
+}
 
 // block-wide exclusive scan of one int per thread (1024 threads)
 __device__ __forceinline__ int block_excl_scan(int v, int* ws, int& total) {
@@ -218,144 +241,214 @@ __device__ void find_bin(const int* hist, int nbins, int k, int* ws, int* out) {
   __syncthreads();
 }
 
-// one round: groups 0..N-1 take their samples in order (single block).
-// Group g takes the k samples of least rank key ck (ties: lowest id): a radix
-// select on ck finds the threshold T and how many T-ties to take (one
-// histogram level when (smax+1)^2 <= kHistBins, else two), then every warp
-// walks its own contiguous id range in order, ranking the T-ties by id.
-// A sample taken by g is struck from the later groups' keys (ck = kTaken).
-constexpr int kHistLog = 14, kHistBins = 1 << kHistLog, kSelUnroll = 8;
-
-__global__ void __launch_bounds__(kSelThreads) k_cl_select(int B, int N, Takes takes,
-                                                           const int32_t* __restrict__ maxsz,
-                                                           uint32_t* ck, int32_t* __restrict__ grp,
-                                                           int32_t* __restrict__ newlist,
-                                                           int32_t* __restrict__ nnew) {
-  extern __shared__ int hist[];            // [kHistBins]
+// One round, group g after group g-1 (multi-block radix select): the
+// threshold T of g's k smallest rank keys and how many T-ties (kk) to take,
+// lowest ids first, from the level-1 histogram (bins ck >> lo) and, when the
+// keys need more than kClHistLog bits, a level-2 histogram of the low bits
+// inside the chosen bin; then every block of kClIds ids counts its ties and
+// assigns.  A sample taken by g leaves the later groups' histograms and keys.
+// sel[g]: {T, kk, partial, b1, kk1}
+__global__ void __launch_bounds__(kSelThreads) k_cl_find1(int k, int nb1, int lo, const int32_t* __restrict__ hist,
+                                                          int32_t* __restrict__ sel) {
   __shared__ int ws[33];
-  __shared__ int sel[2];
-  __shared__ int wcnt[32];
-  __shared__ int nnew_s;
-  const uint32_t nb = uint32_t(*maxsz) + 1;
-  const uint32_t nkeys = nb * nb;          // ck < nb^2 <= 2^28
-  int nbits = 0;
-  while ((1u << nbits) < nkeys) ++nbits;
-  const int lo = nbits > kHistLog ? nbits - kHistLog : 0;
-  const int nb1 = lo ? kHistBins : int(nkeys);
-  const uint32_t lomask = (1u << lo) - 1u;
-  const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t lt = lanemask_lt();
-  const int R = ((B + kSelThreads - 1) / kSelThreads) * 32;   // ids per warp, multiple of 32
-  const int w0 = min(B, warp * R), w1 = min(B, w0 + R);
-  if (threadIdx.x == 0) nnew_s = 0;
-  // warp-aggregated histogram increment (most candidates share a bin)
-  auto hist_add = [&](int bin) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-    if (bin >= 0 && (peers & lt) == 0) atomicAdd(&hist[bin], __popc(peers));
-  };
-  // the warp's range in id order, kSelUnroll loads in flight per lane
-  auto walk = [&](const uint32_t* ckg, auto&& f) {
-    for (int s0 = w0; s0 < w1; s0 += 32 * kSelUnroll) {
-      uint32_t v[kSelUnroll];
-#pragma unroll
-      for (int u = 0; u < kSelUnroll; ++u) {
-        const int s = s0 + u * 32 + lane;
-        v[u] = s < w1 ? ckg[s] : kTaken;
-      }
-#pragma unroll
-      for (int u = 0; u < kSelUnroll; ++u)
-        if (s0 + u * 32 < w1) f(s0 + u * 32 + lane, v[u]);
+  __shared__ int out[2];
+  find_bin(hist, nb1, k, ws, out);
+  if (threadIdx.x == 0) {
+    const int b1 = out[0], kk1 = k - out[1];
+    sel[3] = b1;
+    sel[4] = kk1;
+    if (lo == 0) {
+      sel[0] = b1;
+      sel[1] = kk1;
+      sel[2] = kk1 < hist[b1];
     }
-  };
-  for (int g = 0; g < N; ++g) {
-    const int k = takes.v[g];
-    if (k <= 0) continue;
-    const uint32_t* ckg = ck + int64_t(g) * B;
-    // level 1: bins of ck >> lo
-    for (int b = threadIdx.x; b < nb1; b += kSelThreads) hist[b] = 0;
-    __syncthreads();
-    walk(ckg, [&](int, uint32_t c) { hist_add(c != kTaken ? int(c >> lo) : -1); });
-    __syncthreads();
-    find_bin(hist, nb1, k, ws, sel);
-    uint32_t T = uint32_t(sel[0]);
-    int kk = k - sel[1];
-    int cnt = hist[sel[0]];
-    __syncthreads();
-    if (lo) {   // level 2: low bits inside the chosen bin
-      const uint32_t hi = T;
-      for (int b = threadIdx.x; b < (1 << lo); b += kSelThreads) hist[b] = 0;
-      __syncthreads();
-      walk(ckg, [&](int, uint32_t c) { hist_add(c != kTaken && (c >> lo) == hi ? int(c & lomask) : -1); });
-      __syncthreads();
-      find_bin(hist, 1 << lo, kk, ws, sel);
-      T = (hi << lo) | uint32_t(sel[0]);
-      kk -= sel[1];
-      cnt = hist[sel[0]];
-      __syncthreads();
-    }
-    const bool partial = kk < cnt;   // only then do the T-ties need ranking by id
-    int running = 0;
-    if (partial) {
-      int n = 0;
-      walk(ckg, [&](int, uint32_t c) { n += __popc(__ballot_sync(0xffffffffu, c == T)); });
-      if (lane == 0) wcnt[warp] = n;
-      __syncthreads();
-      for (int w = 0; w < warp; ++w) running += wcnt[w];
-    }
-    walk(ckg, [&](int s, uint32_t c) {
-      const uint32_t tie = __ballot_sync(0xffffffffu, c == T);
-      const bool take = c < T || (c == T && (!partial || running + __popc(tie & lt) < kk));
-      running += __popc(tie);
-      if (take) {
-        grp[s] = g;
-        for (int g2 = g + 1; g2 < N; ++g2) ck[int64_t(g2) * B + s] = kTaken;
-      }
-      const uint32_t m = __ballot_sync(0xffffffffu, take);
-      int base = 0;
-      if (lane == 0 && m) base = atomicAdd(&nnew_s, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (take) newlist[base + __popc(m & lt)] = s;
-    });
-    __syncthreads();
   }
-  if (threadIdx.x == 0) *nnew = nnew_s;
 }
 
-// union(g) grows by the keys of the samples taken this round (warp per sample)
+__global__ void k_cl_hist2(int B, int lo, const uint32_t* __restrict__ ckg, const int32_t* __restrict__ sel,
+                           int32_t* __restrict__ hist2) {
+  const uint32_t b1 = uint32_t(sel[3]), lomask = (1u << lo) - 1u;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < B; s += gridDim.x * blockDim.x) {
+    const uint32_t c = ckg[s];
+    if (c != kTaken && (c >> lo) == b1) atomicAdd(&hist2[c & lomask], 1);
+  }
+}
+
+// the group's threshold: T, the T-ties to take (kk), whether the tie bin is
+// taken partly -- resolved by every block from the histograms (level 1, or
+// level 2 inside the bin k_cl_find1 chose)
+struct Thr {
+  uint32_t T;
+  int kk;
+  bool partial;
+};
+__device__ Thr cl_resolve(int k, int nb1, int lo, const int32_t* hist1, const int32_t* hist2,
+                          const int32_t* sel, int* ws, int* out) {
+  Thr t;
+  if (lo == 0) {
+    find_bin(hist1, nb1, k, ws, out);
+    t.T = uint32_t(out[0]);
+    t.kk = k - out[1];
+    t.partial = t.kk < hist1[out[0]];
+  } else {
+    const int kk1 = sel[4];
+    find_bin(hist2, 1 << lo, kk1, ws, out);
+    t.T = (uint32_t(sel[3]) << lo) | uint32_t(out[0]);
+    t.kk = kk1 - out[1];
+    t.partial = t.kk < hist2[out[0]];
+  }
+  return t;
+}
+
+// ties of T per block of kClIds ids (only when the tie bin is taken partly)
+__global__ void __launch_bounds__(kClIds) k_cl_tiecount(int B, int k, int nb1, int lo,
+                                                        const uint32_t* __restrict__ ckg,
+                                                        const int32_t* __restrict__ hist1,
+                                                        const int32_t* __restrict__ hist2,
+                                                        const int32_t* __restrict__ sel, int32_t* __restrict__ bcnt) {
+  __shared__ int ws[33];
+  __shared__ int out[2];
+  const Thr t = cl_resolve(k, nb1, lo, hist1, hist2, sel, ws, out);
+  if (!t.partial) return;
+  const int s = blockIdx.x * kClIds + threadIdx.x;
+  const int n = __syncthreads_count(s < B && ckg[s] == t.T);
+  if (threadIdx.x == 0) bcnt[blockIdx.x] = n;
+}
+
+__global__ void __launch_bounds__(kClIds) k_cl_assign(int B, int N, int g, int k, int nb1, int lo, uint32_t* ck,
+                                                      const int32_t* __restrict__ sel, int32_t* hist,
+                                                      const int32_t* __restrict__ hist2,
+                                                      const int32_t* __restrict__ bcnt, int32_t* __restrict__ grp,
+                                                      int32_t* __restrict__ newlist, int32_t* __restrict__ nnew) {
+  __shared__ int ws[33];
+  __shared__ int out[2];
+  // (hist rows g2 > g change below, row g does not: every block resolves alike)
+  const Thr t = cl_resolve(k, nb1, lo, hist + g * kClHistBins, hist2, sel, ws, out);
+  const uint32_t T = t.T;
+  const int kk = t.kk;
+  const bool partial = t.partial;
+  int base = 0;
+  if (partial) {   // ties in the blocks before this one
+    int part = 0;
+    for (int b = threadIdx.x; b < blockIdx.x; b += kClIds) part += bcnt[b];
+    int tot;
+    block_excl_scan(part, ws, tot);
+    base = tot;
+  }
+  const int s = blockIdx.x * kClIds + threadIdx.x;
+  const uint32_t c = s < B ? ck[int64_t(g) * B + s] : kTaken;
+  const bool tie = c == T;
+  int tot;
+  const int rank = base + block_excl_scan(tie ? 1 : 0, ws, tot);
+  const bool take = c < T || (tie && (!partial || rank < kk));
+  if (take) {
+    grp[s] = g;
+    for (int g2 = g + 1; g2 < N; ++g2) {
+      uint32_t* p2 = ck + int64_t(g2) * B + s;
+      atomicSub(&hist[g2 * kClHistBins + (*p2 >> lo)], 1);
+      *p2 = kTaken;
+    }
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, take);
+  int at = 0;
+  if (lane_id() == 0 && m) at = atomicAdd(nnew, __popc(m));
+  at = __shfl_sync(0xffffffffu, at, 0);
+  if (take) newlist[at + __popc(m & lanemask_lt())] = s;
+}
+
+constexpr int kSpreadChunk = 128;   // occurrences per spread work item
+
+// union(g) grows by the keys of the samples taken this round (warp per
+// sample); every (key, group) bit set for the first time is listed as work
+// items of <= kSpreadChunk of the key's occurrences: u << 32 | chunk << 3 | g
 __global__ void k_cl_update(int F, const int32_t* __restrict__ newlist, const int32_t* __restrict__ nnew,
                             const int32_t* __restrict__ bag_off, const int32_t* __restrict__ cl_u,
-                            const int32_t* __restrict__ grp, uint32_t* __restrict__ inmask) {
+                            const int32_t* __restrict__ grp, uint32_t* __restrict__ inmask,
+                            const int32_t* __restrict__ kstart, uint64_t* __restrict__ newk,
+                            int32_t* __restrict__ nnewk) {
   const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
   const int n = *nnew;
   const int64_t nw = int64_t(gridDim.x) * blockDim.x / 32;
   for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < n; i += nw) {
     const int s = newlist[i];
-    const uint32_t bit = 1u << grp[s];
+    const int g = grp[s];
+    const uint32_t bit = 1u << g;
     const int j0 = bag_off[int64_t(s) * F], j1 = bag_off[int64_t(s + 1) * F];
-    for (int j = j0 + lane; j < j1; j += 32) {
-      const int32_t u = cl_u[j];
-      if (u >= 0 && !(inmask[u] & bit)) atomicOr(&inmask[u], bit);
+    for (int jb = j0; jb < j1; jb += 32) {
+      const int j = jb + lane;
+      const int32_t u = j < j1 ? cl_u[j] : -1;
+      bool fresh = false;
+      if (u >= 0 && !(inmask[u] & bit)) fresh = !(atomicOr(&inmask[u], bit) & bit);
+      const int nch = fresh ? (kstart[u + 1] - kstart[u] + kSpreadChunk - 1) / kSpreadChunk : 0;
+      const int inc = warp_incl_scan(nch);
+      const int tot = __shfl_sync(0xffffffffu, inc, 31);
+      int at = 0;
+      if (lane == 0 && tot) at = atomicAdd(nnewk, tot);
+      at = __shfl_sync(0xffffffffu, at, 0) + inc - nch;
+      for (int ch = 0; ch < nch; ++ch)
+        newk[at + ch] = (uint64_t(uint32_t(u)) << 32) | (uint64_t(ch) << 3) | uint64_t(g);
     }
   }
 }
 
-// perm = samples sorted by (group, id); mb_offsets = g * cap (single block)
-__global__ void __launch_bounds__(kSelThreads) k_cl_perm(int B, int N, const int32_t* __restrict__ grp,
-                                                         int32_t* __restrict__ perm, int32_t* __restrict__ mbo) {
+// S[g][s] += 1 for every unassigned sample s holding a key that joined
+// union(g) this round (warp per work item: a chunk of the key's occurrences)
+__global__ void k_cl_spread(int B, const uint64_t* __restrict__ newk, const int32_t* __restrict__ nnewk,
+                            const int32_t* __restrict__ kstart, const uint32_t* __restrict__ sk,
+                            const int32_t* __restrict__ sv, const int32_t* __restrict__ cl_u,
+                            const int32_t* __restrict__ samp, const int32_t* __restrict__ grp,
+                            int32_t* __restrict__ S) {
+  const int lane = lane_id();
+  const int n = *nnewk;
+  const int64_t nw = int64_t(gridDim.x) * blockDim.x / 32;
+  for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < n; i += nw) {
+    const uint64_t e = newk[i];
+    const uint32_t u = uint32_t(e >> 32), g = uint32_t(e) & 7u, ch = uint32_t(e) >> 3;
+    const int q0 = kstart[u] + int(ch) * kSpreadChunk;
+    const int q1 = min(q0 + kSpreadChunk, kstart[u + 1]);
+    for (int q = q0 + lane; q < q1; q += 32) {
+      const int32_t j = sv[q];
+      if (cl_u[j] < 0) continue;   // not the sample's first occurrence of u
+      const int32_t s = samp[j];
+      if (grp[s] < 0) atomicAdd(&S[int64_t(g) * B + s], 1);
+    }
+  }
+}
+
+// perm = samples sorted by (group, id): per block of kClIds ids the count of
+// each group, then every block places its members after the earlier blocks'
+__global__ void __launch_bounds__(kClIds) k_cl_gcount(int B, int N, const int32_t* __restrict__ grp,
+                                                      int32_t* __restrict__ bcnt) {
+  const int s = blockIdx.x * kClIds + threadIdx.x;
+  const int gs = s < B ? grp[s] : -1;
+  for (int g = 0; g < N; ++g) {
+    const int n = __syncthreads_count(gs == g);
+    if (threadIdx.x == 0) bcnt[blockIdx.x * N + g] = n;
+  }
+}
+
+__global__ void __launch_bounds__(kClIds) k_cl_perm(int B, int N, const int32_t* __restrict__ grp,
+                                                    const int32_t* __restrict__ bcnt, int32_t* __restrict__ perm,
+                                                    int32_t* __restrict__ mbo) {
   __shared__ int ws[33];
   const int cap = B / N;
-  const int per = (B + kSelThreads - 1) / kSelThreads;
-  const int s0 = threadIdx.x * per, s1 = min(B, s0 + per);
+  const int s = blockIdx.x * kClIds + threadIdx.x;
+  const int gs = s < B ? grp[s] : -1;
   for (int g = 0; g < N; ++g) {
-    int mine = 0;
-    for (int s = s0; s < s1; ++s) mine += grp[s] == g;
+    int part = 0;
+    for (int b = threadIdx.x; b < blockIdx.x; b += kClIds) part += bcnt[b * N + g];
+    int base;
+    block_excl_scan(part, ws, base);
     int tot;
-    int r = block_excl_scan(mine, ws, tot);
-    for (int s = s0; s < s1; ++s)
-      if (grp[s] == g) perm[g * cap + r++] = s;
+    const int r = block_excl_scan(gs == g ? 1 : 0, ws, tot);
+    if (gs == g) perm[g * cap + base + r] = s;
   }
-  if (threadIdx.x <= N) mbo[threadIdx.x] = threadIdx.x * cap;
+  if (blockIdx.x == 0 && threadIdx.x <= N) mbo[threadIdx.x] = threadIdx.x * cap;
 }
+
+static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int nb1, int32_t* maxsz, int32_t* nnew,
+                           cudaStream_t st);
 
 void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N,
                     int32_t* perm, int32_t* mb_offsets, cudaStream_t st) {
@@ -384,7 +477,7 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
   int kbits = 0;
   while ((int64_t(1) << kbits) < c.Kcap) ++kbits;
   radix_sort_pairs(c, c.tkey[0], c.tval[0], c.cl_sk, c.cl_sv, nnz, kbits, st);
-  k_cl_first<<<grid(nnz, 256), 256, 0, st>>>(nnz, c.cl_sk, c.cl_sv, samp, c.cl_u);
+  k_cl_first<<<grid(nnz, 256), 256, 0, st>>>(nnz, c.cl_sk, c.cl_sv, samp, c.cl_u, c.cl_kstart);
   NEST_CUDA(cudaMemsetAsync(c.cl_small, 0, sizeof(int64_t) * 4, st));
   int32_t* maxsz = reinterpret_cast<int32_t*>(c.cl_small);
   unsigned long long* best = reinterpret_cast<unsigned long long*>(c.cl_small + 1);
@@ -399,34 +492,89 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
                                                                  c.cl_size, c.cl_grp, best);
     k_cl_seed_apply<<<1, 256, 0, st>>>(F, g, bag_offsets, c.cl_u, best, c.cl_inmask, c.cl_grp);
   }
-  // rounds: admission sizes are a function of (B, N) only
+  k_cl_S_full<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(B, F, N, bag_offsets, c.cl_u, c.cl_inmask, c.cl_Scnt);
+  // the rank keys' histogram split needs smax (one read back on this stream)
+  int32_t smax = 0;
+  NEST_CUDA(cudaMemcpyAsync(c.cl_hmax, maxsz, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  NEST_CUDA(cudaStreamSynchronize(st));
+  smax = *c.cl_hmax;
+  const uint32_t nkeys = uint32_t(smax + 1) * uint32_t(smax + 1);
+  int nbits = 0;
+  while ((1u << nbits) < nkeys) ++nbits;
+  const int lo = nbits > kClHistLog ? nbits - kClHistLog : 0;
+  const int nb1 = lo ? kClHistBins : int(nkeys);
+  // rounds: admission sizes are a function of (B, N) only, every buffer is the
+  // library's, so the whole round sequence is captured once per (B, N, lo)
+  // into a CUDA graph and replayed (it is ~37 rounds of 3N + 4 launches)
+  NEST_CUDA(cudaMemcpyAsync(c.cl_boff, bag_offsets, sizeof(int32_t) * (nbags + 1), cudaMemcpyDeviceToDevice, st));
+  const auto gkey = std::make_tuple(B, N, lo);
+  auto git = c.cl_graphs.find(gkey);
+  if (st == nullptr) {
+    cluster_rounds(c, B, N, F, lo, nb1, maxsz, nnew, st);   // legacy stream: no capture
+  } else if (git == c.cl_graphs.end()) {
+    NEST_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    cluster_rounds(c, B, N, F, lo, nb1, maxsz, nnew, st);
+    cudaGraph_t graph = nullptr;
+    NEST_CUDA(cudaStreamEndCapture(st, &graph));
+    cudaGraphExec_t exec = nullptr;
+    NEST_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    git = c.cl_graphs.emplace(gkey, exec).first;
+  }
+  if (st != nullptr) NEST_CUDA(cudaGraphLaunch(git->second, st));
+  const int nblk = (B + kClIds - 1) / kClIds;
+  k_cl_gcount<<<nblk, kClIds, 0, st>>>(B, N, c.cl_grp, c.cl_bcnt);
+  k_cl_perm<<<nblk, kClIds, 0, st>>>(B, N, c.cl_grp, c.cl_bcnt, perm, mb_offsets);
+  NEST_LAUNCH_CHECK();
+}
+
+// the admission rounds on library buffers only (captured into a graph)
+static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int nb1, int32_t* maxsz, int32_t* nnew,
+                           cudaStream_t st) {
+  int32_t* nnewk = reinterpret_cast<int32_t*>(c.cl_small + 3);
+  const int32_t* bag_offsets = c.cl_boff;
+  auto grid = [](int64_t n, int t) {
+    int64_t b = (n + t - 1) / t;
+    return int(b < 1 ? 1 : (b > 148 * 16 ? 148 * 16 : b));
+  };
   const int cap = B / N;
+  const int nblk = (B + kClIds - 1) / kClIds;
   std::vector<int64_t> have(N, 1);
   int64_t assigned = N;
   uint64_t Q = uint64_t(1) << 32;
-  const size_t smem = sizeof(int) * kHistBins;
   uint32_t* ck = reinterpret_cast<uint32_t*>(c.cl_S);
-  static bool attr = false;
-  if (!attr) {
-    NEST_CUDA(cudaFuncSetAttribute(k_cl_select, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  int32_t* hist2 = c.cl_hist + int64_t(N) * kClHistBins;
   while (assigned < B) {
     if (Q < (uint64_t(1) << 62)) Q = (5 * Q) / 4;
     const int64_t q = std::max<int64_t>(1, int64_t(Q >> 32));
-    Takes tk{};
+    int take[NEST_MAX_MICRO_BATCHES];
     for (int g = 0; g < N; ++g) {
-      tk.v[g] = int32_t(std::min<int64_t>(cap - have[g], q));
-      have[g] += tk.v[g];
-      assigned += tk.v[g];
+      take[g] = int(std::min<int64_t>(cap - have[g], q));
+      have[g] += take[g];
+      assigned += take[g];
     }
-    k_cl_S<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(B, F, N, bag_offsets, c.cl_u, c.cl_inmask, c.cl_grp,
-                                                      c.cl_size, maxsz, ck);
-    k_cl_select<<<1, kSelThreads, smem, st>>>(B, N, tk, maxsz, ck, c.cl_grp, c.cl_new, nnew);
+    NEST_CUDA(cudaMemsetAsync(c.cl_hist, 0, sizeof(int32_t) * kClHistBins * N, st));
+    NEST_CUDA(cudaMemsetAsync(nnew, 0, sizeof(int32_t), st));
+    k_cl_rank<<<grid(B, 256), 256, 0, st>>>(B, N, lo, c.cl_Scnt, c.cl_grp, c.cl_size, maxsz, ck, c.cl_hist);
+    for (int g = 0; g < N; ++g) {
+      if (take[g] <= 0) continue;
+      int32_t* sel = c.cl_sel + 8 * g;
+      const int32_t* h1 = c.cl_hist + int64_t(g) * kClHistBins;
+      if (lo) {
+        k_cl_find1<<<1, kSelThreads, 0, st>>>(take[g], nb1, lo, h1, sel);
+        NEST_CUDA(cudaMemsetAsync(hist2, 0, sizeof(int32_t) << lo, st));
+        k_cl_hist2<<<grid(B, 256), 256, 0, st>>>(B, lo, ck + int64_t(g) * B, sel, hist2);
+      }
+      k_cl_tiecount<<<nblk, kClIds, 0, st>>>(B, take[g], nb1, lo, ck + int64_t(g) * B, h1, hist2, sel, c.cl_bcnt);
+      k_cl_assign<<<nblk, kClIds, 0, st>>>(B, N, g, take[g], nb1, lo, ck, sel, c.cl_hist, hist2, c.cl_bcnt,
+                                           c.cl_grp, c.cl_new, nnew);
+    }
+    NEST_CUDA(cudaMemsetAsync(nnewk, 0, sizeof(int32_t), st));
     k_cl_update<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(F, c.cl_new, nnew, bag_offsets, c.cl_u, c.cl_grp,
-                                                           c.cl_inmask);
+                                                           c.cl_inmask, c.cl_kstart, c.cl_newk, nnewk);
+    k_cl_spread<<<148 * 8, 256, 0, st>>>(B, c.cl_newk, nnewk, c.cl_kstart, c.cl_sk, c.cl_sv, c.cl_u,
+                                         c.cl_samp, c.cl_grp, c.cl_Scnt);
   }
-  k_cl_perm<<<1, kSelThreads, 0, st>>>(B, N, c.cl_grp, perm, mb_offsets);
   NEST_LAUNCH_CHECK();
 }
 

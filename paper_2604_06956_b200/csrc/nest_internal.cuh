@@ -7,6 +7,9 @@
 #pragma once
 
 #include <cuda_bf16.h>
+
+#include <map>
+#include <tuple>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -189,6 +192,15 @@ struct Ctx {
   int32_t* cl_S = nullptr;         // [Nmax][Bcap]
   int32_t* cl_new = nullptr;       // [Bcap]
   int64_t* cl_small = nullptr;     // [4]
+  int32_t* cl_hist = nullptr;      // [Nmax + 1][kClHistBins] rank-key histograms (level 1 per group | level 2)
+  int32_t* cl_sel = nullptr;       // [Nmax][8] per-group threshold state
+  int32_t* cl_bcnt = nullptr;      // [B / kClIds + 1][Nmax] ties / group members per id block
+  int32_t* cl_hmax = nullptr;      // pinned: largest distinct-key count of a sample (host copy)
+  int32_t* cl_boff = nullptr;      // [Bcap*F+1] library copy of the batch's bag offsets (graph input)
+  int32_t* cl_Scnt = nullptr;      // [Nmax][Bcap] S = |keys(s) & union(g)|, maintained incrementally
+  int32_t* cl_kstart = nullptr;    // [Kcap+1] first position of each key id in the key-sorted occurrences
+  uint64_t* cl_newk = nullptr;     // [Kcap + Kcap/128 + 64] (key id, chunk, group) spread work items
+  std::map<std::tuple<int, int, int>, cudaGraphExec_t> cl_graphs;  // (B, N, lo) -> captured rounds
   Slot slot[2];
   uint32_t epoch = 0;
   // last use of the shared routing scratch (tkey/tval, hist, scan_tmp, occ_*,
@@ -223,6 +235,10 @@ inline float* src_rows_of(const Ctx& c, const Slot& s) {
   return c.src_rows + slot_index(c, s) * c.src_slot_stride;
 }
 inline float* peer_src_of(const Ctx& c, const Slot& s, int p) { return c.peer_src_slot[slot_index(c, s)][p]; }
+
+// GPU clustering (cluster.cu): histogram bins of the radix select, ids per
+// block of the ordered passes
+constexpr int kClHistLog = 14, kClHistBins = 1 << kClHistLog, kClIds = 1024;
 
 // bump allocator over a caller-owned buffer (base == nullptr: size only)
 struct Carver {

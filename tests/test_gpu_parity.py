@@ -228,10 +228,17 @@ def test_unpooled_expand_p1():
 
 
 # --------------------------------------------------------------------------- clustering
-@pytest.mark.parametrize("case", ["tiny-N2", "tiny-N4", "corr-N4", "corr-N8", "dlrmish-N4"])
+@pytest.mark.parametrize("case", ["tiny-N2", "tiny-N4", "corr-N4", "corr-N8", "dlrmish-N4", "longbag-N4"])
 def test_cluster_bit_exact_vs_oracle(case):
-    """R14: GPU round-based greedy == oracle.cluster.cluster_rounds (perm + offsets)."""
-    if case.startswith("tiny"):
+    """R14: GPU round-based greedy == oracle.cluster.cluster_rounds (perm + offsets).
+    longbag: > 127 distinct keys per sample, so the rank keys need the second
+    histogram level of the select."""
+    if case.startswith("longbag"):
+        cfg = WL.CONFIGS["tiny"].with_(table_rows=(20000,) * 4, bag_len=(30, 60), bag_repeats=True, zipf=1.1)
+        B, N = 256, 4
+        keys, offs = WL.gen_batch(cfg, 6, 0, 0, batch=B)
+        assert max(len(k) for k in OC.sample_keysets(keys, offs, cfg.num_features)) > 127
+    elif case.startswith("tiny"):
         cfg, B, N = WL.CONFIGS["tiny"], 32, int(case[-1])
         keys, offs = WL.gen_batch(cfg, 4, 0, 0, batch=B)
     elif case.startswith("corr"):
@@ -246,6 +253,23 @@ def test_cluster_bit_exact_vs_oracle(case):
     ref_perm, ref_mbo = OC.cluster_rounds(OC.sample_keysets(keys, offs, cfg.num_features), N)
     assert np.array_equal(perm.cpu().numpy(), ref_perm)
     assert np.array_equal(mbo.cpu().numpy(), ref_mbo)
+
+
+def test_cluster_repeated_batches_same_shape():
+    """The captured round sequence is replayed for later batches of the same
+    shape: every batch still matches the oracle."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(3000,) * 4)
+    B, N = 512, 4
+    ctx = make_ctx(cfg, B, N=N, K=B * cfg.num_features * cfg.bag_len[1])
+    side = torch.cuda.Stream()   # a non-legacy stream: the rounds are captured and replayed
+    for t in range(3):
+        keys, offs = WL.gen_correlated_batch(cfg, 9, t, 0, groups=8, rho=0.6, batch=B)
+        kd, od = to_dev(keys, torch.int64), to_dev(offs, torch.int32)
+        side.wait_stream(torch.cuda.current_stream())
+        perm, mbo = ctx.fwp_schedule(kd, od, B, N, "clustered", stream=side)
+        torch.cuda.synchronize()
+        ref_perm, _ = OC.cluster_rounds(OC.sample_keysets(keys, offs, cfg.num_features), N)
+        assert np.array_equal(perm.cpu().numpy(), ref_perm), t
 
 
 def test_train_w1_clustered_p1_bit_exact():
