@@ -79,6 +79,25 @@ def peaks():
     return 6650.0, 1400.0, "fallback"
 
 
+def roofline_from(st, key_prefix):
+    """HBM roofline of the dominant single-kernel stage of a profiled run:
+    algorithmic bytes per launch / event-measured time per launch."""
+    hbm_peak, _, src = peaks()
+    # single-kernel HBM stages (route / sort / owner_dedup are multi-kernel
+    # sequences on the aux stream, reported in `stages` only)
+    hbm_stages = ["gather", "refresh", "send_gather", "pool", "segsum", "update"]
+    dom = max((n for n in hbm_stages if st[n]["records"]), key=lambda n: st[n]["ms"])
+    ds = st[dom]
+    achieved = ds["bytes"] / (ds["ms"] * 1e6)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{key_prefix}/{dom}")
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": src,
+            "bytes_per_launch": ds["bytes"] / ds["records"], "ms_per_launch": ds["ms"] / ds["records"]}
+
+
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
     FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
@@ -154,10 +173,12 @@ def oracle_sample_step(cfg, seed, rank, samples, step=0):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(cfg, seed, budget_s=15.0):
+def cpu_baseline(cfg, seed, min_s=10.0):
+    """The oracle on a bounded sample: grow the sample x4 until one step costs
+    >= min_s of CPU time (10-30 s) or covers the whole local batch."""
     samples = 1024
     dt = oracle_sample_step(cfg, seed, 0, samples)
-    while dt < budget_s / 4 and samples < cfg.batch_local:
+    while dt < min_s and samples < cfg.batch_local:
         samples = min(cfg.batch_local, samples * 4)
         dt = oracle_sample_step(cfg, seed, 0, samples)
     return {"value": samples / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -403,6 +424,8 @@ def main():
         st1 = prof1["stages"]
         return {"N": Nv, "steps": args.steps, "ms_per_step": ms1 / args.steps,
                 "samples_per_s": B * world * args.steps / (ms1 / 1e3),
+                # the same roofline kernel without the tower's GEMMs beside it
+                "roofline": roofline_from(st1, f"{cfg.name}/W{world}/N{Nv}"),
                 "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in st1.items() if v["records"]}}
 
     with_tower_runs, embedding_only = None, None
@@ -444,22 +467,7 @@ def main():
                 e["hbm_gbs"] = gbs
                 e["frac_of_measured_hbm"] = gbs / hbm_peak if gbs else None
             stages[name] = e
-        # single-kernel HBM stages (route / sort / owner_dedup are multi-kernel
-        # sequences on the aux stream, reported in `stages` only)
-        hbm_stages = ["gather", "refresh", "send_gather", "pool", "segsum", "update"]
-        dom = max((n for n in hbm_stages if n in stages), key=lambda n: st[n]["ms"])
-        ds = st[dom]
-        achieved = ds["bytes"] / (ds["ms"] * 1e6)
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
-            tj = json.load(open(tp))
-            key = f"{cfg.name}/W{world}/N{N}/{dom}"
-            if key in tj:
-                traffic = tj[key]
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": src,
-                    "bytes_per_launch": ds["bytes"] / ds["records"], "ms_per_launch": ds["ms"] / ds["records"]}
+        roofline = roofline_from(st, f"{cfg.name}/W{world}/N{N}")
         summ = prof["summary"]
         a2a = None
         if world > 1:
