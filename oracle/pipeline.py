@@ -64,6 +64,7 @@ class PipeConfig:
     F: int = 1
     pipelined: bool = True               # prefetch(t+1) before update(t)
     unsafe_six_stage: bool = False
+    optimizer: object = None             # None: SGD (Eq. 2); else step.RowwiseAdagrad
 
 
 @dataclass
@@ -179,7 +180,8 @@ def nestpipe_train(shard_init: LazyTable, batches_by_step, douts_by_step,
         # ---------------- single deferred update + write-back ----------------
         for o in range(W):
             if len(active[o].keys):
-                active[o].rows = sgd_rows(active[o].rows, acc[o], cfg.lr_over_B)
+                active[o].rows = sgd_rows(active[o].rows, acc[o], cfg.lr_over_B) if cfg.optimizer is None \
+                    else cfg.optimizer.apply(active[o].keys, active[o].rows, acc[o])
                 active[o].dirty = active[o].keys.copy()
                 shards[o].set(active[o].keys, active[o].rows)
         table = {}
@@ -200,13 +202,13 @@ def nestpipe_train(shard_init: LazyTable, batches_by_step, douts_by_step,
 
 
 def sync_train(table: LazyTable, batches_by_step, douts_by_step, lr_over_B,
-               pooling="sum", grad_mode="lin"):
+               pooling="sum", grad_mode="lin", optimizer=None):
     """T steps of oracle.step.sync_step; returns per-step {key: row} of K(B_t)."""
     from .step import sync_step
     out = []
     for t, batches in enumerate(batches_by_step):
         res = sync_step(table, batches, douts_by_step[t] if douts_by_step else None,
-                        lr_over_B, pooling, grad_mode)
+                        lr_over_B, pooling, grad_mode, optimizer)
         rows = table.get(res.grads.keys)
         out.append({int(k): r.copy() for k, r in zip(res.grads.keys, rows)})
     return out

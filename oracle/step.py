@@ -125,6 +125,40 @@ def sgd_rows(rows: np.ndarray, grad: np.ndarray, lr_over_B: float) -> np.ndarray
     return (rows.astype(np.float64) - s * grad).astype(np.float32)
 
 
+class RowwiseAdagrad:
+    """Row-wise AdaGrad, the sparse optimizer of SURVEY §8(f) NEXT-2 (the paper
+    and SPEC leave the optimizer open; industry convention = FBGEMM's
+    exact row-wise AdaGrad).  One accumulator m per embedding row, initially
+    `init`; for a key k of K(B_t) with summed gradient G_k (the same sum Eq. 2
+    scales):
+        g   = grad_scale * G_k                      (grad_scale = 1/|B|)
+        m_k = m_k + (1/d) * sum_j g_j^2
+        e_k = e_k - lr * g / (sqrt(m_k) + eps)
+    Rows of keys outside K(B_t) and their accumulators are unchanged.  fp64
+    arithmetic on the fp32 inputs (grad_scale, lr, eps as fp32 values), the row
+    rounded to fp32 once per step; the accumulator is kept in fp64.
+    """
+
+    def __init__(self, lr: float, grad_scale: float, eps: float = 1e-8, init: float = 0.0):
+        self.lr = np.float64(np.float32(lr))
+        self.gs = np.float64(np.float32(grad_scale))
+        self.eps = np.float64(np.float32(eps))
+        self.init = float(init)
+        self.state = {}
+
+    def get_state(self, keys) -> np.ndarray:
+        return np.array([self.state.get(int(k), self.init) for k in np.asarray(keys, np.int64)], np.float64)
+
+    def apply(self, keys, rows: np.ndarray, grad: np.ndarray) -> np.ndarray:
+        keys = np.asarray(keys, np.int64)
+        g = self.gs * np.asarray(grad, np.float64)
+        m = self.get_state(keys) + (g * g).mean(axis=1)
+        for k, mk in zip(keys, m):
+            self.state[int(k)] = float(mk)
+        mult = self.lr / (np.sqrt(m) + self.eps)
+        return (rows.astype(np.float64) - mult[:, None] * g).astype(np.float32)
+
+
 @dataclass
 class StepResult:
     pooled: List[np.ndarray]   # per rank, fp32
@@ -132,17 +166,20 @@ class StepResult:
 
 
 def sync_step(table: LazyTable, batches, douts=None, lr_over_B: float = 2.0 ** -10,
-              pooling: str = "sum", grad_mode: str = "lin") -> StepResult:
+              pooling: str = "sum", grad_mode: str = "lin", optimizer=None) -> StepResult:
     """oracle.sync_step: one synchronous step over the global batch.
 
     grad_mode 'lin'  : dpooled = douts[r] (seeded, independent of E)
     grad_mode 'quad' : L = 1/2 sum ||pooled||^2, so dpooled = pooled.
     Mutates `table` to E_{t+1}; only keys in K(B_t) change (Eq. 2).
+    optimizer: None = SGD of Eq. 2 with lr_over_B, else a RowwiseAdagrad.
     """
     pooled = [forward(table, k, o, pooling) for (k, o) in batches]
     if grad_mode == "quad":
         douts = pooled
     g = key_grads(batches, douts, pooling)
     if len(g.keys):
-        table.set(g.keys, sgd_rows(table.get(g.keys), g.grad, lr_over_B))
+        rows = table.get(g.keys)
+        new = sgd_rows(rows, g.grad, lr_over_B) if optimizer is None else optimizer.apply(g.keys, rows, g.grad)
+        table.set(g.keys, new)
     return StepResult(pooled, g)

@@ -436,3 +436,73 @@ def test_workload_deterministic_and_skewed():
     r = WL.zipf_ranks(np.random.default_rng(0), 1.2, 10 ** 4, 10 ** 5)
     cnt = np.bincount(r, minlength=10 ** 4)
     assert cnt[0] > cnt[99] > 0
+
+
+# --------------------------------------------------------------------------- row-wise AdaGrad (NEXT-2)
+def _one_bag_step(opt, dout_rows, keys_per_bag, seed=3, d=4):
+    """One sync step: bag b holds keys_per_bag[b] (one rank), dpooled = dout_rows."""
+    keys = np.array([k for ks in keys_per_bag for k in ks], np.int64)
+    offs = np.concatenate([[0], np.cumsum([len(ks) for ks in keys_per_bag])]).astype(np.int64)
+    tab = S.LazyTable(seed, d, "dyadic")
+    before = {int(k): tab.get([k])[0].copy() for k in np.unique(keys)}
+    S.sync_step(tab, [(keys, offs)], [np.asarray(dout_rows, np.float32)], 0.0, optimizer=opt)
+    return tab, before
+
+
+def test_adagrad_first_steps_closed_form():
+    """eps = 0, uniform gradient c: step 1 moves every element by exactly
+    -lr*sign(c) (m = c^2); step 2 by -lr*sign(c)/sqrt(2) (m = 2c^2)."""
+    k, c, lr = (2 << 40) | 17, -2.0 ** -3, 2.0 ** -4
+    opt = S.RowwiseAdagrad(lr=lr, grad_scale=1.0, eps=0.0)
+    tab, before = _one_bag_step(opt, [[c] * 4], [[k]])
+    e1 = tab.get([k])[0]
+    assert np.array_equal(e1, (before[k].astype(np.float64) + lr).astype(np.float32))
+    assert opt.get_state([k])[0] == c * c
+    keys, offs = np.array([k], np.int64), np.array([0, 1], np.int64)
+    S.sync_step(tab, [(keys, offs)], [np.full((1, 4), c, np.float32)], 0.0, optimizer=opt)
+    e2 = tab.get([k])[0]
+    assert np.array_equal(e2, (e1.astype(np.float64) + lr / np.sqrt(2.0)).astype(np.float32))
+    assert opt.get_state([k])[0] == 2 * c * c
+
+
+def test_adagrad_rowwise_mean_and_sum_before_square():
+    """m is the mean over d of the squared SUMMED gradient: g = (3,4,0,0)/16
+    gives sqrt(m) = 2.5/16, so the step is lr*(1.2, 1.6, 0, 0); a key in two
+    bags with gradient c each moves like one bag with 2c (sum, then square)."""
+    k, lr = (1 << 40) | 5, 2.0 ** -3
+    opt = S.RowwiseAdagrad(lr=lr, grad_scale=1.0, eps=0.0)
+    tab, before = _one_bag_step(opt, [[3 / 16, 4 / 16, 0, 0]], [[k]])
+    want = (before[k].astype(np.float64) - lr * np.array([1.2, 1.6, 0.0, 0.0])).astype(np.float32)
+    assert np.allclose(tab.get([k])[0], want, rtol=0, atol=1e-7)
+    c = 2.0 ** -5
+    opt2 = S.RowwiseAdagrad(lr=lr, grad_scale=1.0, eps=0.0)
+    tab2, before2 = _one_bag_step(opt2, [[c] * 4, [c] * 4], [[k], [k]])
+    assert np.array_equal(tab2.get([k])[0], (before2[k].astype(np.float64) - lr).astype(np.float32))
+    assert opt2.get_state([k])[0] == (2 * c) ** 2
+
+
+def test_adagrad_grad_scale_eps_and_untouched_keys():
+    """grad_scale scales g before squaring; eps enters the denominator; keys
+    outside K(B_t) keep their rows and accumulators."""
+    k, other, lr, gs, eps = (0 << 40) | 9, (0 << 40) | 10, 2.0 ** -2, 2.0 ** -2, 2.0 ** -4
+    opt = S.RowwiseAdagrad(lr=lr, grad_scale=gs, eps=eps, init=2.0 ** -6)
+    tab, before = _one_bag_step(opt, [[1.0] * 4], [[k]])
+    g = gs * 1.0
+    m = 2.0 ** -6 + g * g
+    want = (before[k].astype(np.float64) - lr * g / (np.sqrt(m) + eps)).astype(np.float32)
+    assert np.array_equal(tab.get([k])[0], want)
+    assert opt.get_state([other])[0] == 2.0 ** -6
+    assert np.array_equal(tab.get([other])[0], S.LazyTable(3, 4, "dyadic").get([other])[0])
+
+
+@pytest.mark.parametrize("W,N,cl", [(2, 1, "sequential"), (2, 2, "clustered"), (3, 2, "sequential")])
+def test_adagrad_pipelined_equals_sync_bitwise(W, N, cl):
+    """Corollary 1 with row-wise AdaGrad: the accumulator lives with the
+    owner's row and is read and written only by the update, so DBP+FWP still
+    reproduce the synchronous step bit for bit (P1 gradients)."""
+    batches, douts = _tiny_traj(W)
+    mk = lambda: S.RowwiseAdagrad(lr=2.0 ** -6, grad_scale=2.0 ** -5, eps=1e-8)
+    ref = P.sync_train(S.LazyTable(1, 16, "dyadic"), batches, douts, 0.0, optimizer=mk())
+    tr = P.nestpipe_train(S.LazyTable(1, 16, "dyadic"), batches, douts,
+                          P.PipeConfig(W=W, N=N, cluster=cl, F=4, optimizer=mk()))
+    assert P.first_divergence(ref, [t.table for t in tr]) is None
