@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--variant", default="et", choices=["et", "e"],
                     help="et: embedding + stand-in tower (FWP overlap partner; headline); e: embedding only")
     ap.add_argument("--batches", type=int, default=3, help="distinct batches cycled per rank")
+    ap.add_argument("--optimizer", default="sgd", choices=["sgd", "rowwise_adagrad"],
+                    help="sparse update: SGD of Eq. 2 (default) or row-wise AdaGrad (SURVEY NEXT-2)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -212,7 +214,7 @@ def config_json(args, cfg, world):
     return {"workload": cfg.name, "tables": cfg.num_tables, "total_rows": int(sum(cfg.table_rows)),
             "dim": cfg.dim, "batch_per_gpu": cfg.batch_local, "global_batch": cfg.batch_local * world,
             "bag_len": f"U{{{cfg.bag_len[0]}..{cfg.bag_len[1]}}}", "zipf": cfg.zipf, "pooling": cfg.pooling,
-            "micro_batches": args.micro_batches, "schedule": args.schedule,
+            "micro_batches": args.micro_batches, "schedule": args.schedule, "optimizer": args.optimizer,
             "variant": "E+T (embedding + stand-in tower)" if args.variant == "et" else "E (embedding only)",
             "tower": f"{cfg.tower_layers}x{cfg.tower_hidden} bf16 cuBLAS" if args.variant == "et" else None,
             "dout": "stand-in tower input gradient" if args.variant == "et" else
@@ -279,7 +281,7 @@ def main():
                       max_keys=K + 1024,
                       max_batch=B, max_micro_batches=Nctx, seed=args.seed + 1, init_mode="uniform",
                       tower_layers=cfg.tower_layers if with_tower else 0,
-                      tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev,
+                      tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev, optimizer=args.optimizer,
                       max_recv_keys=int(1.5 * U) + 1024 if world > 1 else U + 1024,
                       max_mb_rows=mb_rows,
                       max_owner_mb_rows=int(1.5 * mb_rows) if world > 1 else 0)
@@ -288,6 +290,8 @@ def main():
     dev_b = [(torch.from_numpy(k).to(dev), torch.from_numpy(o).to(dev), B) for k, o in batches]
     host_b = [(torch.from_numpy(k).pin_memory(), torch.from_numpy(o).pin_memory()) for k, o in batches]
     lr = 1e-3 / (B * world)
+    # row-wise AdaGrad: g = G / |B_global|, step size 0.01
+    adagrad = (1.0 / (B * world), 0.01) if args.optimizer == "rowwise_adagrad" else None
 
     def pooled_dtype(variant):
         # the bf16 tower takes bf16 pooled rows straight from the pool kernel
@@ -366,7 +370,7 @@ def main():
             ms = float(tt.item())
         return ms, prof, h2d, d2h
 
-    runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr,
+    runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
                     pooled_dtype=pooled_dtype(args.variant))
     timed(runner, args.warmup, 0)
     clocks = Clocks(local)
@@ -383,7 +387,7 @@ def main():
     # e2e through the public API with host inputs (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
-        r2 = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr,
+        r2 = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
                     pooled_dtype=pooled_dtype(args.variant))
         r2.t = runner.t
         timed(r2, 2, runner.t, source="host")
@@ -398,7 +402,7 @@ def main():
     # N = 1 (no FWP) and, when there is an All2All to hide, N = 2 (FWP)
     def tower_run(Nv, t0):
         r1 = Runner(ctx, N=Nv, schedule=args.schedule if Nv > 1 else "sequential", pipelined=True,
-                    lr_over_B=lr, pooled_dtype=pooled_dtype("et"))
+                    lr_over_B=lr, adagrad=adagrad, pooled_dtype=pooled_dtype("et"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="et")
         k2 = max(5, args.steps // 2)
@@ -416,7 +420,7 @@ def main():
         return out, r1.t
 
     def embedding_run(Nv, t0):
-        r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr,
+        r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
                     pooled_dtype=pooled_dtype("e"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="e")

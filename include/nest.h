@@ -73,6 +73,9 @@ typedef struct nest_ctx nest_ctx_t;   /* opaque; one per rank */
 enum { NEST_POOL_SUM = 0, NEST_POOL_NONE = 1 };
 enum { NEST_INIT_UNIFORM = 0, NEST_INIT_DYADIC = 1, NEST_INIT_ZERO = 2 };
 enum { NEST_SCHED_SEQUENTIAL = 0, NEST_SCHED_CLUSTERED = 1 };
+/* sparse optimizer of the update: SGD of Eq. 2, or row-wise
+ * AdaGrad (the paper and SPEC leave it open) */
+enum { NEST_OPT_SGD = 0, NEST_OPT_ROWWISE_ADAGRAD = 1 };
 enum { NEST_MAX_WORLD = 64, NEST_MAX_MICRO_BATCHES = 8, NEST_MAX_TABLES = 1024 };
 
 /* Static configuration of one rank.  Capacities bound every per-batch count;
@@ -97,6 +100,8 @@ typedef struct {
   int32_t init_mode;          /* NEST_INIT_UNIFORM (+-1/sqrt(d)), _DYADIC (parity regime P1), _ZERO */
   int32_t tower_layers;       /* stand-in dense tower depth L (0 = no tower) */
   int32_t tower_hidden;       /* tower width (bf16 GEMMs) */
+  int32_t optimizer;          /* NEST_OPT_SGD (default) or NEST_OPT_ROWWISE_ADAGRAD */
+  float adagrad_eps;          /* AdaGrad denominator epsilon (fp32) */
 } nest_config_t;
 
 /* Host-known counts of one slot after nest_route (all per this rank). */
@@ -136,8 +141,9 @@ NEST_API const char* nest_version(void);
  * twice (main + aux communicator) and broadcast the bytes to all ranks. */
 NEST_API nest_status_t nest_get_unique_id(void* uid_out);
 
-/* Bytes of table memory (the shard, fp32 [shard_rows, dim]) and of workspace
- * this configuration needs.  Pure host computation. */
+/* Bytes of table memory (the shard, fp32 [shard_rows, dim], then with
+ * NEST_OPT_ROWWISE_ADAGRAD the fp32 accumulators [shard_rows]) and of
+ * workspace this configuration needs.  Pure host computation. */
 NEST_API nest_status_t nest_workspace_bytes(const nest_config_t* cfg, size_t* table_bytes,
                                    size_t* work_bytes);
 
@@ -233,6 +239,17 @@ NEST_API nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32
                                    const float* dout, float lr_over_B,
                                    void* compute, void* comm);
 
+/* nest_grad_bwd_update for a context created with NEST_OPT_ROWWISE_ADAGRAD:
+ * the same backward, and after the last micro-batch the owner applies, per
+ * owner key with summed gradient G (same (micro-batch, source) order),
+ *   g = grad_scale * G;  m += (1/d) sum_j g_j^2;  e -= lr * g / (sqrt(m) + eps)
+ * with one fp32 accumulator m per shard row (initially 0, kept in table_mem
+ * after the rows).  grad_scale = 1/|B_global|.  NEST_ERR_INVALID on an SGD
+ * context (and nest_grad_bwd_update on an AdaGrad one). */
+NEST_API nest_status_t nest_grad_bwd_update_adagrad(nest_ctx_t* ctx, int32_t slot, int32_t mb,
+                                                    const float* dout, float grad_scale, float lr,
+                                                    void* compute, void* comm);
+
 /* Stand-in dense tower (the FWP overlap partner, not the product):
  * fixed bf16 MLP forward + backward on `stream` via cuBLAS, input = the pooled
  * rows of a micro-batch viewed as [rows/F, F*d]; writes its input gradient
@@ -265,6 +282,11 @@ NEST_API nest_status_t nest_route_view(const nest_ctx_t* ctx, int32_t slot, nest
  * foreign / out-of-range keys give a zero row and raise the sticky error). */
 NEST_API nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out,
                              void* stream);
+
+/* out[i] = AdaGrad accumulator of keys[i]'s shard row (device, n keys owned by
+ * this rank; NEST_ERR_INVALID on an SGD context). */
+NEST_API nest_status_t nest_read_state(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out,
+                                       void* stream);
 
 /* All2All plan of one batch, as nest_route derives it after the count
  * exchange (host-only; exposed so the multi-rank bookkeeping can be tested

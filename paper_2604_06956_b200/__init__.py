@@ -45,6 +45,7 @@ class NestContext:
                  max_batch: int, max_micro_batches: int = 1, max_recv_keys: int = 0,
                  max_mb_rows: int = 0, max_owner_mb_rows: int = 0, seed: int = 0,
                  init_mode: str = "uniform", tower_layers: int = 0, tower_hidden: int = 1024,
+                 optimizer: str = "sgd", adagrad_eps: float = 1e-8,
                  nccl_uids: Optional[bytes] = None, device=None, init_tables: bool = True):
         import torch
         self.lib = L.load()
@@ -59,7 +60,10 @@ class NestContext:
             max_recv_keys=max_recv_keys, max_owner_keys=0, max_mb_rows=max_mb_rows,
             max_owner_mb_rows=max_owner_mb_rows, seed=seed,
             init_mode={"uniform": L.INIT_UNIFORM, "dyadic": L.INIT_DYADIC, "zero": L.INIT_ZERO}[init_mode],
-            tower_layers=tower_layers, tower_hidden=tower_hidden)
+            tower_layers=tower_layers, tower_hidden=tower_hidden,
+            optimizer={"sgd": L.OPT_SGD, "rowwise_adagrad": L.OPT_ROWWISE_ADAGRAD}[optimizer],
+            adagrad_eps=adagrad_eps)
+        self.optimizer = optimizer
         self.world, self.rank, self.dim = world, rank, dim
         self.F = self.cfg.num_features
         tb, wb = C.c_size_t(), C.c_size_t()
@@ -135,6 +139,12 @@ class NestContext:
                                                   _stream(compute),
                                                   _stream(comm if comm is not None else compute)))
 
+    def grad_bwd_update_adagrad(self, slot: int, mb: int, dout, grad_scale: float, lr: float, compute=None,
+                                comm=None) -> None:
+        self._check(self.lib.nest_grad_bwd_update_adagrad(self.ctx, slot, mb, _ptr(dout), float(grad_scale),
+                                                          float(lr), _stream(compute),
+                                                          _stream(comm if comm is not None else compute)))
+
     def tower_fwd_bwd(self, pooled, dout, stream=None) -> None:
         """Stand-in tower on fp32 or bf16 pooled rows (-> nest_tower_fwd_bwd_bf16)."""
         fn = self.lib.nest_tower_fwd_bwd_bf16 if str(pooled.dtype) == "torch.bfloat16" else self.lib.nest_tower_fwd_bwd
@@ -157,6 +167,13 @@ class NestContext:
         out = torch.empty((int(keys.numel()), self.dim), dtype=torch.float32, device=self.device)
         self._check(self.lib.nest_read_rows(self.ctx, _ptr(keys), int(keys.numel()), _ptr(out),
                                             _stream(stream)))
+        return out
+
+    def read_state(self, keys, stream=None):
+        """Row-wise AdaGrad accumulators of owned keys (nest_read_state)."""
+        torch = self.torch
+        out = torch.empty(int(keys.numel()), dtype=torch.float32, device=self.device)
+        self._check(self.lib.nest_read_state(self.ctx, _ptr(keys), int(keys.numel()), _ptr(out), _stream(stream)))
         return out
 
     def profile_enable(self, on: bool = True) -> None:

@@ -17,13 +17,15 @@ STATUS = {0: "NEST_OK", 1: "NEST_ERR_INVALID", 2: "NEST_ERR_CUDA", 3: "NEST_ERR_
 POOL_SUM, POOL_NONE = 0, 1
 INIT_UNIFORM, INIT_DYADIC, INIT_ZERO = 0, 1, 2
 SCHED_SEQUENTIAL, SCHED_CLUSTERED = 0, 1
+OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
 MAX_MICRO_BATCHES = 8
 
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
            "nest_create", "nest_destroy", "nest_init_tables", "nest_fwp_schedule", "nest_route",
            "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_lookup_fwd_bf16",
-           "nest_grad_bwd_update", "nest_tower_fwd_bwd", "nest_tower_fwd_bwd_bf16", "nest_join",
+           "nest_grad_bwd_update", "nest_grad_bwd_update_adagrad", "nest_tower_fwd_bwd",
+           "nest_tower_fwd_bwd_bf16", "nest_join", "nest_read_state",
            "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
            "nest_profile_read", "nest_last_error"]
 PROFILE_STAGES = 16
@@ -43,7 +45,8 @@ class Config(C.Structure):
                 ("max_micro_batches", C.c_int32), ("max_recv_keys", C.c_int64),
                 ("max_owner_keys", C.c_int64), ("max_mb_rows", C.c_int64),
                 ("max_owner_mb_rows", C.c_int64), ("seed", C.c_uint64), ("init_mode", C.c_int32),
-                ("tower_layers", C.c_int32), ("tower_hidden", C.c_int32)]
+                ("tower_layers", C.c_int32), ("tower_hidden", C.c_int32), ("optimizer", C.c_int32),
+                ("adagrad_eps", C.c_float)]
 
 
 class SlotInfo(C.Structure):
@@ -111,12 +114,14 @@ def load() -> C.CDLL:
         "nest_lookup_fwd": ([vp, i32, i32, vp, vp, vp], i32),
         "nest_lookup_fwd_bf16": ([vp, i32, i32, vp, vp, vp], i32),
         "nest_grad_bwd_update": ([vp, i32, i32, vp, f32, vp, vp], i32),
+        "nest_grad_bwd_update_adagrad": ([vp, i32, i32, vp, f32, f32, vp, vp], i32),
         "nest_tower_fwd_bwd": ([vp, vp, i64, vp, vp], i32),
         "nest_tower_fwd_bwd_bf16": ([vp, vp, i64, vp, vp], i32),
         "nest_join": ([vp, vp], i32),
         "nest_slot_info": ([vp, i32, C.POINTER(SlotInfo)], i32),
         "nest_route_view": ([vp, i32, C.POINTER(RouteView)], i32),
         "nest_read_rows": ([vp, vp, i64, vp, vp], i32),
+        "nest_read_state": ([vp, vp, i64, vp, vp], i32),
         "nest_exchange_plan": ([C.POINTER(Config), i32, vp, C.POINTER(ExchangePlan)], i32),
         "nest_profile_enable": ([vp, i32], i32),
         "nest_profile_read": ([vp, C.POINTER(ProfileStage), C.POINTER(ProfileSummary)], i32),

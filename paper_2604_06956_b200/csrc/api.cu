@@ -40,6 +40,10 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
   NEST_CHECK(c.Nmax >= 1 && c.Nmax <= NEST_MAX_MICRO_BATCHES, NEST_ERR_INVALID,
              "max_micro_batches must be in [1, 8]");
   NEST_CHECK(cfg->init_mode >= 0 && cfg->init_mode <= 2, NEST_ERR_INVALID, "bad init_mode");
+  NEST_CHECK(cfg->optimizer == NEST_OPT_SGD || cfg->optimizer == NEST_OPT_ROWWISE_ADAGRAD, NEST_ERR_INVALID,
+             "bad optimizer");
+  NEST_CHECK(cfg->optimizer == NEST_OPT_SGD || cfg->adagrad_eps >= 0.f, NEST_ERR_INVALID,
+             "adagrad_eps must be >= 0");
   c.rows.assign(cfg->table_rows, cfg->table_rows + c.T);
   for (int t = 0; t < c.T; ++t)
     NEST_CHECK(c.rows[t] >= 1 && c.rows[t] <= int64_t(kRowMask), NEST_ERR_INVALID, "bad table_rows");
@@ -297,6 +301,8 @@ nest_status_t nest_workspace_bytes(const nest_config_t* cfg, size_t* table_bytes
     Ctx c;
     derive(c, cfg);
     *table_bytes = size_t(std::max<int64_t>(c.Vo, 1)) * c.D * sizeof(float);
+    if (cfg->optimizer == NEST_OPT_ROWWISE_ADAGRAD)   // + one fp32 accumulator per row
+      *table_bytes += size_t(std::max<int64_t>(c.Vo, 1)) * sizeof(float);
     *work_bytes = layout(c, nullptr);
   });
 }
@@ -323,6 +329,10 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
                    (reinterpret_cast<uintptr_t>(work_mem) & 255) == 0,
                NEST_ERR_INVALID, "memory must be 256-byte aligned");
     c->shard = reinterpret_cast<float*>(table_mem);
+    if (c->cfg.optimizer == NEST_OPT_ROWWISE_ADAGRAD) {
+      c->opt_state = c->shard + std::max<int64_t>(c->Vo, 1) * c->D;
+      NEST_CUDA(cudaMemsetAsync(c->opt_state, 0, sizeof(float) * std::max<int64_t>(c->Vo, 1), S(stream)));
+    }
     layout(*c, reinterpret_cast<char*>(work_mem));
     cudaStream_t st0 = S(stream);
     NEST_CUDA(cudaMemcpyAsync(c->d_rows, c->rows.data(), sizeof(int64_t) * c->T, cudaMemcpyHostToDevice, st0));
@@ -403,7 +413,11 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
 nest_status_t nest_init_tables(nest_ctx_t* ctx, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
-  return guard(c, [&] { launch_init_tables(*c, S(stream)); });
+  return guard(c, [&] {
+    launch_init_tables(*c, S(stream));
+    if (c->opt_state)   // row-wise AdaGrad accumulators start at 0
+      NEST_CUDA(cudaMemsetAsync(c->opt_state, 0, sizeof(float) * std::max<int64_t>(c->Vo, 1), S(stream)));
+  });
 }
 
 nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int32_t* bag_offsets,
@@ -603,11 +617,13 @@ nest_status_t nest_lookup_fwd_bf16(nest_ctx_t* ctx, int32_t slot, int32_t mb, vo
   return lookup_fwd_impl(reinterpret_cast<Ctx*>(ctx), slot, mb, out, true, compute, comm);
 }
 
-nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, const float* dout,
-                                   float lr_over_B, void* compute, void* comm) {
-  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* dout, const OptStep& opt,
+                               void* compute, void* comm) {
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] {
+    NEST_CHECK(opt.kind == c->cfg.optimizer, NEST_ERR_INVALID,
+               "update call does not match the context's optimizer (nest_grad_bwd_update: SGD, "
+               "nest_grad_bwd_update_adagrad: row-wise AdaGrad)");
     Slot& s = slot_of(*c, slot);
     NEST_CHECK(s.routed && !s.updated, NEST_ERR_ORDER, "backward outside the window");
     NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
@@ -616,12 +632,12 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
     Slot& other = c->slot[1 - slot];
     const double row = double(c->D) * sizeof(float);
     if (mb == 0) NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
-    if (c->W == 1 && s.N == 1) {
+    if (c->W == 1 && s.N == 1 && opt.kind == NEST_OPT_SGD) {
       // one rank, one micro-batch: the segment-sum applies Eq. 2 itself
       NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
       {
         ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
-        launch_segsum_sgd(*c, s, dout, lr_over_B, cs);
+        launch_segsum_sgd(*c, s, dout, opt.lr, cs);
         ps.launches = s.info.mb_uniq[0] > 0 ? 7 : 0;
         // N7 + N8 without the gradient-row round trip: gradient rows read +
         // 4 K + frozen rows read + rows written back
@@ -695,10 +711,10 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
         NEST_CUDA(cudaStreamWaitEvent(ms, other.ev_gather, 0));
         {
           ProfScope ps(*c, ST_UPDATE, SK_COMM, ms);
-          launch_reduce_sgd(*c, s, lr_over_B, ms);
+          launch_reduce_sgd(*c, s, opt, ms);
           ps.bytes = upd_fixed;
           ps.dcount = s.n_owner;
-          ps.bpc = 2.0 * row;  // frozen buffer row read + shard write-back
+          ps.bpc = 2.0 * row + (opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 : 0.0);  // + accumulator r/w
         }
         NEST_CUDA(cudaEventRecord(s.ev_update, ms));
         NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
@@ -707,15 +723,29 @@ nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, co
       NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
       {
         ProfScope ps(*c, ST_UPDATE, SK_COMPUTE, cs);
-        launch_reduce_sgd(*c, s, lr_over_B, cs);
+        launch_reduce_sgd(*c, s, opt, cs);
         ps.bytes = upd_fixed;
         ps.dcount = s.n_owner;
-        ps.bpc = 2.0 * row;  // frozen buffer row read + shard write-back
+        ps.bpc = 2.0 * row + (opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 : 0.0);  // + accumulator r/w
       }
       NEST_CUDA(cudaEventRecord(s.ev_update, cs));
     }
     if (mb == s.N - 1) s.updated = true;
   });
+}
+
+nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb, const float* dout,
+                                   float lr_over_B, void* compute, void* comm) {
+  const OptStep opt{NEST_OPT_SGD, lr_over_B, 1.f, 0.f, nullptr};
+  return grad_impl(reinterpret_cast<Ctx*>(ctx), slot, mb, dout, opt, compute, comm);
+}
+
+nest_status_t nest_grad_bwd_update_adagrad(nest_ctx_t* ctx, int32_t slot, int32_t mb, const float* dout,
+                                           float grad_scale, float lr, void* compute, void* comm) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  const OptStep opt{NEST_OPT_ROWWISE_ADAGRAD, lr, grad_scale, c->cfg.adagrad_eps, c->opt_state};
+  return grad_impl(c, slot, mb, dout, opt, compute, comm);
 }
 
 static nest_status_t tower_impl(Ctx* c, const void* pooled, bool bf16, int64_t rows, float* dout, void* stream) {
@@ -778,6 +808,16 @@ nest_status_t nest_read_rows(nest_ctx_t* ctx, const int64_t* keys, int64_t n, fl
   return guard(c, [&] {
     NEST_CHECK(n >= 0 && (n == 0 || (keys && out)), NEST_ERR_INVALID, "bad arguments");
     launch_read_rows(*c, keys, n, out, S(stream));
+  });
+}
+
+nest_status_t nest_read_state(nest_ctx_t* ctx, const int64_t* keys, int64_t n, float* out, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CHECK(c->opt_state != nullptr, NEST_ERR_INVALID, "no optimizer state (SGD context)");
+    NEST_CHECK(n >= 0 && (n == 0 || (keys && out)), NEST_ERR_INVALID, "bad arguments");
+    launch_read_state(*c, keys, n, out, S(stream));
   });
 }
 

@@ -155,7 +155,8 @@ struct Ctx {
   int64_t* d_rows = nullptr;       // [T]
   int64_t* d_seg_base = nullptr;   // [W*T+1]
   int64_t* d_lbase = nullptr;      // [T+1]
-  float* shard = nullptr;          // [Vo][d]
+  float* shard = nullptr;
+  float* opt_state = nullptr;      // [Vo] row-wise AdaGrad accumulators (table_mem after the rows)          // [Vo][d]
   // shared transient workspace
   uint32_t* sbm = nullptr;         // source bitmap [words+1] (W>1; W==1 uses slot obm)
   int32_t* swr = nullptr;          // [words+1]
@@ -495,7 +496,6 @@ void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_row
 // out: fp32 rows, or bf16 rows (pooled sum only) when bf16
 void launch_pool(Ctx& c, Slot& s, int mb, void* out, bool bf16, cudaStream_t st);
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st);
-void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st);
 void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st);
 void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N, int mode,
@@ -534,6 +534,18 @@ struct PeerRows {
   float sgd_lr;
 };
 enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
+// the update's sparse optimizer step: Eq. 2 SGD (e = fma(-lr, G, e), lr =
+// eta/|B|) or row-wise AdaGrad (g = gscale*G; m += mean(g^2);
+// e = fma(-lr/(sqrt(m)+eps), g, e); m in state[shard row])
+struct OptStep {
+  int kind;       // NEST_OPT_SGD / NEST_OPT_ROWWISE_ADAGRAD
+  float lr;
+  float gscale;
+  float eps;
+  float* state;
+};
+void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& opt, cudaStream_t st);
+void launch_read_state(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 enum EarlyPush : int { EP_OFF = 0, EP_CE = 1, EP_SM = 2 };
 int a2a_mode_wanted(int W);
 int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb);

@@ -673,21 +673,26 @@ struct MbBases {
   int64_t v[NEST_MAX_MICRO_BATCHES];
 };
 
+// (the loop trip count is warp-uniform: row-wise AdaGrad reduces sum g^2
+// across the row's lane group with shuffles)
 template <int D, bool W1>
 __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
-    const int32_t* __restrict__ n_dev, int N, int W, float lr, MbBases base,
+    const int32_t* __restrict__ n_dev, int N, int W, const OptStep opt, MbBases base,
     const uint32_t* __restrict__ mask, const int32_t* __restrict__ pos, int64_t pos_stride,
     const int32_t* __restrict__ src_tab, const int64_t* __restrict__ recv,
     const int32_t* __restrict__ sendpos, int64_t sp_stride, const float* __restrict__ rows,
     const int32_t* __restrict__ owner_rows, float* __restrict__ buffer, float* __restrict__ shard) {
   Grp<D> gp;
-  constexpr int VPL = RowGeom<D>::VPL;
+  constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
   const int64_t n = *n_dev;
-  for (int64_t u = gp.g; u < n; u += gp.ng) {
+  const bool ada = opt.kind == NEST_OPT_ROWWISE_ADAGRAD;
+  for (int64_t u = gp.g; __any_sync(0xffffffffu, u < n); u += gp.ng) {
+    const bool act = u < n;
     float4 acc[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (W1) {
+    if (!act) {
+    } else if (W1) {
       const uint32_t m = __ldg(mask + u);
       for (int i = 0; i < N; ++i) {
         if (!((m >> i) & 1u)) continue;
@@ -709,20 +714,45 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
     // the updated row goes to the shard only (write-back): the
     // dual-buffer refresh reads written-back rows from the shard, so the
     // frozen active buffer is never rewritten (one row of traffic less)
-    const int64_t srow = __ldg(owner_rows + u);
+    const int64_t srow = act ? __ldg(owner_rows + u) : 0;
+    float step = opt.lr;   // SGD: e = fma(-lr, G, e)
+    if (ada) {
+      // g = gscale * G; m += mean(g^2) (lane sums in order, then a fixed xor
+      // tree over the group's lanes); step = lr / (sqrt(m) + eps)
+      float sq = 0.f;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        acc[v] = make_float4(opt.gscale * acc[v].x, opt.gscale * acc[v].y, opt.gscale * acc[v].z,
+                             opt.gscale * acc[v].w);
+        sq = __fmaf_rn(acc[v].x, acc[v].x, sq);
+        sq = __fmaf_rn(acc[v].y, acc[v].y, sq);
+        sq = __fmaf_rn(acc[v].z, acc[v].z, sq);
+        sq = __fmaf_rn(acc[v].w, acc[v].w, sq);
+      }
+#pragma unroll
+      for (int o = L / 2; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      float m = 0.f;
+      if (act && gp.l == 0) {
+        m = opt.state[srow] + sq * (1.f / float(D));
+        opt.state[srow] = m;
+      }
+      m = __shfl_sync(0xffffffffu, m, lane_id() - gp.l);
+      step = opt.lr / (sqrtf(m) + opt.eps);
+    }
+    if (!act) continue;
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
       float4 e = ld_f4(buffer + u * D + gp.col(v));
-      e.x = __fmaf_rn(-lr, acc[v].x, e.x);
-      e.y = __fmaf_rn(-lr, acc[v].y, e.y);
-      e.z = __fmaf_rn(-lr, acc[v].z, e.z);
-      e.w = __fmaf_rn(-lr, acc[v].w, e.w);
+      e.x = __fmaf_rn(-step, acc[v].x, e.x);
+      e.y = __fmaf_rn(-step, acc[v].y, e.y);
+      e.z = __fmaf_rn(-step, acc[v].z, e.z);
+      e.w = __fmaf_rn(-step, acc[v].w, e.w);
       st_f4_cs(shard + srow * D + gp.col(v), e);
     }
   }
 }
 
-void launch_reduce_sgd(Ctx& c, Slot& s, float lr, cudaStream_t st) {
+void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& lr, cudaStream_t st) {
   MbBases b{};
   const bool w1 = c.W == 1;
   for (int i = 0; i < s.N; ++i) b.v[i] = w1 ? s.src_base[i] : s.own_base[i];
@@ -867,6 +897,26 @@ __global__ void __launch_bounds__(kRowThreads) k_read_rows(
     const int64_t ld = lbase[t] + int64_t(row / uint64_t(W));
     copy_row<D>(out + i * D, shard + ld * D, gp);
   }
+}
+
+// parity helper: out[i] = row-wise AdaGrad accumulator of keys[i]'s shard row
+__global__ void k_read_state(int64_t n, const int64_t* __restrict__ keys, int T, int W, int rank,
+                             const int64_t* __restrict__ rows, const int64_t* __restrict__ lbase,
+                             const float* __restrict__ state, float* __restrict__ out, int32_t* __restrict__ err) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = uint64_t(keys[i]);
+    const uint64_t t = key >> kRowBits, row = key & kRowMask;
+    const bool ok = t < uint64_t(T) && row < uint64_t(rows[t]) && row % uint64_t(W) == uint64_t(rank);
+    if (!ok) atomicOr(err, kErrShard);
+    out[i] = ok ? state[lbase[t] + int64_t(row / uint64_t(W))] : 0.f;
+  }
+}
+
+void launch_read_state(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  k_read_state<<<blocks_for_rows(n, 256), 256, 0, st>>>(n, keys, c.T, c.W, c.rank, c.d_rows, c.d_lbase,
+                                                        c.opt_state, out, c.d_err);
+  NEST_LAUNCH_CHECK();
 }
 
 void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st) {

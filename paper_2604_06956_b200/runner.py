@@ -62,9 +62,12 @@ class Runner:
     gradient)."""
 
     def __init__(self, ctx: NestContext, N: int = 1, schedule: str = "sequential",
-                 pipelined: bool = True, lr_over_B: float = 2.0 ** -10, pooled_dtype=None):
+                 pipelined: bool = True, lr_over_B: float = 2.0 ** -10, pooled_dtype=None,
+                 adagrad=None):
         self.ctx, self.N, self.schedule, self.pipelined = ctx, N, schedule, pipelined
         self.lr = lr_over_B
+        # row-wise AdaGrad contexts: (grad_scale, lr) of nest_grad_bwd_update_adagrad
+        self.adagrad = adagrad
         # bf16: pooled rows for a bf16 dense consumer (nest_lookup_fwd_bf16)
         self.pooled_dtype = pooled_dtype or torch.float32
         self._hold: List[torch.Tensor] = []
@@ -98,6 +101,12 @@ class Runner:
         self._ev_dense = [torch.cuda.Event() for _ in range(8)]
 
     # -- helpers ---------------------------------------------------------------
+    def _grad(self, slot, mb, dout, cs, ms):
+        if self.adagrad is not None:
+            self.ctx.grad_bwd_update_adagrad(slot, mb, dout, self.adagrad[0], self.adagrad[1], cs, ms)
+        else:
+            self.ctx.grad_bwd_update(slot, mb, dout, self.lr, cs, ms)
+
     def _schedule(self, slot, keys, offs, B, stream):
         perm, mbo = self.ctx.fwp_schedule(keys, offs, B, self.N, self.schedule, stream=stream)
         self.sched[slot] = (perm, mbo)
@@ -158,7 +167,7 @@ class Runner:
                 nk, no, nB = next_batch
                 self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
                 self._route(p, nk, no, nB, self.aux)      # host blocks for counts here
-            ctx.grad_bwd_update(a, i, dout, self.lr, cs, ms)
+            self._grad(a, i, dout, cs, ms)
         if self.pipelined and next_batch is not None:
             ctx.dbp_refresh(a, p, cs)
         self.t += 1
@@ -183,7 +192,7 @@ class Runner:
                 nk, no, nB = next_batch
                 self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
                 self._route(p, nk, no, nB, self.aux)
-            ctx.grad_bwd_update(a, i, dout, self.lr, cs, ms)
+            self._grad(a, i, dout, cs, ms)
             if i + 1 < self.N:
                 ctx.lookup_fwd(a, i + 1, outs[i + 1], cs, ms)
         if self.pipelined and next_batch is not None:

@@ -47,15 +47,17 @@ def skewed_batches(cfg, B, T, world, seed=31):
     return out
 
 
-def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=None):
+def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=None, adagrad=None):
     F, d = cfg.num_features, cfg.dim
     batches = gen(cfg, B, T, world) if gen else \
         [[WL.gen_batch(cfg, 21, t, r, batch=B) for r in range(world)] for t in range(T)]
     douts = [[WL.gen_dout(21, t, r, B * F, d, dmode) for r in range(world)] for t in range(T)]
     K = max(1, max(len(b[rank][0]) for b in batches))
     ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, max_keys=K, max_batch=B,
-                      max_micro_batches=N, seed=13, init_mode=init, nccl_uids=uids, device=dev)
-    run = Runner(ctx, N=N, pipelined=True, lr_over_B=lr)
+                      max_micro_batches=N, seed=13, init_mode=init, nccl_uids=uids, device=dev,
+                      optimizer="rowwise_adagrad" if adagrad else "sgd",
+                      adagrad_eps=adagrad[2] if adagrad else 1e-8)
+    run = Runner(ctx, N=N, pipelined=True, lr_over_B=lr, adagrad=adagrad[:2] if adagrad else None)
     mine = [(torch.from_numpy(b[rank][0]).to(dev), torch.from_numpy(b[rank][1]).to(dev), B) for b in batches]
     cap = B // N
     pooled = []
@@ -75,8 +77,9 @@ def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=No
     ok = True
     if rank == 0:
         tab = OS.LazyTable(13, d, init)
+        opt = OS.RowwiseAdagrad(lr=adagrad[1], grad_scale=adagrad[0], eps=adagrad[2]) if adagrad else None
         for t in range(T):
-            res = OS.sync_step(tab, batches[t], douts[t], lr)
+            res = OS.sync_step(tab, batches[t], douts[t], lr, optimizer=opt)
             for r in range(world):
                 g = gathered[r][0][t]
                 good = np.array_equal(g, res.pooled[r]) if dmode == "dyadic" else rel_ok(g, res.pooled[r])
@@ -143,12 +146,17 @@ def main():
     # (name, cfg, B, N, T, init, dout mode, lr, batch generator)
     cases.append(("edge-owner0-empty-P1-N2", WL.CONFIGS["tiny"].with_(bag_repeats=True, table_rows=(4000, 800, 64, 9)),
                   64, 2, 5, "dyadic", "dyadic", 2.0 ** -10, skewed_batches))
+    # row-wise AdaGrad (NEXT-2): (grad_scale, lr, eps), P2 tolerance
+    cases.append(("adagrad-P2-N2", WL.CONFIGS["tiny"].with_(table_rows=(3000, 700, 90, 20), zipf=1.2,
+                                                            bag_repeats=True, dim=32),
+                  128, 2, 4, "uniform", "realistic", 0.0, None, (1.0 / 256, 0.05, 1e-8)))
     all_ok = True
     for case in cases:
         obj = [unique_ids() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         gen = case[8] if len(case) > 8 else None
-        all_ok &= run_case(*case[:8], rank, world, dev, obj[0], gen=gen)
+        ada = case[9] if len(case) > 9 else None
+        all_ok &= run_case(*case[:8], rank, world, dev, obj[0], gen=gen, adagrad=ada)
     dist.barrier(device_ids=[local])
     dist.destroy_process_group()
     if rank == 0:

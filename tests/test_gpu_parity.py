@@ -98,6 +98,56 @@ def test_route_mid_size_radix_tiles_and_ragged_tail():
     assert np.array_equal(v["pos"].astype(np.int64), rs.pos)
 
 
+# --------------------------------------------------------------------------- row-wise AdaGrad
+@pytest.mark.parametrize("N,pipelined", [(1, True), (2, True), (1, False)])
+def test_train_w1_rowwise_adagrad_vs_oracle(N, pipelined):
+    """NEXT-2: the update with row-wise AdaGrad (tables and accumulators after
+    T steps) against oracle.step.RowwiseAdagrad, 1e-5 row-wise (P2)."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(5000, 3000, 200, 77), zipf=1.3, bag_repeats=True, dim=32)
+    B, T, F, d, seed = 256, 5, cfg.num_features, cfg.dim, 7
+    batches = [[WL.gen_batch(cfg, seed, t, 0, batch=B)] for t in range(T)]
+    douts = [[WL.gen_dout(seed, t, 0, B * F, d, "realistic")] for t in range(T)]
+    K = max(len(b[0][0]) for b in batches)
+    gs, lr, eps = 1.0 / B, 0.05, 1e-8
+    ctx = make_ctx(cfg, B, N=N, K=K, init="uniform", seed=11, optimizer="rowwise_adagrad", adagrad_eps=eps)
+    run = Runner(ctx, N=N, pipelined=pipelined, adagrad=(gs, lr))
+    dev_b = [(to_dev(b[0][0], torch.int64), to_dev(b[0][1], torch.int32), B) for b in batches]
+    cap = B // N
+    for t in range(T):
+        dd = to_dev(douts[t][0], torch.float32)
+        run.step(dev_b[t], dev_b[t + 1] if t + 1 < T else None,
+                 lambda tt, i, p, dd=dd: dd[i * cap * F:(i + 1) * cap * F])
+    run.join()
+    torch.cuda.synchronize()
+    tab = OS.LazyTable(11, d, "uniform")
+    opt = OS.RowwiseAdagrad(lr=lr, grad_scale=gs, eps=eps)
+    for t in range(T):
+        OS.sync_step(tab, batches[t], douts[t], 0.0, optimizer=opt)
+    allk = np.unique(np.concatenate([b[0][0] for b in batches]))
+    kd = to_dev(allk, torch.int64)
+    assert rel_rowwise_ok(ctx.read_rows(kd).cpu().numpy(), tab.get(allk))
+    m = ctx.read_state(kd).cpu().numpy().astype(np.float64)
+    ref_m = opt.get_state(allk)
+    assert np.all(np.abs(m - ref_m) <= 1e-5 * ref_m + 1e-30)
+    assert (ref_m > 0).all()
+
+
+def test_rowwise_adagrad_errors():
+    cfg = WL.CONFIGS["tiny"]
+    sgd = make_ctx(cfg, 32)
+    with pytest.raises(NestError):
+        sgd.read_state(to_dev(np.array([0], np.int64), torch.int64))
+    ada = make_ctx(cfg, 32, optimizer="rowwise_adagrad")
+    keys, offs = WL.gen_batch(cfg, 1, 0, 0, batch=32)
+    ada.route(0, to_dev(keys, torch.int64), to_dev(offs, torch.int32), 32)
+    out = torch.empty((32 * cfg.num_features, cfg.dim), dtype=torch.float32, device=DEV)
+    ada.lookup_fwd(0, 0, out)
+    with pytest.raises(NestError):
+        ada.grad_bwd_update(0, 0, out, 0.1)          # SGD call on an AdaGrad context
+    ada.grad_bwd_update_adagrad(0, 0, out, 1 / 32, 0.1)
+    torch.cuda.synchronize()
+
+
 # --------------------------------------------------------------------------- bf16 hand-off
 def test_lookup_bf16_and_tower_bf16_input_match_fp32_path():
     """nest_lookup_fwd_bf16 == bf16(RN) of nest_lookup_fwd bit for bit, and the
