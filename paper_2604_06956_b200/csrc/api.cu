@@ -632,17 +632,18 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
     Slot& other = c->slot[1 - slot];
     const double row = double(c->D) * sizeof(float);
     if (mb == 0) NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
-    if (c->W == 1 && s.N == 1 && opt.kind == NEST_OPT_SGD) {
+    if (c->W == 1 && s.N == 1) {
       // one rank, one micro-batch: the segment-sum applies Eq. 2 itself
       NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
       {
         ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
-        launch_segsum_sgd(*c, s, dout, opt.lr, cs);
+        launch_segsum_sgd(*c, s, dout, opt, cs);
         ps.launches = s.info.mb_uniq[0] > 0 ? 7 : 0;
         // N7 + N8 without the gradient-row round trip: gradient rows read +
         // 4 K + frozen rows read + rows written back
         ps.bytes = row * double(s.info.mb_out_rows[0]) + 4.0 * double(s.info.mb_nnz[0]) +
-                   2.0 * row * double(s.info.mb_uniq[0]);
+                   2.0 * row * double(s.info.mb_uniq[0]) +
+                   (opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 * double(s.info.mb_uniq[0]) : 0.0);
       }
       NEST_CUDA(cudaEventRecord(s.ev_update, cs));
       s.updated = true;

@@ -532,6 +532,11 @@ struct PeerRows {
   const int32_t* sgd_rows;
   float* sgd_shard;
   float sgd_lr;
+  // ... or row-wise AdaGrad (ada != 0): g = gscale*G, m += mean(g^2) in
+  // state[shard row], shard row = fma(-lr/(sqrt(m)+eps), g, buffer[k])
+  int32_t ada;
+  float ada_gscale, ada_eps;
+  float* ada_state;
 };
 enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
 // the update's sparse optimizer step: Eq. 2 SGD (e = fma(-lr, G, e), lr =
@@ -545,6 +550,7 @@ struct OptStep {
   float* state;
 };
 void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& opt, cudaStream_t st);
+void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, cudaStream_t st);
 void launch_read_state(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 enum EarlyPush : int { EP_OFF = 0, EP_CE = 1, EP_SM = 2 };
 int a2a_mode_wanted(int W);
@@ -555,7 +561,6 @@ void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st);
 // every requester of micro-batch mb of slot p (early push)
 void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st);
 void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st);
-void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, float lr, cudaStream_t st);
 void xfer_signal(Ctx& c, Slot& s, int kind, int mb, cudaStream_t st);
 // copy-engine transport (xfer.cu)
 bool xfer_wanted(int W);

@@ -373,6 +373,47 @@ __device__ __forceinline__ void put_grad(const PeerRows& m, int64_t k, int D, in
 
 // IL cold segments per lane group at once (k, k + ng, ...), two rows of each
 // in flight per pass, each segment summed in occurrence order
+// fused one-rank update of key k's gradient row with row-wise AdaGrad: every
+// lane of the row's group calls it (converged), `valid` marks a real row
+template <int D>
+__device__ __forceinline__ void put_row_adagrad(const PeerRows& m, int64_t k, bool valid,
+                                                float4 (&acc)[RowGeom<D>::VPL], int l) {
+  constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
+  const int lane = lane_id();
+  const uint32_t gmask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane - l));
+  float sq = 0.f;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    acc[v] = make_float4(m.ada_gscale * acc[v].x, m.ada_gscale * acc[v].y, m.ada_gscale * acc[v].z,
+                         m.ada_gscale * acc[v].w);
+    sq = __fmaf_rn(acc[v].x, acc[v].x, sq);
+    sq = __fmaf_rn(acc[v].y, acc[v].y, sq);
+    sq = __fmaf_rn(acc[v].z, acc[v].z, sq);
+    sq = __fmaf_rn(acc[v].w, acc[v].w, sq);
+  }
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) sq += __shfl_xor_sync(gmask, sq, o);
+  const int64_t srow = valid ? __ldg(m.sgd_rows + k) : 0;
+  float mm = 0.f;
+  if (valid && l == 0) {
+    mm = m.ada_state[srow] + sq * (1.f / float(D));
+    m.ada_state[srow] = mm;
+  }
+  mm = __shfl_sync(gmask, mm, lane - l);
+  if (!valid) return;
+  const float step = m.sgd_lr / (sqrtf(mm) + m.ada_eps);
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const int col = (v * L + l) * 4;
+    float4 e = ldg_f4(m.sgd_buffer + k * D + col);
+    e.x = __fmaf_rn(-step, acc[v].x, e.x);
+    e.y = __fmaf_rn(-step, acc[v].y, e.y);
+    e.z = __fmaf_rn(-step, acc[v].z, e.z);
+    e.w = __fmaf_rn(-step, acc[v].w, e.w);
+    st_f4_cs(m.sgd_shard + srow * D + col, e);
+  }
+}
+
 template <int D, int IL>
 __global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_segsum_cold(int64_t Ui, int chunk,
                                                              const int32_t* __restrict__ seg_start,
@@ -381,7 +422,8 @@ __global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_segsum_c
                                                              const PeerRows out) {
   Grp<D> gp;
   constexpr int VPL = RowGeom<D>::VPL;
-  for (int64_t k0 = gp.g; k0 < Ui; k0 += IL * gp.ng) {
+  // warp-uniform trip count (the AdaGrad row reduction shuffles)
+  for (int64_t k0 = gp.g; __any_sync(0xffffffffu, k0 < Ui); k0 += IL * gp.ng) {
     int a[IL], b[IL];
     int len = 0;
 #pragma unroll
@@ -425,9 +467,13 @@ __global__ void __launch_bounds__(kRowThreads, ilp_min_blocks<D>(IL)) k_segsum_c
 #pragma unroll
     for (int i = 0; i < IL; ++i) {
       const int64_t k = k0 + i * gp.ng;
-      if (k < Ui && b[i] >= a[i])
+      const bool valid = k < Ui && b[i] >= a[i];
+      if (out.ada) {
+        put_row_adagrad<D>(out, k, valid, acc[i], gp.l);
+      } else if (valid) {
 #pragma unroll
         for (int v = 0; v < VPL; ++v) put_grad(out, k, D, gp.col(v), acc[i][v]);
+      }
     }
   }
   if (out.fence) __threadfence_system();
@@ -483,11 +529,18 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
     for (int v = 0; v < G::VPL; ++v) red[grp][v * G::L + l] = acc[v];
     __syncthreads();
     if (grp == 0) {
+      float4 row[G::VPL];
 #pragma unroll
       for (int v = 0; v < G::VPL; ++v) {
         float4 s = red[0][v * G::L + l];
         for (int q = 1; q < NG; ++q) s = f4add(s, red[q][v * G::L + l]);
-        put_grad(out, k, D, (v * G::L + l) * 4, s);
+        row[v] = s;
+      }
+      if (out.ada) {
+        put_row_adagrad<D>(out, k, true, row, l);
+      } else {
+#pragma unroll
+        for (int v = 0; v < G::VPL; ++v) put_grad(out, k, D, (v * G::L + l) * 4, row[v]);
       }
     }
     __syncthreads();
@@ -509,7 +562,7 @@ void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) 
 // R10 + R12 fused for W == 1, N == 1: each key's gradient is its only
 // contribution, so the segment-sum applies the SGD update and writes the row
 // back directly (no gradient rows stored and re-read)
-void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, float lr, cudaStream_t st) {
+void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, cudaStream_t st) {
   PeerRows out{};
   out.base[0] = c.src_rows;
   out.off[0] = 0;
@@ -518,7 +571,11 @@ void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, float lr, cudaStream_
   out.sgd_buffer = s.buffer;
   out.sgd_rows = s.owner_rows;
   out.sgd_shard = c.shard;
-  out.sgd_lr = lr;
+  out.sgd_lr = opt.lr;
+  out.ada = opt.kind == NEST_OPT_ROWWISE_ADAGRAD;
+  out.ada_gscale = opt.gscale;
+  out.ada_eps = opt.eps;
+  out.ada_state = opt.state;
   launch_segsum_to(c, s, 0, dout, out, st);
 }
 
