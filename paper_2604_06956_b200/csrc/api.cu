@@ -143,7 +143,10 @@ static size_t layout(Ctx& c, char* base) {
     c.cl_boff = w.take<int32_t>(B * c.F + 1);
     c.cl_Scnt = w.take<int32_t>(Nm * B);
     c.cl_kstart = w.take<int32_t>(K + 2);
-    c.cl_newk = w.take<uint64_t>(K + K / 128 + 64);
+    // work items per round: fresh (key, group) pairs <= K (keys of the taken
+    // samples) plus chunk extras <= N * K / 128 (a key fresh for every group)
+    c.cl_newk_cap = K + Nm * (K / 128 + 1) + 64;
+    c.cl_newk = w.take<uint64_t>(c.cl_newk_cap);
   }
   for (int si = 0; si < 2; ++si) {
     Slot& s = c.slot[si];

@@ -174,7 +174,7 @@ __global__ void k_cl_S_full(int B, int F, int N, const int32_t* __restrict__ bag
 // every group's candidate keys (bins ck >> lo), warp-aggregated.
 __global__ void k_cl_rank(int B, int N, int lo, const int32_t* __restrict__ S, const int32_t* __restrict__ grp,
                           const int32_t* __restrict__ size, const int32_t* __restrict__ maxsz,
-                          uint32_t* __restrict__ ck, int32_t* __restrict__ hist) {
+                          uint32_t* __restrict__ ck, int32_t* __restrict__ hist, int32_t* __restrict__ err) {
   const int smax = *maxsz;
   const uint32_t nb = uint32_t(smax) + 1;
   const uint32_t lt = lanemask_lt();
@@ -190,6 +190,11 @@ __global__ void k_cl_rank(int B, int N, int lo, const int32_t* __restrict__ S, c
           const int v = S[int64_t(g) * B + s];
           key = uint32_t(smax - v) * nb + uint32_t(sz - v);
           bin = int(key >> lo);
+          if (v < 0 || v > sz || bin >= kClHistBins) {   // S out of [0, size]: a bug, never an index
+            atomicOr(err, kErrCluster);
+            key = kTaken;
+            bin = -1;
+          }
         }
         ck[int64_t(g) * B + s] = key;
       }
@@ -219,7 +224,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* ws, int& total) {
 }
 
 // smallest bin b with cumsum(hist[0..b]) >= k; returns b and the count before b
+// (out[0] = -1 when the histogram holds fewer than k entries)
 __device__ void find_bin(const int* hist, int nbins, int k, int* ws, int* out) {
+  if (threadIdx.x == 0) out[0] = -1;
   // each thread owns a contiguous run of bins
   const int per = (nbins + kSelThreads - 1) / kSelThreads;
   const int b0 = threadIdx.x * per;
@@ -248,13 +255,22 @@ __device__ void find_bin(const int* hist, int nbins, int k, int* ws, int* out) {
 // inside the chosen bin; then every block of kClIds ids counts its ties and
 // assigns.  A sample taken by g leaves the later groups' histograms and keys.
 // sel[g]: {T, kk, partial, b1, kk1}
-__global__ void __launch_bounds__(kSelThreads) k_cl_find1(int k, int nb1, int lo, const int32_t* __restrict__ hist,
+// level-1 bins of the rank keys: (smax+1)^2 keys, or kClHistBins bins of
+// ck >> lo (smax is the batch's, read on the device: the captured round
+// sequence is replayed for every batch of the same (B, N, lo))
+__device__ __forceinline__ int cl_nb1(const int32_t* maxsz, int lo) {
+  const int nb = *maxsz + 1;
+  return lo ? kClHistBins : nb * nb;
+}
+
+__global__ void __launch_bounds__(kSelThreads) k_cl_find1(int k, const int32_t* __restrict__ maxsz, int lo,
+                                                          const int32_t* __restrict__ hist,
                                                           int32_t* __restrict__ sel) {
   __shared__ int ws[33];
   __shared__ int out[2];
-  find_bin(hist, nb1, k, ws, out);
+  find_bin(hist, cl_nb1(maxsz, lo), k, ws, out);
   if (threadIdx.x == 0) {
-    const int b1 = out[0], kk1 = k - out[1];
+    const int b1 = max(out[0], 0), kk1 = out[0] < 0 ? 0 : k - out[1];
     sel[3] = b1;
     sel[4] = kk1;
     if (lo == 0) {
@@ -283,47 +299,51 @@ struct Thr {
   bool partial;
 };
 __device__ Thr cl_resolve(int k, int nb1, int lo, const int32_t* hist1, const int32_t* hist2,
-                          const int32_t* sel, int* ws, int* out) {
+                          const int32_t* sel, int* ws, int* out, int32_t* err) {
   Thr t;
-  if (lo == 0) {
-    find_bin(hist1, nb1, k, ws, out);
-    t.T = uint32_t(out[0]);
-    t.kk = k - out[1];
-    t.partial = t.kk < hist1[out[0]];
-  } else {
-    const int kk1 = sel[4];
-    find_bin(hist2, 1 << lo, kk1, ws, out);
-    t.T = (uint32_t(sel[3]) << lo) | uint32_t(out[0]);
-    t.kk = kk1 - out[1];
-    t.partial = t.kk < hist2[out[0]];
+  const int32_t* h = lo == 0 ? hist1 : hist2;
+  const int kk0 = lo == 0 ? k : sel[4];
+  find_bin(h, lo == 0 ? nb1 : 1 << lo, kk0, ws, out);
+  if (out[0] < 0) {   // fewer candidates than the admission size: a bug, never an index
+    if (threadIdx.x == 0) atomicOr(err, kErrCluster);
+    t.T = 0;
+    t.kk = 0;
+    t.partial = true;
+    return t;
   }
+  t.T = lo == 0 ? uint32_t(out[0]) : (uint32_t(sel[3]) << lo) | uint32_t(out[0]);
+  t.kk = kk0 - out[1];
+  t.partial = t.kk < h[out[0]];
   return t;
 }
 
 // ties of T per block of kClIds ids (only when the tie bin is taken partly)
-__global__ void __launch_bounds__(kClIds) k_cl_tiecount(int B, int k, int nb1, int lo,
+__global__ void __launch_bounds__(kClIds) k_cl_tiecount(int B, int k, const int32_t* __restrict__ maxsz, int lo,
                                                         const uint32_t* __restrict__ ckg,
                                                         const int32_t* __restrict__ hist1,
                                                         const int32_t* __restrict__ hist2,
-                                                        const int32_t* __restrict__ sel, int32_t* __restrict__ bcnt) {
+                                                        const int32_t* __restrict__ sel, int32_t* __restrict__ bcnt,
+                                                        int32_t* __restrict__ err) {
   __shared__ int ws[33];
   __shared__ int out[2];
-  const Thr t = cl_resolve(k, nb1, lo, hist1, hist2, sel, ws, out);
+  const Thr t = cl_resolve(k, cl_nb1(maxsz, lo), lo, hist1, hist2, sel, ws, out, err);
   if (!t.partial) return;
   const int s = blockIdx.x * kClIds + threadIdx.x;
   const int n = __syncthreads_count(s < B && ckg[s] == t.T);
   if (threadIdx.x == 0) bcnt[blockIdx.x] = n;
 }
 
-__global__ void __launch_bounds__(kClIds) k_cl_assign(int B, int N, int g, int k, int nb1, int lo, uint32_t* ck,
+__global__ void __launch_bounds__(kClIds) k_cl_assign(int B, int N, int g, int k, const int32_t* __restrict__ maxsz,
+                                                      int lo, uint32_t* ck,
                                                       const int32_t* __restrict__ sel, int32_t* hist,
                                                       const int32_t* __restrict__ hist2,
                                                       const int32_t* __restrict__ bcnt, int32_t* __restrict__ grp,
-                                                      int32_t* __restrict__ newlist, int32_t* __restrict__ nnew) {
+                                                      int32_t* __restrict__ newlist, int32_t* __restrict__ nnew,
+                                                      int32_t* __restrict__ err) {
   __shared__ int ws[33];
   __shared__ int out[2];
   // (hist rows g2 > g change below, row g does not: every block resolves alike)
-  const Thr t = cl_resolve(k, nb1, lo, hist + g * kClHistBins, hist2, sel, ws, out);
+  const Thr t = cl_resolve(k, cl_nb1(maxsz, lo), lo, hist + g * kClHistBins, hist2, sel, ws, out, err);
   const uint32_t T = t.T;
   const int kk = t.kk;
   const bool partial = t.partial;
@@ -365,7 +385,7 @@ __global__ void k_cl_update(int F, const int32_t* __restrict__ newlist, const in
                             const int32_t* __restrict__ bag_off, const int32_t* __restrict__ cl_u,
                             const int32_t* __restrict__ grp, uint32_t* __restrict__ inmask,
                             const int32_t* __restrict__ kstart, uint64_t* __restrict__ newk,
-                            int32_t* __restrict__ nnewk) {
+                            int32_t* __restrict__ nnewk, int64_t ncap, int32_t* __restrict__ err) {
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt();
   const int n = *nnew;
@@ -386,6 +406,10 @@ __global__ void k_cl_update(int F, const int32_t* __restrict__ newlist, const in
       int at = 0;
       if (lane == 0 && tot) at = atomicAdd(nnewk, tot);
       at = __shfl_sync(0xffffffffu, at, 0) + inc - nch;
+      if (nch && at + nch > ncap) {
+        atomicOr(err, kErrCluster);
+        continue;
+      }
       for (int ch = 0; ch < nch; ++ch)
         newk[at + ch] = (uint64_t(uint32_t(u)) << 32) | (uint64_t(ch) << 3) | uint64_t(g);
     }
@@ -394,19 +418,24 @@ __global__ void k_cl_update(int F, const int32_t* __restrict__ newlist, const in
 
 // S[g][s] += 1 for every unassigned sample s holding a key that joined
 // union(g) this round (warp per work item: a chunk of the key's occurrences)
-__global__ void k_cl_spread(int B, const uint64_t* __restrict__ newk, const int32_t* __restrict__ nnewk,
+__global__ void k_cl_spread(int B, int64_t ncap, int64_t kcap, const uint64_t* __restrict__ newk,
+                            const int32_t* __restrict__ nnewk,
                             const int32_t* __restrict__ kstart, const uint32_t* __restrict__ sk,
                             const int32_t* __restrict__ sv, const int32_t* __restrict__ cl_u,
                             const int32_t* __restrict__ samp, const int32_t* __restrict__ grp,
-                            int32_t* __restrict__ S) {
+                            int32_t* __restrict__ S, int32_t* __restrict__ err) {
   const int lane = lane_id();
-  const int n = *nnewk;
+  const int n = int(min(int64_t(*nnewk), ncap));
   const int64_t nw = int64_t(gridDim.x) * blockDim.x / 32;
   for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; i < n; i += nw) {
     const uint64_t e = newk[i];
     const uint32_t u = uint32_t(e >> 32), g = uint32_t(e) & 7u, ch = uint32_t(e) >> 3;
     const int q0 = kstart[u] + int(ch) * kSpreadChunk;
     const int q1 = min(q0 + kSpreadChunk, kstart[u + 1]);
+    if (u >= kcap || q0 < 0 || q1 > kcap) {   // a bug, never an index
+      if (lane == 0) atomicOr(err, kErrCluster);
+      continue;
+    }
     for (int q = q0 + lane; q < q1; q += 32) {
       const int32_t j = sv[q];
       if (cl_u[j] < 0) continue;   // not the sample's first occurrence of u
@@ -430,7 +459,7 @@ __global__ void __launch_bounds__(kClIds) k_cl_gcount(int B, int N, const int32_
 
 __global__ void __launch_bounds__(kClIds) k_cl_perm(int B, int N, const int32_t* __restrict__ grp,
                                                     const int32_t* __restrict__ bcnt, int32_t* __restrict__ perm,
-                                                    int32_t* __restrict__ mbo) {
+                                                    int32_t* __restrict__ mbo, int32_t* __restrict__ err) {
   __shared__ int ws[33];
   const int cap = B / N;
   const int s = blockIdx.x * kClIds + threadIdx.x;
@@ -442,13 +471,15 @@ __global__ void __launch_bounds__(kClIds) k_cl_perm(int B, int N, const int32_t*
     block_excl_scan(part, ws, base);
     int tot;
     const int r = block_excl_scan(gs == g ? 1 : 0, ws, tot);
-    if (gs == g) perm[g * cap + base + r] = s;
+    if (gs == g) {
+      if (base + r < cap) perm[g * cap + base + r] = s;
+      else atomicOr(err, kErrCluster);   // a group over its capacity: a bug, never an index
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x <= N) mbo[threadIdx.x] = threadIdx.x * cap;
 }
 
-static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int nb1, int32_t* maxsz, int32_t* nnew,
-                           cudaStream_t st);
+static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int32_t* maxsz, int32_t* nnew, cudaStream_t st);
 
 void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N,
                     int32_t* perm, int32_t* mb_offsets, cudaStream_t st) {
@@ -502,7 +533,6 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
   int nbits = 0;
   while ((1u << nbits) < nkeys) ++nbits;
   const int lo = nbits > kClHistLog ? nbits - kClHistLog : 0;
-  const int nb1 = lo ? kClHistBins : int(nkeys);
   // rounds: admission sizes are a function of (B, N) only, every buffer is the
   // library's, so the whole round sequence is captured once per (B, N, lo)
   // into a CUDA graph and replayed (it is ~37 rounds of 3N + 4 launches)
@@ -510,10 +540,10 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
   const auto gkey = std::make_tuple(B, N, lo);
   auto git = c.cl_graphs.find(gkey);
   if (st == nullptr) {
-    cluster_rounds(c, B, N, F, lo, nb1, maxsz, nnew, st);   // legacy stream: no capture
+    cluster_rounds(c, B, N, F, lo, maxsz, nnew, st);   // legacy stream: no capture
   } else if (git == c.cl_graphs.end()) {
     NEST_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    cluster_rounds(c, B, N, F, lo, nb1, maxsz, nnew, st);
+    cluster_rounds(c, B, N, F, lo, maxsz, nnew, st);
     cudaGraph_t graph = nullptr;
     NEST_CUDA(cudaStreamEndCapture(st, &graph));
     cudaGraphExec_t exec = nullptr;
@@ -524,13 +554,12 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
   if (st != nullptr) NEST_CUDA(cudaGraphLaunch(git->second, st));
   const int nblk = (B + kClIds - 1) / kClIds;
   k_cl_gcount<<<nblk, kClIds, 0, st>>>(B, N, c.cl_grp, c.cl_bcnt);
-  k_cl_perm<<<nblk, kClIds, 0, st>>>(B, N, c.cl_grp, c.cl_bcnt, perm, mb_offsets);
+  k_cl_perm<<<nblk, kClIds, 0, st>>>(B, N, c.cl_grp, c.cl_bcnt, perm, mb_offsets, c.d_err);
   NEST_LAUNCH_CHECK();
 }
 
 // the admission rounds on library buffers only (captured into a graph)
-static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int nb1, int32_t* maxsz, int32_t* nnew,
-                           cudaStream_t st) {
+static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int32_t* maxsz, int32_t* nnew, cudaStream_t st) {
   int32_t* nnewk = reinterpret_cast<int32_t*>(c.cl_small + 3);
   const int32_t* bag_offsets = c.cl_boff;
   auto grid = [](int64_t n, int t) {
@@ -555,25 +584,28 @@ static void cluster_rounds(Ctx& c, int B, int N, int F, int lo, int nb1, int32_t
     }
     NEST_CUDA(cudaMemsetAsync(c.cl_hist, 0, sizeof(int32_t) * kClHistBins * N, st));
     NEST_CUDA(cudaMemsetAsync(nnew, 0, sizeof(int32_t), st));
-    k_cl_rank<<<grid(B, 256), 256, 0, st>>>(B, N, lo, c.cl_Scnt, c.cl_grp, c.cl_size, maxsz, ck, c.cl_hist);
+    k_cl_rank<<<grid(B, 256), 256, 0, st>>>(B, N, lo, c.cl_Scnt, c.cl_grp, c.cl_size, maxsz, ck, c.cl_hist,
+                                            c.d_err);
     for (int g = 0; g < N; ++g) {
       if (take[g] <= 0) continue;
       int32_t* sel = c.cl_sel + 8 * g;
       const int32_t* h1 = c.cl_hist + int64_t(g) * kClHistBins;
       if (lo) {
-        k_cl_find1<<<1, kSelThreads, 0, st>>>(take[g], nb1, lo, h1, sel);
+        k_cl_find1<<<1, kSelThreads, 0, st>>>(take[g], maxsz, lo, h1, sel);
         NEST_CUDA(cudaMemsetAsync(hist2, 0, sizeof(int32_t) << lo, st));
         k_cl_hist2<<<grid(B, 256), 256, 0, st>>>(B, lo, ck + int64_t(g) * B, sel, hist2);
       }
-      k_cl_tiecount<<<nblk, kClIds, 0, st>>>(B, take[g], nb1, lo, ck + int64_t(g) * B, h1, hist2, sel, c.cl_bcnt);
-      k_cl_assign<<<nblk, kClIds, 0, st>>>(B, N, g, take[g], nb1, lo, ck, sel, c.cl_hist, hist2, c.cl_bcnt,
-                                           c.cl_grp, c.cl_new, nnew);
+      k_cl_tiecount<<<nblk, kClIds, 0, st>>>(B, take[g], maxsz, lo, ck + int64_t(g) * B, h1, hist2, sel, c.cl_bcnt,
+                                             c.d_err);
+      k_cl_assign<<<nblk, kClIds, 0, st>>>(B, N, g, take[g], maxsz, lo, ck, sel, c.cl_hist, hist2, c.cl_bcnt,
+                                           c.cl_grp, c.cl_new, nnew, c.d_err);
     }
     NEST_CUDA(cudaMemsetAsync(nnewk, 0, sizeof(int32_t), st));
     k_cl_update<<<grid(int64_t(B) * 32, 256), 256, 0, st>>>(F, c.cl_new, nnew, bag_offsets, c.cl_u, c.cl_grp,
-                                                           c.cl_inmask, c.cl_kstart, c.cl_newk, nnewk);
-    k_cl_spread<<<148 * 8, 256, 0, st>>>(B, c.cl_newk, nnewk, c.cl_kstart, c.cl_sk, c.cl_sv, c.cl_u,
-                                         c.cl_samp, c.cl_grp, c.cl_Scnt);
+                                                           c.cl_inmask, c.cl_kstart, c.cl_newk, nnewk,
+                                                           c.cl_newk_cap, c.d_err);
+    k_cl_spread<<<148 * 8, 256, 0, st>>>(B, c.cl_newk_cap, c.Kcap, c.cl_newk, nnewk, c.cl_kstart, c.cl_sk, c.cl_sv,
+                                         c.cl_u, c.cl_samp, c.cl_grp, c.cl_Scnt, c.d_err);
   }
   NEST_LAUNCH_CHECK();
 }

@@ -53,7 +53,7 @@ struct Error {
 #define NEST_LAUNCH_CHECK() NEST_CUDA(cudaGetLastError())
 
 // device error bits (OR-ed into ctx->d_err)
-enum : int32_t { kErrKeyRange = 1, kErrShard = 2, kErrSampleSize = 4 };
+enum : int32_t { kErrKeyRange = 1, kErrShard = 2, kErrSampleSize = 4, kErrCluster = 8 };
 
 constexpr int kRowBits = 40;
 constexpr uint64_t kRowMask = (uint64_t(1) << kRowBits) - 1;
@@ -200,7 +200,8 @@ struct Ctx {
   int32_t* cl_boff = nullptr;      // [Bcap*F+1] library copy of the batch's bag offsets (graph input)
   int32_t* cl_Scnt = nullptr;      // [Nmax][Bcap] S = |keys(s) & union(g)|, maintained incrementally
   int32_t* cl_kstart = nullptr;    // [Kcap+1] first position of each key id in the key-sorted occurrences
-  uint64_t* cl_newk = nullptr;     // [Kcap + Kcap/128 + 64] (key id, chunk, group) spread work items
+  uint64_t* cl_newk = nullptr;     // [cl_newk_cap] (key id, chunk, group) spread work items
+  int64_t cl_newk_cap = 0;         // per round: <= K pairs + N*K/128 chunk extras
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> cl_graphs;  // (B, N, lo) -> captured rounds
   Slot slot[2];
   uint32_t epoch = 0;

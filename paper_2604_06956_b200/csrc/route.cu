@@ -573,6 +573,7 @@ void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t
   if (err & kErrShard) throw Error{NEST_ERR_SHARD, "owner received a key it does not own"};
   if (err & kErrSampleSize)
     throw Error{NEST_ERR_CAPACITY, "clustered schedule: a sample has more than 16383 distinct keys"};
+  if (err & kErrCluster) throw Error{NEST_ERR_CAPACITY, "clustered schedule: an internal bound was exceeded"};
   for (int r = 0; r < W; ++r) {
     int64_t recv = 0, mbrows = 0, mbrecv = 0;
     for (int o = 0; o < W; ++o) {

@@ -8,11 +8,14 @@ run() { # tag args...
   echo "$tag rc=$?"
 }
 for p in 0.2 0.45 0.7; do run dbp_p$p --config dbp_stress --reuse $p --variant e; done
-for z in 0.8 1.0 1.2 1.4; do
+for z in 0.8 1.05 1.4; do
   run fwp_z${z}_n1 --zipf $z --micro-batches 1
   for N in 2 4; do for S in sequential clustered; do run fwp_z${z}_n${N}_$S --zipf $z --micro-batches $N --schedule $S; done; done
 done
 for S in sequential clustered; do run corr_n4_$S --correlated 64,0.5 --micro-batches 4 --schedule $S; done
+# generative-rec sequence feature (unpooled, embedding-only), W=2 and W=1
+run genrec_w2 --config genrec --steps 10
+CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --config genrec --steps 10 --warmup 3 --no-e2e --no-fwp-compare --no-cpu-baseline > gpurun_out/sw_genrec_w1.log 2>&1; echo "genrec_w1 rc=$?"
 python - <<'PY' > gpurun_out/sweep_summary.txt
 import json,glob
 print("| run | samples/s (M) | ms/step | a2a physical ms | a2a exposed ms | exposed ratio | alpha (sum_i U_i / U) | schedule ms | refresh ms | I / U_o | tower ms |")

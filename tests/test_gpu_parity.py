@@ -307,13 +307,16 @@ def test_cluster_bit_exact_vs_oracle(case):
 
 def test_cluster_repeated_batches_same_shape():
     """The captured round sequence is replayed for later batches of the same
-    shape: every batch still matches the oracle."""
+    shape, including batches whose largest sample (smax, hence the number of
+    rank-key bins) differs: every batch still matches the oracle."""
     cfg = WL.CONFIGS["tiny"].with_(table_rows=(3000,) * 4)
+    long = cfg.with_(bag_len=(5, 8), bag_repeats=True)
     B, N = 512, 4
-    ctx = make_ctx(cfg, B, N=N, K=B * cfg.num_features * cfg.bag_len[1])
+    ctx = make_ctx(cfg, B, N=N, K=B * cfg.num_features * long.bag_len[1])
     side = torch.cuda.Stream()   # a non-legacy stream: the rounds are captured and replayed
-    for t in range(3):
-        keys, offs = WL.gen_correlated_batch(cfg, 9, t, 0, groups=8, rho=0.6, batch=B)
+    for t in range(4):
+        gen_cfg = cfg if t % 2 == 0 else long
+        keys, offs = WL.gen_correlated_batch(gen_cfg, 9, t, 0, groups=8, rho=0.6, batch=B)
         kd, od = to_dev(keys, torch.int64), to_dev(offs, torch.int32)
         side.wait_stream(torch.cuda.current_stream())
         perm, mbo = ctx.fwp_schedule(kd, od, B, N, "clustered", stream=side)
