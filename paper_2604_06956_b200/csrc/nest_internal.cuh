@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>

@@ -60,6 +60,18 @@ static int row_ilp() {
     default: { constexpr int IL = 1; __VA_ARGS__; } break;               \
   }
 
+// rows in flight per lane group in the streaming kernels: NEST_STREAM_U = 4 (default) or 8
+static int stream_u() {
+  static const int v = [] {
+    const char* e = std::getenv("NEST_STREAM_U");
+    return e && std::atoi(e) == 8 ? 8 : 4;
+  }();
+  return v;
+}
+#define NEST_DISPATCH_U(...)                                             \
+  if (stream_u() == 8) { constexpr int SU = 8; __VA_ARGS__; }            \
+  else { constexpr int SU = 4; __VA_ARGS__; }
+
 // resident blocks to ask of ptxas for a kernel holding IL row vectors per lane
 // group in flight: full occupancy (32 registers) for one float4 per lane
 template <int D>
@@ -258,6 +270,103 @@ __global__ void __launch_bounds__(kRowThreads) k_expand_rows(int nsamp, int F,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Streaming forms of R8 and R10 (default).  A lane group owns a run of
+// consecutive items (the occurrences of one sample's bags / a fixed range of
+// sorted occurrences): it loads the run's indices with one coalesced load per
+// L items, then streams the rows with U loads in flight, flushing a bag /
+// segment when the next item belongs to the next one.  The index chain is paid
+// once per L items instead of once per bag, and every row load of a batch is
+// independent.  Summation order is unchanged for pooling (left to right from
+// 0) and fixed for the segment-sum (see k_segsum_range).
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ uint32_t group_mask(const Grp<D>& gp) {
+  constexpr int L = RowGeom<D>::L;
+  return L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (lane_id() - gp.l));
+}
+
+// R8, pooled: lane group per sample of the micro-batch; bags of a sample are
+// contiguous in the batch's CSR, so the sample's occurrences are one run
+template <int D, bool W1, int U, typename OutT>
+__global__ void __launch_bounds__(kRowThreads) k_pool_stream(int64_t nsamp, int F,
+                                                             const int32_t* __restrict__ perm_mb,
+                                                             const int32_t* __restrict__ bag_off,
+                                                             const int32_t* __restrict__ inverse,
+                                                             const int32_t* __restrict__ pos,
+                                                             const float* __restrict__ src,
+                                                             OutT* __restrict__ out) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
+  const uint32_t gm = group_mask<D>(gp);
+  for (int64_t p = gp.g; p < nsamp; p += gp.ng) {
+    const int64_t bag0 = int64_t(__ldg(perm_mb + p)) * F;
+    OutT* orow = out + p * F * D;
+    int fb = 0;   // first bag of the window of bag ends the lanes hold
+    int be = gp.l < F ? __ldg(bag_off + bag0 + gp.l + 1) : INT_MAX;
+    const int j0 = __ldg(bag_off + bag0), j1 = __ldg(bag_off + bag0 + F);
+    int f = 0;
+    int cur_end = __shfl_sync(gm, be, 0, L);
+    float4 acc[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = j0; c0 < j1; c0 += L) {
+      const int n = min(L, j1 - c0);
+      int r_l = 0;
+      if (gp.l < n) {
+        const int u = __ldg(inverse + c0 + gp.l);
+        r_l = W1 ? u : __ldg(pos + u);
+      }
+      for (int t0 = 0; t0 < n; t0 += U) {
+        float4 x[U][VPL];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int r = __shfl_sync(gm, r_l, (t0 + k) & (L - 1), L);
+          if (t0 + k < n)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) x[k][v] = ldg_f4(src + int64_t(r) * D + gp.col(v));
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          if (t0 + k >= n) break;
+          const int j = c0 + t0 + k;
+          while (j >= cur_end) {   // bag f is complete (empty bags flush zeros)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              st_out4_cs(orow + int64_t(f) * D + gp.col(v), acc[v]);
+              acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            ++f;
+            if (f - fb >= L) {
+              fb += L;
+              be = fb + gp.l < F ? __ldg(bag_off + bag0 + fb + gp.l + 1) : INT_MAX;
+            }
+            cur_end = __shfl_sync(gm, be, f - fb, L);
+          }
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], x[k][v]);
+        }
+      }
+    }
+    for (; f < F; ++f)   // the last bag, then trailing empty bags
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        st_out4_cs(orow + int64_t(f) * D + gp.col(v), acc[v]);
+        acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+  }
+}
+
+// pooling form: NEST_POOL = stream (default: k_pool_stream, lane group per
+// sample) or bag (k_pool, lane group per bag, the r01 kernel)
+static bool pool_by_bag() {
+  static const bool v = [] {
+    const char* e = std::getenv("NEST_POOL");
+    return e && std::string(e) == "bag";
+  }();
+  return v;
+}
+
 void launch_pool(Ctx& c, Slot& s, int mb, void* out_v, bool bf16, cudaStream_t st) {
   float* out = reinterpret_cast<float*>(out_v);
   __nv_bfloat16* out_h = reinterpret_cast<__nv_bfloat16*>(out_v);
@@ -267,7 +376,25 @@ void launch_pool(Ctx& c, Slot& s, int mb, void* out_v, bool bf16, cudaStream_t s
   const int32_t* perm_mb = s.perm + int64_t(mb) * s.cap;
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    if (c.cfg.pooling == NEST_POOL_SUM) {
+    if (c.cfg.pooling == NEST_POOL_SUM && !pool_by_bag()) {
+      NEST_DISPATCH_U({
+        if (bf16) {
+          if (w1)
+            k_pool_stream<D, true, SU><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
+                s.cap, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out_h);
+          else
+            k_pool_stream<D, false, SU><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
+                s.cap, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out_h);
+        } else {
+          if (w1)
+            k_pool_stream<D, true, SU><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
+                s.cap, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+          else
+            k_pool_stream<D, false, SU><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
+                s.cap, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
+        }
+      });
+    } else if (c.cfg.pooling == NEST_POOL_SUM) {
       const int64_t nrows = int64_t(s.cap) * c.F;
       const int grid = emb_blocks(nrows, rpb);
       if (bf16) {
@@ -548,6 +675,269 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
   if (out.fence) __threadfence_system();
 }
 
+// R10 over fixed ranges of kSegRange sorted occurrences: range w = [w*R, w*R+R).
+// A segment (key) that starts and ends inside a range is summed in occurrence
+// order and finished there (stored, or with the fused update applied).  A
+// segment cut by range boundaries leaves partial rows: B[w] for its part in the
+// range where it starts, A[w'] for its part in each later range; the range
+// where it starts lists itself, and k_segsum_fix sums B[w] + A[w+1] + ... in
+// range order.  Fixed ranges => a fixed summation order => bitwise
+// reproducible, whatever the grid; load balance does not depend on skew.
+constexpr int kSegRange = 256;
+
+template <int D>
+__device__ __forceinline__ void finish_row(const PeerRows& out, int64_t k, float4 (&acc)[RowGeom<D>::VPL],
+                                           const Grp<D>& gp) {
+  if (out.ada) {
+    put_row_adagrad<D>(out, k, true, acc, gp.l);
+  } else {
+#pragma unroll
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) put_grad(out, k, D, gp.col(v), acc[v]);
+  }
+}
+
+// a finished segment: fused update with the prefetched frozen row (PRE), or
+// the store / AdaGrad of finish_row
+template <int D, bool PRE>
+__device__ __forceinline__ void seg_finish(const PeerRows& out, int32_t k, int32_t srow,
+                                           const float4 (&ecur)[RowGeom<D>::VPL], float4 (&g)[RowGeom<D>::VPL],
+                                           const Grp<D>& gp) {
+  if (PRE) {
+#pragma unroll
+    for (int v = 0; v < RowGeom<D>::VPL; ++v) {
+      float4 e = ecur[v];
+      e.x = __fmaf_rn(-out.sgd_lr, g[v].x, e.x);
+      e.y = __fmaf_rn(-out.sgd_lr, g[v].y, e.y);
+      e.z = __fmaf_rn(-out.sgd_lr, g[v].z, e.z);
+      e.w = __fmaf_rn(-out.sgd_lr, g[v].w, e.w);
+      st_f4_cs(out.sgd_shard + int64_t(srow) * D + gp.col(v), e);
+    }
+  } else {
+    finish_row<D>(out, k, g, gp);
+  }
+}
+
+// PRE: fused SGD (W == 1, N == 1, plain SGD) with the frozen rows prefetched
+// alongside the gradient row of the segment's first occurrence
+template <int D, int U, bool PRE>
+__global__ void __launch_bounds__(kRowThreads) k_segsum_range(int64_t Ki, const uint32_t* __restrict__ skey,
+                                                              uint32_t umask, const int32_t* __restrict__ pos,
+                                                              const int32_t* __restrict__ sval,
+                                                              const float* __restrict__ dout, const PeerRows out,
+                                                              float* __restrict__ partial,
+                                                              int32_t* __restrict__ olist,
+                                                              int32_t* __restrict__ ocount) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
+  const uint32_t gm = group_mask<D>(gp);
+  const int64_t nr = (Ki + kSegRange - 1) / kSegRange;
+  for (int64_t w = gp.g; w < nr; w += gp.ng) {
+    const int64_t q0 = w * kSegRange, q1 = (q0 + kSegRange < Ki ? q0 + kSegRange : Ki);
+    const uint32_t ufirst = __ldg(skey + q0) & umask;
+    const bool carry_in = q0 > 0 && (__ldg(skey + q0 - 1) & umask) == ufirst;
+    const bool carry_out = q1 < Ki && (__ldg(skey + q1) & umask) == (__ldg(skey + q1 - 1) & umask);
+    bool open = carry_in, part_a = carry_in;   // segment open; it started before q0
+    int32_t kcur = 0, srow = 0;
+    uint32_t uprev = carry_in ? ufirst : 0xffffffffu;
+    float4 acc[VPL], ecur[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = ecur[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t c0 = q0; c0 < q1; c0 += L) {
+      const int n = int(q1 - c0 < L ? q1 - c0 : L);
+      uint32_t u_l = 0xfffffffeu;
+      int32_t r_l = 0, k_l = 0, s_l = 0;
+      if (gp.l < n) {
+        u_l = __ldg(skey + c0 + gp.l) & umask;
+        r_l = __ldg(sval + c0 + gp.l);
+      }
+      uint32_t up = __shfl_up_sync(gm, u_l, 1, L);
+      if (gp.l == 0) up = uprev;
+      const bool head = gp.l < n && u_l != up;
+      if (head) {
+        k_l = __ldg(pos + u_l);
+        if (PRE) s_l = __ldg(out.sgd_rows + k_l);
+      }
+      const uint32_t heads = __ballot_sync(gm, head) >> (lane_id() - gp.l);
+      uprev = __shfl_sync(gm, u_l, n - 1, L);
+      for (int t0 = 0; t0 < n; t0 += U) {
+        float4 x[U][VPL], ex[U][VPL];
+        int32_t kk[U], ss[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int t = t0 + k, sl = t & (L - 1);
+          const int32_t r = __shfl_sync(gm, r_l, sl, L);
+          kk[k] = __shfl_sync(gm, k_l, sl, L);
+          ss[k] = PRE ? __shfl_sync(gm, s_l, sl, L) : 0;
+          if (t < n) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) x[k][v] = ldg_f4(dout + int64_t(r) * D + gp.col(v));
+            if (PRE && ((heads >> t) & 1u))
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) ex[k][v] = ldg_f4(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v));
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int t = t0 + k;
+          if (t >= n) break;
+          if ((heads >> t) & 1u) {
+            if (open) {   // the previous segment ends here
+              if (part_a) {
+#pragma unroll
+                for (int v = 0; v < VPL; ++v) st_f4(partial + w * D + gp.col(v), acc[v]);
+              } else {
+                seg_finish<D, PRE>(out, kcur, srow, ecur, acc, gp);
+              }
+            }
+            open = true;
+            part_a = false;
+            kcur = kk[k];
+            srow = ss[k];
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              if (PRE) ecur[v] = ex[k][v];
+              acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], x[k][v]);
+        }
+      }
+    }
+    // the segment open at the range end
+    if (carry_out || part_a) {
+      float* dst = partial + (part_a ? w : nr + w) * D;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) st_f4(dst + gp.col(v), acc[v]);
+      if (carry_out && !part_a && gp.l == 0) olist[atomicAdd(ocount, 1)] = int32_t(w);
+    } else {
+      seg_finish<D, PRE>(out, kcur, srow, ecur, acc, gp);
+    }
+  }
+  if (out.fence) __threadfence_system();
+}
+
+// last range of the segment that starts in range w and continues past it
+__device__ __forceinline__ int64_t seg_last_range(int64_t Ki, const uint32_t* __restrict__ skey, uint32_t umask,
+                                                  int64_t w, uint32_t u) {
+  const int64_t nr = (Ki + kSegRange - 1) / kSegRange;
+  auto through = [&](int64_t r) {   // the segment continues past range r
+    return r + 1 < nr && (__ldg(skey + (r + 1) * kSegRange) & umask) == u;
+  };
+  // through(w) holds (w's carry-out); the last range is the first r > w without it
+  int64_t lo = w, hi = w + 1, step = 1;
+  while (hi < nr - 1 && through(hi)) {
+    lo = hi;
+    step <<= 1;
+    hi = min(lo + step, nr - 1);
+  }
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (through(mid)) lo = mid; else hi = mid;
+  }
+  return hi;
+}
+
+constexpr int kFixWarpMax = 64;   // partials a lane group sums itself; more go to k_segsum_fix_big
+
+// cut segments: B[w] + A[w+1] + ... + A[wb] in range order
+template <int D, int U>
+__global__ void __launch_bounds__(kRowThreads) k_segsum_fix(int64_t Ki, const uint32_t* __restrict__ skey,
+                                                            uint32_t umask, const int32_t* __restrict__ pos,
+                                                            const int32_t* __restrict__ olist,
+                                                            const int32_t* __restrict__ ocount,
+                                                            const float* __restrict__ partial, const PeerRows out,
+                                                            int32_t* __restrict__ big, int32_t* __restrict__ nbig) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL;
+  const int64_t nr = (Ki + kSegRange - 1) / kSegRange;
+  const int n = *ocount;
+  for (int64_t e = gp.g; e < n; e += gp.ng) {
+    const int64_t w = olist[e];
+    const int64_t q1 = ((w + 1) * kSegRange < Ki ? (w + 1) * kSegRange : Ki);
+    const uint32_t u = __ldg(skey + q1 - 1) & umask;
+    const int64_t wb = seg_last_range(Ki, skey, umask, w, u);
+    const int32_t k = __ldg(pos + u);
+    if (wb - w + 1 > kFixWarpMax) {
+      if (gp.l == 0) {
+        const int b = atomicAdd(nbig, 1);
+        big[3 * b] = int32_t(w);
+        big[3 * b + 1] = int32_t(wb);
+        big[3 * b + 2] = k;
+      }
+      continue;
+    }
+    float4 acc[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc[v] = ld_f4(partial + (nr + w) * D + gp.col(v));
+    for (int64_t r = w + 1; r <= wb; r += U) {
+      float4 x[U][VPL];
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+        if (r + i <= wb)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) x[i][v] = ld_f4(partial + (r + i) * D + gp.col(v));
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+        if (r + i <= wb)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], x[i][v]);
+    }
+    finish_row<D>(out, k, acc, gp);
+  }
+  if (out.fence) __threadfence_system();
+}
+
+// cut segments with more than kFixWarpMax partials: one block each, groups
+// sum strided partials (p = 0: B[w], p >= 1: A[w+p]), then a fixed sequential
+// combine of the group sums
+template <int D>
+__global__ void __launch_bounds__(kRowThreads) k_segsum_fix_big(int64_t Ki, const int32_t* __restrict__ big,
+                                                                const int32_t* __restrict__ nbig,
+                                                                const float* __restrict__ partial, const PeerRows out) {
+  using G = RowGeom<D>;
+  constexpr int NG = (kRowThreads / 32) * G::GPW;
+  __shared__ float4 red[NG][G::kVec];
+  const int64_t nr = (Ki + kSegRange - 1) / kSegRange;
+  const int lane = lane_id();
+  const int grp = (threadIdx.x >> 5) * G::GPW + lane / G::L;
+  const int l = lane % G::L;
+  const int nb = *nbig;
+  for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t w = big[3 * b], wb = big[3 * b + 1];
+    const int32_t k = big[3 * b + 2];
+    const int64_t np = wb - w + 1;
+    float4 acc[G::VPL];
+#pragma unroll
+    for (int v = 0; v < G::VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t m = grp; m < np; m += NG) {
+      const int64_t prow = m == 0 ? nr + w : w + m;
+#pragma unroll
+      for (int v = 0; v < G::VPL; ++v) acc[v] = f4add(acc[v], ld_f4(partial + prow * D + (v * G::L + l) * 4));
+    }
+#pragma unroll
+    for (int v = 0; v < G::VPL; ++v) red[grp][v * G::L + l] = acc[v];
+    __syncthreads();
+    if (grp == 0) {
+      float4 row[G::VPL];
+#pragma unroll
+      for (int v = 0; v < G::VPL; ++v) {
+        float4 s = red[0][v * G::L + l];
+        for (int q = 1; q < NG; ++q) s = f4add(s, red[q][v * G::L + l]);
+        row[v] = s;
+      }
+      if (out.ada) {
+        put_row_adagrad<D>(out, k, true, row, l);
+      } else {
+#pragma unroll
+        for (int v = 0; v < G::VPL; ++v) put_grad(out, k, D, (v * G::L + l) * 4, row[v]);
+      }
+    }
+    __syncthreads();
+  }
+  if (out.fence) __threadfence_system();
+}
+
 // local gradient rows of micro-batch mb (NCCL / CE transports send them)
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st) {
   PeerRows out{};
@@ -679,6 +1069,15 @@ void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st) {
   NEST_LAUNCH_CHECK();
 }
 
+// segment-sum form: NEST_SEGSUM = range (default: k_segsum_range + fix-ups) or
+// chunks (cold lane groups + hot chunk partials, the r01 kernels)
+static bool segsum_chunks() {
+  static const bool v = [] {
+    const char* e = std::getenv("NEST_SEGSUM");
+    return e && std::string(e) == "chunks";
+  }();
+  return v;
+}
 void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st) {
   const int64_t Ui = s.info.mb_uniq[mb];
   const int64_t Ki = s.info.mb_nnz[mb];
@@ -687,6 +1086,28 @@ void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows
   const int32_t* sval = s.sval + s.q0[mb];
   const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
   const uint32_t umask = (1u << s.ubits) - 1u;
+  if (!segsum_chunks()) {
+    // counters: seg_tot[0] = cut segments listed, seg_tot[1] = big ones
+    NEST_CUDA(cudaMemsetAsync(c.seg_tot, 0, 2 * sizeof(int32_t), st));
+    const int64_t nr = (Ki + kSegRange - 1) / kSegRange;
+    const bool pre = out.sgd_shard && !out.ada;
+    NEST_DISPATCH_D(c.D, {
+      const int gpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+      NEST_DISPATCH_U({
+        if (pre)
+          k_segsum_range<D, SU, true><<<emb_blocks(nr, gpb), kRowThreads, 0, st>>>(
+              Ki, skey, umask, pos, sval, dout, out, c.partial, c.hot_list, c.seg_tot);
+        else
+          k_segsum_range<D, SU, false><<<emb_blocks(nr, gpb), kRowThreads, 0, st>>>(
+              Ki, skey, umask, pos, sval, dout, out, c.partial, c.hot_list, c.seg_tot);
+      });
+      k_segsum_fix<D, 4><<<blocks_for_rows(nr / 4 + 1, gpb, 148 * 2), kRowThreads, 0, st>>>(
+          Ki, skey, umask, pos, c.hot_list, c.seg_tot, c.partial, out, c.seg_aux, c.seg_tot + 1);
+      k_segsum_fix_big<D><<<148, kRowThreads, 0, st>>>(Ki, c.seg_aux, c.seg_tot + 1, c.partial, out);
+    });
+    NEST_LAUNCH_CHECK();
+    return;
+  }
   int32_t* seg = c.seg_start;
   k_seg_heads<<<emb_blocks(Ki, 256), 256, 0, st>>>(Ki, skey, umask, pos, seg, Ui);
   // hot-segment bookkeeping: (is_hot, chunks) prefix -> hot_list, hot_ppos

@@ -113,10 +113,12 @@ def test_train_w1_rowwise_adagrad_vs_oracle(N, pipelined):
     run = Runner(ctx, N=N, pipelined=pipelined, adagrad=(gs, lr))
     dev_b = [(to_dev(b[0][0], torch.int64), to_dev(b[0][1], torch.int32), B) for b in batches]
     cap = B // N
+    # every step's dout stays referenced until the end: the library reads it
+    # asynchronously on its own streams (the caller owns input lifetimes)
+    dds = [to_dev(douts[t][0], torch.float32) for t in range(T)]
     for t in range(T):
-        dd = to_dev(douts[t][0], torch.float32)
         run.step(dev_b[t], dev_b[t + 1] if t + 1 < T else None,
-                 lambda tt, i, p, dd=dd: dd[i * cap * F:(i + 1) * cap * F])
+                 lambda tt, i, p, dd=dds[t]: dd[i * cap * F:(i + 1) * cap * F])
     run.join()
     torch.cuda.synchronize()
     tab = OS.LazyTable(11, d, "uniform")
@@ -409,6 +411,27 @@ def test_edge_single_key_everywhere_hot():
     _p1_check(cfg, [(keys, offs), (keys[::-1].copy(), offs)], N=4)
 
 
+@pytest.mark.parametrize("d,N", [(16, 1), (128, 1), (128, 2)])
+def test_edge_segments_cut_by_ranges_and_giant_segment(d, N):
+    """The segment-sum works on fixed ranges of 256 sorted occurrences: one key
+    with ~80K occurrences (hundreds of ranges: the block fix-up), keys of a few
+    hundred occurrences (the lane-group fix-up), and many short keys cut by a
+    range boundary.  N = 1 runs the fused update (frozen rows prefetched)."""
+    cfg = WL.CONFIGS["tiny"].with_(dim=d, bag_repeats=True)
+    F, B, L = cfg.num_features, 4096, 10
+    rng = np.random.default_rng(7)
+    offs = (np.arange(B * F + 1, dtype=np.int64) * L).astype(np.int32)
+    K = B * F * L
+    rows = rng.integers(0, 1000, size=K)
+    tabs = rng.integers(0, 4, size=K)
+    keys = (tabs.astype(np.int64) << 40) | rows
+    keys[rng.random(K) < 0.5] = (1 << 40) | 17            # the giant segment
+    keys[rng.random(K) < 0.02] = (2 << 40) | 3             # ~3K occurrences
+    keys[rng.random(K) < 0.002] = (3 << 40) | 999          # ~330 occurrences
+    keys2 = keys[::-1].copy()
+    _p1_check(cfg, [(keys, offs), (keys2, offs)], N=N, lr=2.0 ** -12)
+
+
 # --------------------------------------------------------------------------- errors
 def test_error_paths():
     cfg = WL.CONFIGS["tiny"]
@@ -467,12 +490,14 @@ def test_genrec_full_tables_unpooled_sampled():
     ctx.close()
 
 
-def test_dlrm_full_size_w1_sampled():
-    """BASELINE configs[1] at W=1 (the bench launch configuration): routing
-    invariants at full size, sampled pooled rows and sampled updated rows
+@pytest.mark.parametrize("N", [1, 4])
+def test_dlrm_full_size_w1_sampled(N):
+    """BASELINE configs[1] at W=1 (N = 1 is the bench launch configuration:
+    fused segment-sum + update): routing invariants at full size, sampled
+    pooled rows and sampled updated rows -- the hottest keys included --
     computed one by one by the oracle."""
     cfg = WL.CONFIGS["dlrm"]
-    B, N, F, d = cfg.batch_local, 4, cfg.num_features, cfg.dim
+    B, F, d = cfg.batch_local, cfg.num_features, cfg.dim
     keys, offs = WL.gen_batch(cfg, 0, 0, 0)
     ctx = NestContext(cfg.table_rows, d, max_keys=len(keys), max_batch=B, max_micro_batches=N,
                       seed=5, init_mode="uniform", device=DEV)
@@ -499,10 +524,14 @@ def test_dlrm_full_size_w1_sampled():
     # sampled updated rows: e' = e0 - s * sum of the bag grads of its occurrences
     dnp = dout_all.cpu().numpy().astype(np.float64)
     bag_of = np.repeat(np.arange(B * F), np.diff(offs))
-    sample = rng.choice(np.unique(keys), size=64, replace=False)
+    uk, cnt = np.unique(keys, return_counts=True)
+    sample = np.concatenate([uk[np.argsort(-cnt)[:8]], rng.choice(uk, size=64, replace=False)])
     got = ctx.read_rows(to_dev(sample, torch.int64)).cpu().numpy()
-    for k, row in zip(sample, got):
-        occ = np.nonzero(keys == k)[0]
+    order = np.argsort(keys, kind="stable")
+    starts = np.searchsorted(keys[order], sample)
+    for k, row, s0 in zip(sample, got, starts):
+        occ = order[s0:s0 + cnt[np.searchsorted(uk, k)]]
+        assert (keys[occ] == k).all()
         g = dnp[bag_of[occ]].sum(axis=0)
         ref = OS.sgd_rows(OPRF.init_rows(5, np.array([k]), d), g[None], 0.5)[0]
         scale = np.abs(dnp[bag_of[occ]]).sum(axis=0) * 0.5 + np.abs(ref)
