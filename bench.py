@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--batches", type=int, default=3, help="distinct batches cycled per rank")
     ap.add_argument("--optimizer", default="sgd", choices=["sgd", "rowwise_adagrad"],
                     help="sparse update: SGD of Eq. 2 (default) or row-wise AdaGrad (SURVEY NEXT-2)")
+    ap.add_argument("--tables", default="hbm", choices=["hbm", "host"],
+                    help="table tier: HBM (default) or pinned host DRAM over PCIe (SURVEY NEXT-3)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -221,7 +223,9 @@ def config_json(args, cfg, world):
                     "fixed seeded loss gradient of the pooled rows (N(0, 1e-2))",
             "parallelism": f"tables row-sharded over {world} GPU(s), data-parallel samples",
             "l2": "inputs larger than L2 (tables 4*rows*dim bytes, GB-scale per-step traffic)",
-            "pipelined": "DBP (route t+1 on aux stream) + FWP (comm/compute streams)"}
+            "pipelined": "DBP (route t+1 on aux stream) + FWP (comm/compute streams)",
+            "tables_in": "HBM" if getattr(args, "tables", "hbm") == "hbm" else
+                         "pinned host DRAM (retrieval / refresh / write-back over PCIe)"}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -284,7 +288,8 @@ def main():
                       tower_hidden=cfg.tower_hidden, nccl_uids=uids, device=dev, optimizer=args.optimizer,
                       max_recv_keys=int(1.5 * U) + 1024 if world > 1 else U + 1024,
                       max_mb_rows=mb_rows,
-                      max_owner_mb_rows=int(1.5 * mb_rows) if world > 1 else 0)
+                      max_owner_mb_rows=int(1.5 * mb_rows) if world > 1 else 0,
+                      table_location=args.tables)
     torch.cuda.synchronize()
     # inputs resident in HBM (value) and pinned host copies (e2e)
     dev_b = [(torch.from_numpy(k).to(dev), torch.from_numpy(o).to(dev), B) for k, o in batches]
@@ -432,6 +437,41 @@ def main():
                 "roofline": roofline_from(st1, f"{cfg.name}/W{world}/N{Nv}"),
                 "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in st1.items() if v["records"]}}
 
+    # host-DRAM tier (NEXT-3): the retrieval's PCIe rate against the measured
+    # pinned H2D copy, and the step with DBP off (route + retrieval inline)
+    host_tier = None
+    if args.tables == "host":
+        hsrc = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        ddst = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+        ddst.copy_(hsrc, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(4):
+            ddst.copy_(hsrc, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        h2d_peak = 4 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9
+        del hsrc, ddst
+        row = d * 4
+        g = prof["stages"]["gather"]
+        rname_h = "emb_repush" if prof["stages"]["emb_repush"]["records"] else "refresh"
+        rf = prof["stages"][rname_h]
+        seq = Runner(ctx, N=N, schedule=args.schedule, pipelined=False, lr_over_B=lr, adagrad=adagrad,
+                     pooled_dtype=pooled_dtype(args.variant))
+        seq.t = runner.t + 4
+        timed(seq, 2, seq.t)
+        ms_seq, _, _, _ = timed(seq, max(5, args.steps // 2), seq.t)
+        host_tier = {"pcie_h2d_copy_gbs": h2d_peak,
+                     "retrieval_gbs": g["units"] * row / (g["ms"] * 1e6) if g["ms"] else None,
+                     "retrieval_frac_of_h2d_copy": (g["units"] * row / (g["ms"] * 1e6)) / h2d_peak if g["ms"] else None,
+                     "retrieval_ms_per_step": g["ms"] / args.steps,
+                     "refresh_ms_per_step": rf["ms"] / args.steps,
+                     "pcie_h2d_bytes_per_step": (g["units"] + rf["units"]) * row / args.steps,
+                     "pcie_d2h_bytes_per_step": g["units"] * row / args.steps,
+                     "ms_per_step_dbp": ms / args.steps,
+                     "ms_per_step_sequential": ms_seq / max(5, args.steps // 2)}
+
     with_tower_runs, embedding_only = None, None
     if not args.no_fwp_compare:
         tnext = runner.t + args.steps + 8
@@ -511,6 +551,8 @@ def main():
                                                if st["gather"]["units"] else None)},
                 "fwp": dict(fwp_stats, with_tower=with_tower_runs),
                 "embedding_only": embedding_only}
+        if host_tier is not None:
+            line["host_tier"] = host_tier
         if args.trace:
             json.dump({"stages": st, "summary": summ}, open(args.trace, "w"), indent=1)
         print(json.dumps(line), flush=True)

@@ -76,6 +76,8 @@ enum { NEST_SCHED_SEQUENTIAL = 0, NEST_SCHED_CLUSTERED = 1 };
 /* sparse optimizer of the update: SGD of Eq. 2, or row-wise
  * AdaGrad (the paper and SPEC leave it open) */
 enum { NEST_OPT_SGD = 0, NEST_OPT_ROWWISE_ADAGRAD = 1 };
+/* where the table shard lives (nest_config_t.table_location) */
+enum { NEST_TABLE_HBM = 0, NEST_TABLE_HOST = 1 };
 enum { NEST_MAX_WORLD = 64, NEST_MAX_MICRO_BATCHES = 8, NEST_MAX_TABLES = 1024 };
 
 /* Static configuration of one rank.  Capacities bound every per-batch count;
@@ -102,6 +104,14 @@ typedef struct {
   int32_t tower_hidden;       /* tower width (bf16 GEMMs) */
   int32_t optimizer;          /* NEST_OPT_SGD (default) or NEST_OPT_ROWWISE_ADAGRAD */
   float adagrad_eps;          /* AdaGrad denominator epsilon (fp32) */
+  int32_t table_location;     /* NEST_TABLE_HBM (default): table_mem is device memory.
+                                 NEST_TABLE_HOST: table_mem is pinned host memory (cudaHostAlloc /
+                                 cudaHostRegister, device-accessible through UVA) -- the host-DRAM
+                                 tier of SURVEY §8(f) NEXT-3: the DBP
+                                 retrieval (R4 prefetch gather, R5 refresh) reads rows over PCIe
+                                 into the HBM slot buffers, the write-back (R12) stores them back;
+                                 everything else stays in HBM.  nest_create checks the pointer
+                                 kind and returns NEST_ERR_INVALID on a mismatch. */
 } nest_config_t;
 
 /* Host-known counts of one slot after nest_route (all per this rank). */
@@ -182,8 +192,14 @@ NEST_API nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys,
  * host sync), key All2All, owner dedup, gather of the owned rows from the
  * shard into the slot's HBM buffer.  keys/bag_offsets: the local batch (nnz
  * occurrences, B samples).  perm/mb_offsets from nest_fwp_schedule (NULL =
- * one micro-batch, N must be 1).  The gather is ordered after the previous
- * update's write-back (events inside the library, reading Q8).  With the
+ * one micro-batch, N must be 1).  The gather is ordered after this slot's
+ * previous update's write-back (events inside the library, reading Q8).  If
+ * the other slot is routed and its update is still to come (the pipelined
+ * call order: route(t+1) inside window t), the gather skips that slot's keys
+ * K(t) -- they are supplied, updated, by nest_dbp_refresh, which then becomes
+ * mandatory before any lookup of this slot (NEST_ERR_ORDER otherwise) -- so
+ * the retrieval never waits for the update of window t.  Otherwise the gather
+ * waits for the other slot's update.  With the
  * fused NVLink transport (world > 1, NEST_A2A unset, NEST_EARLY_PUSH != 0)
  * the owner then pushes every requested row of the buffer into the
  * requesters' receive rows of this slot (the embedding All2All, issued here
@@ -195,8 +211,9 @@ NEST_API nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* 
 
 /* Dual-buffer synchronization: for every key k in both
  * the active slot's and the prefetch slot's owner key sets, copy the active
- * (already updated) row over the prefetch row.  Waits inside for the active
- * slot's update and the prefetch slot's gather.  After an early push (see
+ * (already updated, written-back) row into the prefetch slot's buffer -- the
+ * rows nest_route's gather skipped.  Waits inside for the active slot's update
+ * and the prefetch slot's gather.  After an early push (see
  * nest_route) the same rows are re-pushed to the requesters that hold stale
  * copies.  Collective in the early-push mode: every rank calls it for the
  * same slots. */

@@ -45,7 +45,7 @@ class NestContext:
                  max_batch: int, max_micro_batches: int = 1, max_recv_keys: int = 0,
                  max_mb_rows: int = 0, max_owner_mb_rows: int = 0, seed: int = 0,
                  init_mode: str = "uniform", tower_layers: int = 0, tower_hidden: int = 1024,
-                 optimizer: str = "sgd", adagrad_eps: float = 1e-8,
+                 optimizer: str = "sgd", adagrad_eps: float = 1e-8, table_location: str = "hbm",
                  nccl_uids: Optional[bytes] = None, device=None, init_tables: bool = True):
         import torch
         self.lib = L.load()
@@ -62,7 +62,9 @@ class NestContext:
             init_mode={"uniform": L.INIT_UNIFORM, "dyadic": L.INIT_DYADIC, "zero": L.INIT_ZERO}[init_mode],
             tower_layers=tower_layers, tower_hidden=tower_hidden,
             optimizer={"sgd": L.OPT_SGD, "rowwise_adagrad": L.OPT_ROWWISE_ADAGRAD}[optimizer],
-            adagrad_eps=adagrad_eps)
+            adagrad_eps=adagrad_eps,
+            table_location={"hbm": L.TABLE_HBM, "host": L.TABLE_HOST}[table_location])
+        self.table_location = table_location
         self.optimizer = optimizer
         self.world, self.rank, self.dim = world, rank, dim
         self.F = self.cfg.num_features
@@ -71,7 +73,12 @@ class NestContext:
         self.table_bytes, self.work_bytes = tb.value, wb.value
         self.shard_rows = self.lib.nest_shard_rows(C.byref(self.cfg))
         with torch.cuda.device(self.device):
-            self.table_mem = torch.empty(self.table_bytes, dtype=torch.uint8, device=self.device)
+            if table_location == "host":
+                # host-DRAM tier (NEXT-3): pinned host memory, reached by the
+                # kernels over PCIe through its UVA device alias
+                self.table_mem = torch.empty(self.table_bytes, dtype=torch.uint8, pin_memory=True)
+            else:
+                self.table_mem = torch.empty(self.table_bytes, dtype=torch.uint8, device=self.device)
             self.work_mem = torch.empty(self.work_bytes, dtype=torch.uint8, device=self.device)
             self.shard = self.table_mem.view(torch.float32)[: self.shard_rows * dim].view(self.shard_rows, dim)
             ctx = C.c_void_p()

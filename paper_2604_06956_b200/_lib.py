@@ -18,6 +18,7 @@ POOL_SUM, POOL_NONE = 0, 1
 INIT_UNIFORM, INIT_DYADIC, INIT_ZERO = 0, 1, 2
 SCHED_SEQUENTIAL, SCHED_CLUSTERED = 0, 1
 OPT_SGD, OPT_ROWWISE_ADAGRAD = 0, 1
+TABLE_HBM, TABLE_HOST = 0, 1
 MAX_MICRO_BATCHES = 8
 
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
@@ -46,7 +47,7 @@ class Config(C.Structure):
                 ("max_owner_keys", C.c_int64), ("max_mb_rows", C.c_int64),
                 ("max_owner_mb_rows", C.c_int64), ("seed", C.c_uint64), ("init_mode", C.c_int32),
                 ("tower_layers", C.c_int32), ("tower_hidden", C.c_int32), ("optimizer", C.c_int32),
-                ("adagrad_eps", C.c_float)]
+                ("adagrad_eps", C.c_float), ("table_location", C.c_int32)]
 
 
 class SlotInfo(C.Structure):

@@ -44,6 +44,8 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
              "bad optimizer");
   NEST_CHECK(cfg->optimizer == NEST_OPT_SGD || cfg->adagrad_eps >= 0.f, NEST_ERR_INVALID,
              "adagrad_eps must be >= 0");
+  NEST_CHECK(cfg->table_location == NEST_TABLE_HBM || cfg->table_location == NEST_TABLE_HOST, NEST_ERR_INVALID,
+             "bad table_location");
   c.rows.assign(cfg->table_rows, cfg->table_rows + c.T);
   for (int t = 0; t < c.T; ++t)
     NEST_CHECK(c.rows[t] >= 1 && c.rows[t] <= int64_t(kRowMask), NEST_ERR_INVALID, "bad table_rows");
@@ -331,10 +333,24 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
     NEST_CHECK((reinterpret_cast<uintptr_t>(table_mem) & 255) == 0 &&
                    (reinterpret_cast<uintptr_t>(work_mem) & 255) == 0,
                NEST_ERR_INVALID, "memory must be 256-byte aligned");
-    c->shard = reinterpret_cast<float*>(table_mem);
+    {
+      // the table tier: device memory (HBM) or pinned host memory reached over
+      // PCIe through its UVA device alias (host-DRAM tier, NEXT-3)
+      cudaPointerAttributes pa{};
+      NEST_CUDA(cudaPointerGetAttributes(&pa, table_mem));
+      if (c->cfg.table_location == NEST_TABLE_HOST) {
+        NEST_CHECK(pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr, NEST_ERR_INVALID,
+                   "table_location HOST needs pinned, device-mapped host memory");
+        c->shard = reinterpret_cast<float*>(pa.devicePointer);
+      } else {
+        NEST_CHECK(pa.type == cudaMemoryTypeDevice, NEST_ERR_INVALID,
+                   "table_location HBM needs device memory (pinned host memory: NEST_TABLE_HOST)");
+        c->shard = reinterpret_cast<float*>(table_mem);
+      }
+    }
     if (c->cfg.optimizer == NEST_OPT_ROWWISE_ADAGRAD) {
       c->opt_state = c->shard + std::max<int64_t>(c->Vo, 1) * c->D;
-      NEST_CUDA(cudaMemsetAsync(c->opt_state, 0, sizeof(float) * std::max<int64_t>(c->Vo, 1), S(stream)));
+      zero_f32(c->opt_state, std::max<int64_t>(c->Vo, 1), S(stream));
     }
     layout(*c, reinterpret_cast<char*>(work_mem));
     cudaStream_t st0 = S(stream);
@@ -419,7 +435,7 @@ nest_status_t nest_init_tables(nest_ctx_t* ctx, void* stream) {
   return guard(c, [&] {
     launch_init_tables(*c, S(stream));
     if (c->opt_state)   // row-wise AdaGrad accumulators start at 0
-      NEST_CUDA(cudaMemsetAsync(c->opt_state, 0, sizeof(float) * std::max<int64_t>(c->Vo, 1), S(stream)));
+      zero_f32(c->opt_state, std::max<int64_t>(c->Vo, 1), S(stream));
   });
 }
 
@@ -556,6 +572,7 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
       ps.bpc = 2.0 * c->D * sizeof(float);
     }
     NEST_CUDA(cudaEventRecord(a.ev_free, st));
+    p.refresh_pending = false;
   });
 }
 
@@ -565,6 +582,8 @@ nest_status_t nest_lookup_prefetch(nest_ctx_t* ctx, int32_t slot, int32_t mb, vo
   return guard(c, [&] {
     Slot& s = slot_of(*c, slot);
     NEST_CHECK(s.routed, NEST_ERR_ORDER, "prefetch before route");
+    NEST_CHECK(!s.refresh_pending, NEST_ERR_ORDER,
+               "dual-buffer refresh pending: nest_dbp_refresh(active, this slot) first (S:276)");
     NEST_CHECK(!s.updated, NEST_ERR_ORDER, "prefetch after the window closed (S:568)");
     NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
     if (s.early) return;   // pushed at route time
@@ -580,6 +599,8 @@ static nest_status_t lookup_fwd_impl(Ctx* c, int32_t slot, int32_t mb, void* out
     NEST_CHECK(!bf16 || c->cfg.pooling == NEST_POOL_SUM, NEST_ERR_INVALID, "bf16 output needs pooling = SUM");
     Slot& s = slot_of(*c, slot);
     NEST_CHECK(s.routed, NEST_ERR_ORDER, "lookup before route");
+    NEST_CHECK(!s.refresh_pending, NEST_ERR_ORDER,
+               "dual-buffer refresh pending: nest_dbp_refresh(active, this slot) first (S:276)");
     NEST_CHECK(!s.updated, NEST_ERR_ORDER, "lookup after the window closed (S:568)");
     NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
     NEST_CHECK(out != nullptr, NEST_ERR_INVALID, "null out");
@@ -632,12 +653,11 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
     NEST_CHECK(mb >= 0 && mb < s.N, NEST_ERR_INVALID, "micro-batch out of range");
     NEST_CHECK(dout != nullptr || s.info.mb_out_rows[mb] == 0, NEST_ERR_INVALID, "null dout");
     cudaStream_t cs = S(compute), ms = S(comm);
-    Slot& other = c->slot[1 - slot];
     const double row = double(c->D) * sizeof(float);
     if (mb == 0) NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
     if (c->W == 1 && s.N == 1) {
-      // one rank, one micro-batch: the segment-sum applies Eq. 2 itself
-      NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
+      // one rank, one micro-batch: the segment-sum applies Eq. 2 itself (the
+      // next slot's gather skipped this slot's rows: no ordering with it)
       {
         ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
         launch_segsum_sgd(*c, s, dout, opt, cs);
@@ -712,7 +732,6 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
       }
       if (mb == s.N - 1) {
         if (c->xfer_ce) xfer_wait_grads(*c, s, ms);  // every requester's gradients have landed
-        NEST_CUDA(cudaStreamWaitEvent(ms, other.ev_gather, 0));
         {
           ProfScope ps(*c, ST_UPDATE, SK_COMM, ms);
           launch_reduce_sgd(*c, s, opt, ms);
@@ -724,7 +743,6 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
         NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
       }
     } else if (mb == s.N - 1) {
-      NEST_CUDA(cudaStreamWaitEvent(cs, other.ev_gather, 0));
       {
         ProfScope ps(*c, ST_UPDATE, SK_COMPUTE, cs);
         launch_reduce_sgd(*c, s, opt, cs);

@@ -104,6 +104,9 @@ struct Slot {
   // right after the prefetch gather (`early`); the dual-buffer refresh re-pushed
   // the rows the previous window updated (`repushed`)
   bool early = false, repushed = false;
+  // the prefetch gather skipped the rows the other slot's pending update
+  // writes (K(t) cap K(t+1)); nest_dbp_refresh supplies them
+  bool refresh_pending = false;
   cudaEvent_t ev_early = nullptr, ev_repush = nullptr;
   cudaEvent_t ev_sorted = nullptr;  // occurrences sorted (the segment-sum's input)
   cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
@@ -180,7 +183,7 @@ struct Ctx {
   float* own_rows = nullptr;       // [OMBcap][d] (== src_rows when W == 1)
   int32_t* d_err = nullptr;        // [1]
   int32_t* d_cnt_scratch = nullptr; // [W*(Nmax)] mb counts scratch
-  int32_t* n_refreshed = nullptr;  // [4] rows copied by the last refresh | rows re-pushed off-GPU
+  int32_t* n_refreshed = nullptr;  // [4] rows copied by the last refresh | rows re-pushed off-GPU | rows gathered
   // FWP clustering scratch (cluster.cu)
   uint32_t* cl_bm = nullptr;       // [words+2]
   int32_t* cl_wr = nullptr;        // [words+2]
@@ -492,8 +495,9 @@ void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offs
 void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
 void route_sort(Ctx& c, Slot& s, cudaStream_t st);
 void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p);
+void zero_f32(float* p, int64_t n, cudaStream_t st);
 void launch_init_tables(Ctx& c, cudaStream_t st);
-void launch_gather(Ctx& c, Slot& s, cudaStream_t st);
+void launch_gather(Ctx& c, Slot& s, const uint32_t* skip_bm, cudaStream_t st);
 void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_rows = nullptr);
 // out: fp32 rows, or bf16 rows (pooled sum only) when bf16
 void launch_pool(Ctx& c, Slot& s, int mb, void* out, bool bf16, cudaStream_t st);

@@ -703,9 +703,18 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
   }
   {
     // ---- R4: gather the owned rows from the shard into the slot buffer ----
+    // DBP (reading Q8): when the other slot's update is still to
+    // come (pipelined: route(t+1) inside window t), its keys K(t) are skipped
+    // here and supplied by nest_dbp_refresh from the written-back shard, so
+    // this gather never waits for -- nor races -- that update; otherwise the
+    // gather follows the other slot's update and reads its written-back rows
+    Slot& o = c.slot[&s == &c.slot[0] ? 1 : 0];
+    const bool skip = o.routed && !o.updated;
+    if (!skip && o.routed) NEST_CUDA(cudaStreamWaitEvent(st, o.ev_update, 0));
+    s.refresh_pending = skip;
     ProfScope ps(c, ST_GATHER, SK_AUX, st);
-    launch_gather(c, s, st);
-    ps.dcount = s.n_owner;
+    launch_gather(c, s, skip ? o.obm : nullptr, st);
+    ps.dcount = c.n_refreshed + 2;          // rows copied (U_o minus the skipped ones)
     ps.bpc = 2.0 * c.D * sizeof(float);  // 2 U_o row
   }
   (void)D;

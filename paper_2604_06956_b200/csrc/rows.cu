@@ -103,39 +103,52 @@ __device__ __forceinline__ void copy_row(float* __restrict__ dst, const float* _
 }
 
 // ---------------------------------------------------------------------------
-// R4: buffer[u] = shard[owner_rows[u]]
+// R4: buffer[u] = shard[owner_rows[u]], except the rows of skip_bm (the keys
+// the other slot's pending update writes: the dual-buffer refresh copies
+// their updated values after that update, so the gather and the update touch
+// disjoint shard rows and need no ordering).  Counts the rows copied.
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_gather(const float* __restrict__ shard,
                                                         const int32_t* __restrict__ rows,
                                                         const int32_t* __restrict__ n_dev,
-                                                        float* __restrict__ out) {
+                                                        const uint32_t* __restrict__ skip_bm,
+                                                        float* __restrict__ out, int32_t* __restrict__ count) {
   Grp<D> gp;
   const int64_t n = *n_dev;
   constexpr int U = 4;
+  int32_t local = 0;
   for (int64_t r0 = gp.g * U; r0 < n; r0 += gp.ng * U) {
     int32_t idx[U];
+    bool take[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) idx[k] = r0 + k < n ? __ldg(rows + r0 + k) : 0;
+    for (int k = 0; k < U; ++k) {
+      idx[k] = r0 + k < n ? __ldg(rows + r0 + k) : 0;
+      take[k] = r0 + k < n && !(skip_bm && bit_test(skip_bm, uint32_t(idx[k])));
+    }
     float4 v[U][RowGeom<D>::VPL];
 #pragma unroll
     for (int k = 0; k < U; ++k)
 #pragma unroll
       for (int q = 0; q < RowGeom<D>::VPL; ++q)
-        if (r0 + k < n) v[k][q] = ldg_f4(shard + int64_t(idx[k]) * D + gp.col(q));
+        if (take[k]) v[k][q] = ldg_f4(shard + int64_t(idx[k]) * D + gp.col(q));
 #pragma unroll
-    for (int k = 0; k < U; ++k)
+    for (int k = 0; k < U; ++k) {
 #pragma unroll
       for (int q = 0; q < RowGeom<D>::VPL; ++q)
-        if (r0 + k < n) st_f4(out + (r0 + k) * D + gp.col(q), v[k][q]);
+        if (take[k]) st_f4(out + (r0 + k) * D + gp.col(q), v[k][q]);
+      if (take[k] && gp.l == 0) ++local;
+    }
   }
+  if (local) atomicAdd(count, local);
 }
 
-void launch_gather(Ctx& c, Slot& s, cudaStream_t st) {
+void launch_gather(Ctx& c, Slot& s, const uint32_t* skip_bm, cudaStream_t st) {
+  NEST_CUDA(cudaMemsetAsync(c.n_refreshed + 2, 0, sizeof(int32_t), st));
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW * 4;
     k_gather<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
-        c.shard, s.owner_rows, s.n_owner, s.buffer);
+        c.shard, s.owner_rows, s.n_owner, skip_bm, s.buffer, c.n_refreshed + 2);
   });
   NEST_LAUNCH_CHECK();
 }
@@ -1341,6 +1354,18 @@ __global__ void k_init_tables(int64_t nvec, int D, int T, int W, int rank,
     v.w = prf_value(h1, c4 * 4 + 3, mode, lo, scale);
     st_f4_cs(shard + e * 4, v);
   }
+}
+
+// zero n floats of device-accessible memory (device or mapped pinned host:
+// the optimizer state of a host-tier table)
+__global__ void k_zero_f32(float* __restrict__ p, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = 0.f;
+}
+void zero_f32(float* p, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_zero_f32<<<blocks_for_rows(n, 256, 148 * 8), 256, 0, st>>>(p, n);
+  NEST_LAUNCH_CHECK();
 }
 
 void launch_init_tables(Ctx& c, cudaStream_t st) {

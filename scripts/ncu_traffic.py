@@ -19,8 +19,9 @@ import os
 import subprocess
 
 STAGE_KERNELS = {
-    "segsum": ("k_seg_heads", "k_segsum_cold", "k_segsum_hot_chunks", "k_segsum_hot_final"),
-    "pool": ("k_pool",),
+    "segsum": ("k_segsum_range", "k_segsum_fix", "k_segsum_fix_big",
+               "k_seg_heads", "k_segsum_cold", "k_segsum_hot_chunks", "k_segsum_hot_final"),
+    "pool": ("k_pool_stream", "k_pool"),
     "gather": ("k_gather",),
     "refresh": ("k_refresh",),
     "update": ("k_reduce_sgd",),

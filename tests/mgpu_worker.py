@@ -47,7 +47,8 @@ def skewed_batches(cfg, B, T, world, seed=31):
     return out
 
 
-def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=None, adagrad=None):
+def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=None, adagrad=None,
+             tables="hbm"):
     F, d = cfg.num_features, cfg.dim
     batches = gen(cfg, B, T, world) if gen else \
         [[WL.gen_batch(cfg, 21, t, r, batch=B) for r in range(world)] for t in range(T)]
@@ -55,7 +56,7 @@ def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=No
     K = max(1, max(len(b[rank][0]) for b in batches))
     ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, max_keys=K, max_batch=B,
                       max_micro_batches=N, seed=13, init_mode=init, nccl_uids=uids, device=dev,
-                      optimizer="rowwise_adagrad" if adagrad else "sgd",
+                      optimizer="rowwise_adagrad" if adagrad else "sgd", table_location=tables,
                       adagrad_eps=adagrad[2] if adagrad else 1e-8)
     run = Runner(ctx, N=N, pipelined=True, lr_over_B=lr, adagrad=adagrad[:2] if adagrad else None)
     mine = [(torch.from_numpy(b[rank][0]).to(dev), torch.from_numpy(b[rank][1]).to(dev), B) for b in batches]
@@ -150,13 +151,18 @@ def main():
     cases.append(("adagrad-P2-N2", WL.CONFIGS["tiny"].with_(table_rows=(3000, 700, 90, 20), zipf=1.2,
                                                             bag_repeats=True, dim=32),
                   128, 2, 4, "uniform", "realistic", 0.0, None, (1.0 / 256, 0.05, 1e-8)))
+    # host-DRAM tier (NEXT-3): every owner's shard in pinned host memory
+    cases.append(("host-tier-P1-N2", WL.CONFIGS["tiny"].with_(table_rows=(3000, 40, 7, 999), zipf=1.3,
+                                                              bag_repeats=True, dim=128),
+                  512, 2, 3, "dyadic", "dyadic", 2.0 ** -12, None, None, "host"))
     all_ok = True
     for case in cases:
         obj = [unique_ids() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         gen = case[8] if len(case) > 8 else None
         ada = case[9] if len(case) > 9 else None
-        all_ok &= run_case(*case[:8], rank, world, dev, obj[0], gen=gen, adagrad=ada)
+        tables = case[10] if len(case) > 10 else "hbm"
+        all_ok &= run_case(*case[:8], rank, world, dev, obj[0], gen=gen, adagrad=ada, tables=tables)
     dist.barrier(device_ids=[local])
     dist.destroy_process_group()
     if rank == 0:

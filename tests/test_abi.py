@@ -45,6 +45,13 @@ def test_host_only_calls(lib):
     cfg.dim = 48
     assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 1  # INVALID
     assert b"dim" in lib.nest_last_error(None)
+    cfg.dim = 16
+    cfg.table_location = L.TABLE_HOST      # host-DRAM tier: same sizes
+    assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 0
+    assert tb.value == 2000 * 16 * 4
+    cfg.table_location = 7
+    assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 1  # INVALID
+    assert b"table_location" in lib.nest_last_error(None)
     assert lib.nest_version().startswith(b"nestpipe")
 
 

@@ -357,7 +357,7 @@ def test_train_w1_clustered_p1_bit_exact():
 
 
 # --------------------------------------------------------------------------- edge cases
-def _p1_check(cfg, batches, N, pipelined=True, lr=2.0 ** -10, seed=5):
+def _p1_check(cfg, batches, N, pipelined=True, lr=2.0 ** -10, seed=5, **ctx_kw):
     """Run the given per-step batches (W=1) and compare pooled rows of every
     step and the final rows bit-exactly against the oracle (P1)."""
     F, d = cfg.num_features, cfg.dim
@@ -365,7 +365,7 @@ def _p1_check(cfg, batches, N, pipelined=True, lr=2.0 ** -10, seed=5):
     douts = [WL.gen_dout(seed, t, 0, (len(o) - 1), d, "dyadic") for t, (k, o) in enumerate(batches)]
     B = (len(batches[0][1]) - 1) // F
     K = max(1, max(len(k) for k, _ in batches))
-    ctx = make_ctx(cfg, B, N=N, K=K, init="dyadic", seed=seed)
+    ctx = make_ctx(cfg, B, N=N, K=K, init="dyadic", seed=seed, **ctx_kw)
     run = Runner(ctx, N=N, pipelined=pipelined, lr_over_B=lr)
     db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), B) for k, o in batches]
     cap = B // N
@@ -430,6 +430,63 @@ def test_edge_segments_cut_by_ranges_and_giant_segment(d, N):
     keys[rng.random(K) < 0.002] = (3 << 40) | 999          # ~330 occurrences
     keys2 = keys[::-1].copy()
     _p1_check(cfg, [(keys, offs), (keys2, offs)], N=N, lr=2.0 ** -12)
+
+
+# --------------------------------------------------------------------------- host-DRAM tier
+@pytest.mark.parametrize("N,pipelined,d", [(1, True, 16), (2, True, 16), (1, False, 128), (4, True, 128)])
+def test_host_tier_p1_bit_exact(N, pipelined, d):
+    """NEXT-3: the table shard in pinned host memory (retrieval, refresh and
+    write-back over PCIe) reaches the same bits as the oracle -- and so as the
+    HBM tier -- through the DBP/FWP pipeline, hot segments included."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(4000, 50, 9, 2000), zipf=1.3, bag_repeats=True, dim=d)
+    batches = [WL.gen_batch(cfg, 60 + t, t, 0, batch=512) for t in range(4)]
+    _p1_check(cfg, batches, N=N, pipelined=pipelined, table_location="host")
+
+
+def test_host_tier_rowwise_adagrad_matches_hbm():
+    """Row-wise AdaGrad with the shard and its accumulators in host memory:
+    bitwise the HBM-tier result (same kernels, same order)."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(5000, 3000, 200, 77), zipf=1.3, bag_repeats=True, dim=32)
+    B, T, F, d = 256, 4, cfg.num_features, cfg.dim
+    batches = [WL.gen_batch(cfg, 9, t, 0, batch=B) for t in range(T)]
+    douts = [to_dev(WL.gen_dout(9, t, 0, B * F, d, "realistic"), torch.float32) for t in range(T)]
+    K = max(len(b[0]) for b in batches)
+    res = []
+    for loc in ("hbm", "host"):
+        ctx = make_ctx(cfg, B, N=1, K=K, init="uniform", seed=4, optimizer="rowwise_adagrad", table_location=loc)
+        run = Runner(ctx, N=1, pipelined=True, adagrad=(1.0 / B, 0.05))
+        db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), B) for k, o in batches]
+        for t in range(T):
+            run.step(db[t], db[t + 1] if t + 1 < T else None, lambda tt, i, p, dd=douts[t]: dd)
+        run.join()
+        torch.cuda.synchronize()
+        allk = to_dev(np.unique(np.concatenate([b[0] for b in batches])), torch.int64)
+        res.append((ctx.read_rows(allk).cpu().numpy(), ctx.read_state(allk).cpu().numpy()))
+        ctx.close()
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+def test_host_tier_pointer_kind_checked():
+    """nest_create rejects device memory for the host tier and pinned host
+    memory for the HBM tier (include/nest.h, table_location)."""
+    import ctypes as C
+    from paper_2604_06956_b200 import _lib as L
+    lib = L.load()
+    rows = (C.c_int64 * 4)(1000, 1000, 1000, 1000)
+    work = None
+    for loc, mem in ((L.TABLE_HOST, "cuda"), (L.TABLE_HBM, "pinned")):
+        cfg = L.Config(world=1, rank=0, num_tables=4, dim=16, table_rows=rows, pooling=0, num_features=4,
+                       max_keys=512, max_batch=32, max_micro_batches=1, seed=1, table_location=loc)
+        tb, wb = C.c_size_t(), C.c_size_t()
+        assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 0
+        tab = (torch.empty(tb.value, dtype=torch.uint8, device=DEV) if mem == "cuda"
+               else torch.empty(tb.value, dtype=torch.uint8, pin_memory=True))
+        work = torch.empty(wb.value, dtype=torch.uint8, device=DEV)
+        ctx = C.c_void_p()
+        st = lib.nest_create(C.byref(cfg), None, C.c_void_p(tab.data_ptr()), C.c_void_p(work.data_ptr()),
+                             C.c_void_p(torch.cuda.current_stream(DEV).cuda_stream), C.byref(ctx))
+        assert st == 1 and not ctx.value, (loc, mem, st)
+        assert b"table_location" in lib.nest_last_error(None) or b"memory" in lib.nest_last_error(None)
 
 
 # --------------------------------------------------------------------------- errors
