@@ -546,9 +546,12 @@ def main():
                 "dbp": {"refresh_ms_per_step": rs["ms"] / max(1, rs["records"]),
                         "refresh_stage": rname,
                         "refreshed_rows_per_step": rs["units"] / max(1, rs["records"]),
-                        "owner_unique_per_step": st["gather"]["units"] / max(1, st["gather"]["records"]),
-                        "intersection_ratio": (rs["units"] / st["gather"]["units"]
-                                               if st["gather"]["units"] else None)},
+                        # the prefetch gather copies U_o - I rows (the pending update's keys
+                        # are skipped and supplied by the refresh), so U_o = gathered + I
+                        "gathered_rows_per_step": st["gather"]["units"] / max(1, st["gather"]["records"]),
+                        "owner_unique_per_step": (st["gather"]["units"] + rs["units"]) / max(1, st["gather"]["records"]),
+                        "intersection_ratio": (rs["units"] / (st["gather"]["units"] + rs["units"])
+                                               if st["gather"]["units"] + rs["units"] else None)},
                 "fwp": dict(fwp_stats, with_tower=with_tower_runs),
                 "embedding_only": embedding_only}
         if host_tier is not None:

@@ -510,6 +510,35 @@ def test_error_paths():
         ctx.route(0, to_dev(keys, torch.int64), to_dev(offs, torch.int32), 32)
 
 
+def test_refresh_required_after_pipelined_route():
+    """Routing the next batch while the active slot's update is pending makes
+    its gather skip K(t) (the refresh supplies those rows): a lookup of that
+    slot before nest_dbp_refresh is an ordering error; after it, the rows are
+    the updated ones (P1, bit-exact)."""
+    cfg = WL.CONFIGS["tiny"]
+    B, F, d = 32, cfg.num_features, cfg.dim
+    b0, b1 = WL.gen_batch(cfg, 3, 0, 0, batch=B), WL.gen_batch(cfg, 3, 1, 0, batch=B)
+    ctx = make_ctx(cfg, B, N=1, seed=6)
+    k0, o0 = to_dev(b0[0], torch.int64), to_dev(b0[1], torch.int32)
+    k1, o1 = to_dev(b1[0], torch.int64), to_dev(b1[1], torch.int32)
+    out = torch.empty((B * F, d), device=DEV)
+    ctx.route(0, k0, o0, B)
+    ctx.lookup_fwd(0, 0, out)
+    ctx.route(1, k1, o1, B)                     # window 0 still open: gather skips K(0)
+    with pytest.raises(NestError) as e:
+        ctx.lookup_fwd(1, 0, out)
+    assert e.value.status == "NEST_ERR_ORDER"
+    dout = to_dev(WL.gen_dout(3, 0, 0, B * F, d, "dyadic"), torch.float32)
+    ctx.grad_bwd_update(0, 0, dout, 2.0 ** -10)
+    ctx.dbp_refresh(0, 1)
+    ctx.lookup_fwd(1, 0, out)
+    torch.cuda.synchronize()
+    tab = OS.LazyTable(6, d, "dyadic")
+    OS.sync_step(tab, [b0], [dout.cpu().numpy()], 2.0 ** -10)
+    ref = OS.sync_step(tab, [b1], [np.zeros((B * F, d))], 0.0).pooled[0]
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
 # --------------------------------------------------------------------------- full size
 def test_genrec_full_tables_unpooled_sampled():
     """BASELINE configs[2] (8 x 50M rows, d=64, seq 1,024 unpooled, Zipf 1.2) with
