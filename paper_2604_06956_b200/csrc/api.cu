@@ -107,6 +107,7 @@ static size_t layout(Ctx& c, char* base) {
     c.tval[i] = w.take<int32_t>(K);
   }
   c.hist = w.take<uint32_t>(int64_t(1 << kRadixMaxDigit) * radix_blocks(K) + 2);
+  c.radix_aux = w.take<uint32_t>(kRadixAux);
   c.scan_tmp = w.take<char>(scan_bytes);
   c.scan_tmp_win = w.take<char>(scan_bytes);
   c.samp_scratch = w.take<int32_t>(B + 2);
@@ -348,6 +349,7 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
         c->shard = reinterpret_cast<float*>(table_mem);
       }
     }
+    if (const char* e = std::getenv("NEST_GATHER_SKIP")) c->gather_skip = std::atoi(e) != 0;
     if (c->cfg.optimizer == NEST_OPT_ROWWISE_ADAGRAD) {
       c->opt_state = c->shard + std::max<int64_t>(c->Vo, 1) * c->D;
       zero_f32(c->opt_state, std::max<int64_t>(c->Vo, 1), S(stream));
@@ -657,7 +659,9 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
     if (mb == 0) NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
     if (c->W == 1 && s.N == 1) {
       // one rank, one micro-batch: the segment-sum applies Eq. 2 itself (the
-      // next slot's gather skipped this slot's rows: no ordering with it)
+      // next slot's gather skipped this slot's rows: no ordering with it,
+      // unless NEST_GATHER_SKIP=0)
+      if (!c->gather_skip) NEST_CUDA(cudaStreamWaitEvent(cs, c->slot[1 - slot].ev_gather, 0));
       {
         ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
         launch_segsum_sgd(*c, s, dout, opt, cs);
@@ -732,6 +736,7 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
       }
       if (mb == s.N - 1) {
         if (c->xfer_ce) xfer_wait_grads(*c, s, ms);  // every requester's gradients have landed
+        if (!c->gather_skip) NEST_CUDA(cudaStreamWaitEvent(ms, c->slot[1 - slot].ev_gather, 0));
         {
           ProfScope ps(*c, ST_UPDATE, SK_COMM, ms);
           launch_reduce_sgd(*c, s, opt, ms);
@@ -743,6 +748,7 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
         NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
       }
     } else if (mb == s.N - 1) {
+      if (!c->gather_skip) NEST_CUDA(cudaStreamWaitEvent(cs, c->slot[1 - slot].ev_gather, 0));
       {
         ProfScope ps(*c, ST_UPDATE, SK_COMPUTE, cs);
         launch_reduce_sgd(*c, s, opt, cs);

@@ -168,7 +168,8 @@ struct Ctx {
   int32_t* occ_mbrow = nullptr;    // [Kcap]
   uint32_t* tkey[2] = {nullptr, nullptr};  // radix ping-pong [Kcap]
   int32_t* tval[2] = {nullptr, nullptr};
-  uint32_t* hist = nullptr;        // [2^kRadixMaxDigit * radix blocks + 2]
+  uint32_t* hist = nullptr;        // [2^kRadixMaxDigit * radix blocks + 2] (one-sweep: tile status words)
+  uint32_t* radix_aux = nullptr;   // [kRadixAux] one-sweep: global digit histograms of every pass + tile counter
   void* scan_tmp = nullptr;        // scan block sums, route-side streams (bytes)
   void* scan_tmp_win = nullptr;    // scan block sums, window-side streams
   int32_t* samp_scratch = nullptr; // [Bcap+1] unpooled sample prefix (route)
@@ -223,6 +224,9 @@ struct Ctx {
   int early_push = 0;              // EarlyPush: embedding rows pushed at route time (fused transport)
   float* send_stage = nullptr;     // [OMBcap][d] early push send rows (copy-engine early push)
   bool grad_ce = false;            // fused transport, gradients by copy engine (NEST_GRAD_PUSH=ce)
+  // the prefetch gather skips the pending update's keys (default); 0: the r01
+  // ordering, update(t) waits for gather(t+1) (NEST_GATHER_SKIP=0)
+  bool gather_skip = true;
   int64_t src_slot_stride = 0;     // floats between the two slots' receive windows (0: shared)
   std::vector<void*> peer_win;
   std::vector<float*> peer_src, peer_own;
@@ -482,6 +486,8 @@ constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kRadixMaxDigit = 8;
 
 inline int radix_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kRadixTile - 1) / kRadixTile); }
+// one-sweep aux words: 4 passes x 256 global digit counts + tile counter
+constexpr int kRadixAux = 4 * 256 + 32;
 
 void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                       int32_t* vout, int64_t n, int bits, cudaStream_t st);
