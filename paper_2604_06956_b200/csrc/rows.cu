@@ -1082,14 +1082,19 @@ void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st) {
   NEST_LAUNCH_CHECK();
 }
 
-// segment-sum form: NEST_SEGSUM = range (default: k_segsum_range + fix-ups) or
-// chunks (cold lane groups + hot chunk partials, the r01 kernels)
-static bool segsum_chunks() {
-  static const bool v = [] {
+// segment-sum form: NEST_SEGSUM = range (k_segsum_range + fix-ups) or chunks
+// (cold lane groups + hot chunk partials, the r01 kernels); default: range at
+// one rank, chunks at W > 1, where the segment-sum stores every key's row into
+// a peer's window and the range form measured slower inside the contended
+// step (W=4 DLRM: 49.6-50.7 vs 53.6-54.3 M samples/s; W=1: range 0.55 vs
+// 0.59 ms serialised, E step 1.50 ms)
+static bool segsum_chunks(const Ctx& c) {
+  static const int v = [] {
     const char* e = std::getenv("NEST_SEGSUM");
-    return e && std::string(e) == "chunks";
+    const std::string s = e ? e : "";
+    return s == "chunks" ? 1 : s == "range" ? 0 : -1;
   }();
-  return v;
+  return v < 0 ? c.W > 1 : v == 1;
 }
 void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st) {
   const int64_t Ui = s.info.mb_uniq[mb];
@@ -1099,7 +1104,7 @@ void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows
   const int32_t* sval = s.sval + s.q0[mb];
   const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
   const uint32_t umask = (1u << s.ubits) - 1u;
-  if (!segsum_chunks()) {
+  if (!segsum_chunks(c)) {
     // counters: seg_tot[0] = cut segments listed, seg_tot[1] = big ones
     NEST_CUDA(cudaMemsetAsync(c.seg_tot, 0, 2 * sizeof(int32_t), st));
     const int64_t nr = (Ki + kSegRange - 1) / kSegRange;

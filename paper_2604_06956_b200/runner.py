@@ -92,7 +92,9 @@ class Runner:
             self.compute = torch.cuda.Stream(device=dev, priority=pe)            # embedding lane
             self.comm = torch.cuda.Stream(device=dev, priority=pc) if ctx.world > 1 else self.compute
             self.dense = torch.cuda.Stream(device=dev, priority=pd)              # tower lane
-            self.aux = torch.cuda.Stream(device=dev)                # DBP lookahead
+            # DBP lookahead (route / owner dedup / gather / early push / sort of
+            # batch t+1); NEST_AUX_PRIORITY (default 0, the lowest)
+            self.aux = torch.cuda.Stream(device=dev, priority=int(os.environ.get("NEST_AUX_PRIORITY", "0")))
         self.t = 0
         self.primed = False
         self.outs: List[torch.Tensor] = []

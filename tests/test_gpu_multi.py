@@ -28,6 +28,7 @@ def _ndev():
 # the embedding push inside the window, copy engines, NCCL send/recv
 TRANSPORTS = {"fused-early": {}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
               "fused-early-gradce": {"NEST_GRAD_PUSH": "ce"},
+              "fused-early-range": {"NEST_SEGSUM": "range"},
               "fused-window": {"NEST_EARLY_PUSH": "0"}, "ce": {"NEST_A2A": "ce"},
               "nccl": {"NEST_A2A": "nccl"}}
 
