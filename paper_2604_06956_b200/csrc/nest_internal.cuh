@@ -489,6 +489,8 @@ inline int radix_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kRadixTile - 1
 // one-sweep aux words: 4 passes x 256 global digit counts + tile counter
 constexpr int kRadixAux = 4 * 256 + 32;
 
+void radix_sort_pairs_shifts(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
+                             int64_t n, const std::vector<int>& shifts, cudaStream_t st);
 void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                       int32_t* vout, int64_t n, int bits, cudaStream_t st);
 int radix_digit_bits(int bits);

@@ -319,6 +319,31 @@ int radix_digit_bits(int bits) {
   return db < 8 ? 8 : db;
 }
 
+// stable LSD sort by the 8-bit digits at the given shifts, in order (the
+// classic per-pass histogram + scan + scatter)
+void radix_sort_pairs_shifts(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
+                             int64_t n, const std::vector<int>& shifts, cudaStream_t st) {
+  if (n <= 0 || shifts.empty()) return;
+  const int nb = radix_blocks(n);
+  const uint32_t* sk = kin;
+  const int32_t* sv = vin;
+  for (size_t p = 0; p < shifts.size(); ++p) {
+    uint32_t* dk;
+    int32_t* dv;
+    if (p + 1 == shifts.size()) {
+      dk = kout;
+      dv = vout;
+    } else {
+      const int t = (sk == c.tkey[0]) ? 1 : 0;
+      dk = c.tkey[t];
+      dv = c.tval[t];
+    }
+    radix_pass<8>(c, sk, sv, dk, dv, n, shifts[p], nb, st);
+    sk = dk;
+    sv = dv;
+  }
+}
+
 // NEST_RADIX=onesweep: the one-sweep sort above; default: per-pass histogram +
 // scan + scatter.  Measured on DLRM W=1 (3.4M pairs, 3 passes): the one-sweep
 // form makes the E step slower (1.55 vs 1.50 ms; 128 registers for the
@@ -918,14 +943,30 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
 // R1 tail: occurrences sorted by (micro-batch, key) -- the grouping of the
 // deterministic segment-sum, first needed by the backward of this batch, so
 // it runs after everything the next window's forward waits for
+// The key is (mb << ubits) | u with ubits sized for the capacity K (fixed
+// before the count sync); after it the batch's U_s is known and u < U_s, so
+// only the digits of bits_for(U_s) (+ the micro-batch digit) can differ: e.g.
+// gen-rec (K = 67M -> 27 bits, U_s = 5M -> 23 bits) sorts in 3 passes, not 4.
 void route_sort(Ctx& c, Slot& s, cudaStream_t st) {
   int mbbits = 0;
   while ((1 << mbbits) < s.N) ++mbbits;
   const int64_t nnz = s.info.nnz;
   ProfScope ps(c, ST_SORT, SK_AUX, st);
-  radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, s.ubits + mbbits, st);
-  const int bits = s.ubits + mbbits, db = radix_digit_bits(bits);
-  const int passes = bits <= db ? 1 : (bits + db - 1) / db;
+  const int ub = std::min(bits_for(std::max<int64_t>(s.info.uniq, 2)), s.ubits);
+  int passes;
+  if (mbbits == 0) {
+    radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, ub, st);
+    const int db = radix_digit_bits(ub);
+    passes = ub <= db ? 1 : (ub + db - 1) / db;
+  } else {
+    // LSD over the u digits, then the micro-batch digit at ubits (a u digit
+    // that also covers micro-batch bits only refines the order of the last pass)
+    std::vector<int> shifts;
+    for (int sh = 0; sh < ub; sh += kRadixMaxDigit) shifts.push_back(sh);
+    shifts.push_back(s.ubits);
+    radix_sort_pairs_shifts(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, shifts, st);
+    passes = int(shifts.size());
+  }
   ps.launches = nnz > 0 ? 5 * passes : 0;
   ps.bytes = double(nnz) * 16 * passes;   // every pass reads + writes (key, value)
 }

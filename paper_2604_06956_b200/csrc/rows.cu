@@ -370,6 +370,50 @@ __global__ void __launch_bounds__(kRowThreads) k_pool_stream(int64_t nsamp, int 
   }
 }
 
+// R8 unpooled, streamed: lane group per sample, the sample's occurrence row
+// indices loaded L at a time (coalesced), then U row copies in flight
+template <int D, bool W1, int U>
+__global__ void __launch_bounds__(kRowThreads) k_expand_stream(int nsamp, int F,
+                                                               const int32_t* __restrict__ perm_mb,
+                                                               const int32_t* __restrict__ bag_off,
+                                                               const int32_t* __restrict__ samp_base,
+                                                               const int32_t* __restrict__ inverse,
+                                                               const int32_t* __restrict__ pos,
+                                                               const float* __restrict__ src,
+                                                               float* __restrict__ out) {
+  Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
+  const uint32_t gm = group_mask<D>(gp);
+  for (int64_t p = gp.g; p < nsamp; p += gp.ng) {
+    const int b = __ldg(perm_mb + p);
+    const int j0 = __ldg(bag_off + int64_t(b) * F), j1 = __ldg(bag_off + int64_t(b + 1) * F);
+    float* orow = out + int64_t(__ldg(samp_base + b) - j0) * D;   // row of occurrence j: orow + j*D
+    for (int c0 = j0; c0 < j1; c0 += L) {
+      const int n = min(L, j1 - c0);
+      int r_l = 0;
+      if (gp.l < n) {
+        const int u = __ldg(inverse + c0 + gp.l);
+        r_l = W1 ? u : __ldg(pos + u);
+      }
+      for (int t0 = 0; t0 < n; t0 += U) {
+        float4 x[U][VPL];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int r = __shfl_sync(gm, r_l, (t0 + k) & (L - 1), L);
+          if (t0 + k < n)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) x[k][v] = ldg_f4(src + int64_t(r) * D + gp.col(v));
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+          if (t0 + k < n)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) st_f4_cs(orow + int64_t(c0 + t0 + k) * D + gp.col(v), x[k][v]);
+      }
+    }
+  }
+}
+
 // pooling form: NEST_POOL = stream (default: k_pool_stream, lane group per
 // sample) or bag (k_pool, lane group per bag, the r01 kernel)
 static bool pool_by_bag() {
@@ -427,6 +471,15 @@ void launch_pool(Ctx& c, Slot& s, int mb, void* out_v, bool bf16, cudaStream_t s
                 nrows, c.F, perm_mb, s.bag_off, s.inverse, pos, src, out);
         });
       }
+    } else if (!pool_by_bag()) {
+      NEST_DISPATCH_U({
+        if (w1)
+          k_expand_stream<D, true, SU><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
+              s.cap, c.F, perm_mb, s.bag_off, s.samp_base, s.inverse, pos, src, out);
+        else
+          k_expand_stream<D, false, SU><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
+              s.cap, c.F, perm_mb, s.bag_off, s.samp_base, s.inverse, pos, src, out);
+      });
     } else {
       if (w1)
         k_expand_rows<D, true><<<emb_blocks(s.cap, rpb), kRowThreads, 0, st>>>(
