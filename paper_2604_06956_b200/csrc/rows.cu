@@ -1332,30 +1332,41 @@ __global__ void __launch_bounds__(kRowThreads) k_refresh(
     const int32_t* __restrict__ n_p, const int32_t* __restrict__ rows_p,
     const uint32_t* __restrict__ bm_a, const float* __restrict__ shard, float* __restrict__ buf_p,
     int32_t* __restrict__ count) {
+  // each lane group tests L keys at once (one coalesced load of their shard
+  // rows + one bit test per lane), then copies the hits -- the ~I/U_o
+  // fraction that is in the active slot's key set -- U rows in flight
   Grp<D> gp;
+  constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
+  constexpr int U = 4;
+  const uint32_t gm = group_mask<D>(gp);
   const int64_t n = *n_p;
   int32_t local = 0;
-  constexpr int U = 4;
-  for (int64_t u0 = gp.g * U; u0 < n; u0 += gp.ng * U) {
-    uint32_t ld[U];
-    bool hit[U];
+  for (int64_t u0 = gp.g * L; u0 < n; u0 += gp.ng * L) {
+    const int64_t u = u0 + gp.l;
+    const uint32_t ld = u < n ? uint32_t(__ldg(rows_p + u)) : 0u;
+    const bool hit = u < n && bit_test(bm_a, ld);
+    uint32_t hits = __ballot_sync(gm, hit) >> (lane_id() - gp.l);
+    if (gp.l == 0) local += __popc(hits);
+    while (hits) {
+      int t[U];
+      float4 v[U][VPL];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      ld[k] = u0 + k < n ? uint32_t(__ldg(rows_p + u0 + k)) : 0u;
-      hit[k] = u0 + k < n && bit_test(bm_a, ld[k]);
-    }
-    float4 v[U][RowGeom<D>::VPL];
+      for (int k = 0; k < U; ++k) {
+        t[k] = hits ? __ffs(hits) - 1 : -1;
+        if (hits) hits &= hits - 1;
+      }
 #pragma unroll
-    for (int k = 0; k < U; ++k)
+      for (int k = 0; k < U; ++k) {
+        const uint32_t r = __shfl_sync(gm, ld, t[k] < 0 ? 0 : t[k], L);
+        if (t[k] >= 0)
 #pragma unroll
-      for (int q = 0; q < RowGeom<D>::VPL; ++q)
-        if (hit[k]) v[k][q] = ldg_f4(shard + int64_t(ld[k]) * D + gp.col(q));
+          for (int q = 0; q < VPL; ++q) v[k][q] = ldg_f4(shard + int64_t(r) * D + gp.col(q));
+      }
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
+      for (int k = 0; k < U; ++k)
+        if (t[k] >= 0)
 #pragma unroll
-      for (int q = 0; q < RowGeom<D>::VPL; ++q)
-        if (hit[k]) st_f4(buf_p + (u0 + k) * D + gp.col(q), v[k][q]);
-      if (hit[k] && gp.l == 0) ++local;
+          for (int q = 0; q < VPL; ++q) st_f4(buf_p + (u0 + t[k]) * D + gp.col(q), v[k][q]);
     }
   }
   if (local) atomicAdd(count, local);
@@ -1364,7 +1375,7 @@ __global__ void __launch_bounds__(kRowThreads) k_refresh(
 void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st) {
   NEST_CUDA(cudaMemsetAsync(c.n_refreshed, 0, sizeof(int32_t), st));
   NEST_DISPATCH_D(c.D, {
-    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW * 4;
+    const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW * RowGeom<D>::L;   // keys per block pass
     k_refresh<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
         p.n_owner, p.owner_rows, a.obm, c.shard, p.buffer, c.n_refreshed);
   });

@@ -129,15 +129,15 @@ void tower_create(Ctx& c) {
   NEST_CUBLAS(cublasCreate(&t->h));
   NEST_CUBLAS(cublasSetWorkspace(t->h, t->ws, t->ws_bytes));
   NEST_CUBLAS(cublasSetMathMode(t->h, CUBLAS_DEFAULT_MATH));
-  // SMs left to the embedding lane (pool / segment-sum / send gather) that
-  // FWP overlaps with the tower: NEST_TOWER_SM_RESERVE, default 0
-  // (W=1 E+T, two A/B rounds: reserve 0 20.3 / 19.8, 12 20.0 / 19.4, 24
-  // 20.0 / 19.4 M samples/s; r01 measured 24 marginally best with its kernels)
+  // SMs left to the embedding lane (pool / segment-sum / send gather) and the
+  // DBP lookahead that run beside the tower: NEST_TOWER_SM_RESERVE,
+  // default 24.  W=1 E+T is within noise for 0 / 12 / 24 (19.4-20.3 M
+  // samples/s); at W=4, reserve 0 measured 50.6 vs 54.2 M samples/s
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const char* rv = std::getenv("NEST_TOWER_SM_RESERVE");
-    const int reserve = rv ? std::atoi(rv) : 0;
+    const int reserve = rv ? std::atoi(rv) : 24;
     if (reserve > 0 && reserve < sms) {
       NEST_CUBLAS(cublasSetSmCountTarget(t->h, sms - reserve));
       t->sm_target = sms - reserve;
