@@ -33,8 +33,8 @@ def to_dev(a, dtype):
 
 def make_ctx(cfg, B, N=1, K=None, init="dyadic", seed=1, **kw):
     K = K or int(B * cfg.num_features * cfg.bag_len[1])
-    return NestContext(cfg.table_rows, cfg.dim, pooling=cfg.pooling, max_keys=K, max_batch=B,
-                       max_micro_batches=N, seed=seed, init_mode=init, device=DEV, **kw)
+    return NestContext(cfg.table_rows, cfg.dim, pooling=cfg.pooling, num_features=cfg.num_features, max_keys=K,
+                       max_batch=B, max_micro_batches=N, seed=seed, init_mode=init, device=DEV, **kw)
 
 
 def rel_rowwise_ok(gpu, ref, tol=1e-5, scale=None):
@@ -430,6 +430,17 @@ def test_edge_segments_cut_by_ranges_and_giant_segment(d, N):
     keys[rng.random(K) < 0.002] = (3 << 40) | 999          # ~330 occurrences
     keys2 = keys[::-1].copy()
     _p1_check(cfg, [(keys, offs), (keys2, offs)], N=N, lr=2.0 ** -12)
+
+
+@pytest.mark.parametrize("d,N", [(16, 1), (128, 2)])
+def test_edge_many_features_per_sample(d, N):
+    """70 bags per sample (more than a lane group's 4..32 lanes hold at once:
+    the streaming pool reloads its window of bag ends), empty bags included,
+    bags of up to 5 keys on 3 tables (feature -> table map)."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(3000, 700, 41), dim=d, bag_len=(0, 5), bag_repeats=True,
+                                   feature_table=tuple(f % 3 for f in range(70)))
+    batches = [WL.gen_batch(cfg, 80 + t, t, 0, batch=64) for t in range(3)]
+    _p1_check(cfg, batches, N=N)
 
 
 # --------------------------------------------------------------------------- host-DRAM tier
