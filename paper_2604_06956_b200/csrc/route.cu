@@ -512,18 +512,27 @@ __global__ void k_emit(int64_t words, const uint32_t* __restrict__ bm, const int
     uint32_t x = bm[w];
     if (!x) continue;
     int32_t r = wr[w];
+    // segment (owner, table) of the word's first bit: largest s with
+    // seg_base[s] <= dom (seg_base[nseg] = V); segments span >= 1 row each,
+    // so later bits of the word advance it at most a few steps
+    const int64_t dom0 = w * 32 + (__ffs(x) - 1);
+    int lo = 0, hi = nseg;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(seg_base + mid) <= dom0) lo = mid; else hi = mid;
+    }
+    int64_t sb = __ldg(seg_base + lo), se = __ldg(seg_base + lo + 1);
     while (x) {
       const int b = __ffs(x) - 1;
       x &= x - 1;
       const int64_t dom = w * 32 + b;
-      // segment (owner, table) containing dom: largest s with seg_base[s] <= dom
-      int lo = 0, hi = nseg;  // seg_base[nseg] = V > dom
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(seg_base + mid) <= dom) lo = mid; else hi = mid;
+      while (dom >= se) {
+        ++lo;
+        sb = se;
+        se = __ldg(seg_base + lo + 1);
       }
       const int o = lo / T, t = lo - o * T;
-      const int64_t row = (dom - __ldg(seg_base + lo)) * W + o;
+      const int64_t row = (dom - sb) * W + o;
       uniq[r] = (int64_t(t) << kRowBits) | row;
       mask[r] = mask0;
       if (owner_rows) owner_rows[r] = int32_t(dom);
