@@ -66,6 +66,8 @@ def parse():
                     help="sparse update: SGD of Eq. 2 (default) or row-wise AdaGrad (SURVEY NEXT-2)")
     ap.add_argument("--tables", default="hbm", choices=["hbm", "host"],
                     help="table tier: HBM (default) or pinned host DRAM over PCIe (SURVEY NEXT-3)")
+    ap.add_argument("--tower-train", action="store_true",
+                    help="train the stand-in tower: dense dW AllReduce + SGD on the dW stream (SURVEY NEXT-4)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -224,6 +226,7 @@ def config_json(args, cfg, world):
             "parallelism": f"tables row-sharded over {world} GPU(s), data-parallel samples",
             "l2": "inputs larger than L2 (tables 4*rows*dim bytes, GB-scale per-step traffic)",
             "pipelined": "DBP (route t+1 on aux stream) + FWP (comm/compute streams)",
+            "tower_trained": bool(getattr(args, "tower_train", False)),
             "tables_in": "HBM" if getattr(args, "tables", "hbm") == "hbm" else
                          "pinned host DRAM (retrieval / refresh / write-back over PCIe)"}
 
@@ -289,7 +292,7 @@ def main():
                       max_recv_keys=int(1.5 * U) + 1024 if world > 1 else U + 1024,
                       max_mb_rows=mb_rows,
                       max_owner_mb_rows=int(1.5 * mb_rows) if world > 1 else 0,
-                      table_location=args.tables)
+                      table_location=args.tables, tower_train=args.tower_train and with_tower, tower_lr=1e-4)
     torch.cuda.synchronize()
     # inputs resident in HBM (value) and pinned host copies (e2e)
     dev_b = [(torch.from_numpy(k).to(dev), torch.from_numpy(o).to(dev), B) for k, o in batches]

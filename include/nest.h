@@ -112,6 +112,15 @@ typedef struct {
                                  into the HBM slot buffers, the write-back (R12) stores them back;
                                  everything else stays in HBM.  nest_create checks the pointer
                                  kind and returns NEST_ERR_INVALID on a mismatch. */
+  int32_t tower_train;        /* 0 (default): the stand-in tower is fixed (north_star).  1: trained
+                                 (P:461-462 dense gradients AllReduced on the
+                                 communication side): after the weight-gradient GEMMs (fp32 out) the
+                                 library sums dW over the ranks (ncclAllReduce on a communicator
+                                 split from the window's) and applies W -= tower_lr * sum_r dW_r to
+                                 fp32 master weights (bf16 copies feed the GEMMs), all on its dW
+                                 stream; the next tower call waits for it.  Collective: every rank
+                                 makes the same sequence of nest_tower_fwd_bwd* calls. */
+  float tower_lr;             /* step size of the trained tower (fp32) */
 } nest_config_t;
 
 /* Host-known counts of one slot after nest_route (all per this rank). */
@@ -284,6 +293,15 @@ NEST_API nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, 
  * read it finish (the next tower call, nest_join or nest_destroy). */
 NEST_API nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pooled, int64_t rows,
                                                float* dout, void* stream);
+
+/* Read the stand-in tower (tests): what = NEST_TOWER_WEIGHTS -> layer `layer`'s
+ * weights [H, in_l] row-major (in_0 = F*d, else H) as fp32 (the fp32 master
+ * copy when trained, else the bf16 weights widened); what = NEST_TOWER_TOP_GRAD
+ * -> the fixed top gradient [max_batch, H] (layer ignored).  `out` is device
+ * memory written on `stream` after the tower's pending work.  NEST_ERR_INVALID
+ * without a tower or with a bad layer / what. */
+enum { NEST_TOWER_WEIGHTS = 0, NEST_TOWER_TOP_GRAD = 1 };
+NEST_API nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, float* out, void* stream);
 
 /* Make `stream` wait for all work the library queued on its internal streams
  * (the tower's deferred weight-gradient GEMMs).  Host-side enqueue only. */

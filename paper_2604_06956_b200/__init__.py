@@ -46,6 +46,7 @@ class NestContext:
                  max_mb_rows: int = 0, max_owner_mb_rows: int = 0, seed: int = 0,
                  init_mode: str = "uniform", tower_layers: int = 0, tower_hidden: int = 1024,
                  optimizer: str = "sgd", adagrad_eps: float = 1e-8, table_location: str = "hbm",
+                 tower_train: bool = False, tower_lr: float = 1e-3,
                  nccl_uids: Optional[bytes] = None, device=None, init_tables: bool = True):
         import torch
         self.lib = L.load()
@@ -63,7 +64,8 @@ class NestContext:
             tower_layers=tower_layers, tower_hidden=tower_hidden,
             optimizer={"sgd": L.OPT_SGD, "rowwise_adagrad": L.OPT_ROWWISE_ADAGRAD}[optimizer],
             adagrad_eps=adagrad_eps,
-            table_location={"hbm": L.TABLE_HBM, "host": L.TABLE_HOST}[table_location])
+            table_location={"hbm": L.TABLE_HBM, "host": L.TABLE_HOST}[table_location],
+            tower_train=1 if tower_train else 0, tower_lr=tower_lr)
         self.table_location = table_location
         self.optimizer = optimizer
         self.world, self.rank, self.dim = world, rank, dim
@@ -156,6 +158,17 @@ class NestContext:
         """Stand-in tower on fp32 or bf16 pooled rows (-> nest_tower_fwd_bwd_bf16)."""
         fn = self.lib.nest_tower_fwd_bwd_bf16 if str(pooled.dtype) == "torch.bfloat16" else self.lib.nest_tower_fwd_bwd
         self._check(fn(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout), _stream(stream)))
+
+    def tower_read(self, what: str, layer: int = 0, stream=None):
+        """The tower's layer weights [H, in_l] or its fixed top gradient
+        [max_batch, H] as an fp32 device tensor (nest_tower_read)."""
+        torch = self.torch
+        H, in0 = self.cfg.tower_hidden, self.F * self.dim
+        shape = ((H, in0 if layer == 0 else H) if what == "weights" else (self.cfg.max_batch, H))
+        out = torch.empty(shape, dtype=torch.float32, device=self.device)
+        self._check(self.lib.nest_tower_read(self.ctx, {"weights": 0, "top_grad": 1}[what], layer, _ptr(out),
+                                             _stream(stream)))
+        return out
 
     def join(self, stream=None) -> None:
         """`stream` waits for the library's internal streams (nest_join)."""

@@ -46,6 +46,8 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
              "adagrad_eps must be >= 0");
   NEST_CHECK(cfg->table_location == NEST_TABLE_HBM || cfg->table_location == NEST_TABLE_HOST, NEST_ERR_INVALID,
              "bad table_location");
+  NEST_CHECK(cfg->tower_train == 0 || (cfg->tower_train == 1 && cfg->tower_layers > 0), NEST_ERR_INVALID,
+             "tower_train needs tower_layers > 0");
   c.rows.assign(cfg->table_rows, cfg->table_rows + c.T);
   for (int t = 0; t < c.T; ++t)
     NEST_CHECK(c.rows[t] >= 1 && c.rows[t] <= int64_t(kRowMask), NEST_ERR_INVALID, "bad table_rows");
@@ -796,6 +798,12 @@ nest_status_t nest_tower_fwd_bwd(nest_ctx_t* ctx, const float* pooled, int64_t r
 nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pooled, int64_t rows, float* dout,
                                       void* stream) {
   return tower_impl(reinterpret_cast<Ctx*>(ctx), pooled, true, rows, dout, stream);
+}
+
+nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, float* out, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { tower_read(*c, what, layer, out, S(stream)); });
 }
 
 nest_status_t nest_join(nest_ctx_t* ctx, void* stream) {

@@ -593,5 +593,6 @@ void tower_destroy(Ctx& c);
 // in place (they must stay unmodified until the deferred dW GEMMs finish)
 double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, float* dout, cudaStream_t st);
 void tower_join(Ctx& c, cudaStream_t st);
+void tower_read(Ctx& c, int what, int layer, float* out, cudaStream_t st);
 
 }  // namespace nest

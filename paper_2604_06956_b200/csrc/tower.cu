@@ -47,6 +47,13 @@ struct Tower {
   cudaEvent_t ev_dx = nullptr, ev_dw = nullptr;
   bool dw_pending = false;
   char* mem = nullptr;
+  // trained tower (NEXT-4): fp32 master weights, per-layer fp32 dW, the dense
+  // gradient AllReduce communicator (split from the window's, W > 1)
+  bool train = false;
+  float lr = 0.f;
+  float* w32 = nullptr;
+  float* dw32 = nullptr;
+  ncclComm_t comm = nullptr;
 };
 
 #define NEST_CUBLAS(call)                                                                 \
@@ -65,7 +72,9 @@ size_t tower_workspace_bytes(const Ctx& c) {
   elems += int64_t(std::max(L - 1, 1)) * bmax * H;   // dY of layers 0..L-2 (>= 1: forward scratch)
   elems += int64_t(H) * std::max<int64_t>(H, in0);   // dw
   elems += bmax * H;                                 // top gradient
-  return size_t(elems) * 2 + 2 * (32u << 20) + 8 * 256;
+  const int64_t wel = H * in0 + int64_t(L - 1) * H * H;
+  const size_t train = c.cfg.tower_train ? size_t(wel) * 2 * sizeof(float) + 256 : 0;  // w32 + dw32
+  return size_t(elems) * 2 + 2 * (32u << 20) + 8 * 256 + train;
 }
 
 void tower_bind(Ctx& c, char* mem) {
@@ -83,6 +92,21 @@ __global__ void k_fill_bf16(__nv_bfloat16* p, int64_t n, uint64_t seed, float sc
     z ^= z >> 31;
     const float u = float(uint32_t(z >> 40)) * 5.9604644775390625e-08f;  // [0,1)
     p[i] = __float2bfloat16((2.f * u - 1.f) * scale);
+  }
+}
+
+__global__ void k_widen_bf16(const __nv_bfloat16* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = __bfloat162float(in[i]);
+}
+
+// trained tower: w32 -= lr * dW (summed over ranks), bf16 copy for the GEMMs
+__global__ void k_dense_sgd(float* __restrict__ w32, __nv_bfloat16* __restrict__ w16,
+                            const float* __restrict__ dw, int64_t n, float lr) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float v = __fmaf_rn(-lr, dw[i], w32[i]);
+    w32[i] = v;
+    w16[i] = __float2bfloat16_rn(v);
   }
 }
 
@@ -117,6 +141,13 @@ void tower_create(Ctx& c) {
   t->gtop = w.take<__nv_bfloat16>(bmax * H);
   t->ws = w.take<char>(int64_t(t->ws_bytes));
   t->ws_dw = w.take<char>(int64_t(t->ws_bytes));
+  t->train = c.cfg.tower_train != 0;
+  t->lr = c.cfg.tower_lr;
+  if (t->train) {
+    t->w32 = w.take<float>(t->woff[L]);
+    t->dw32 = w.take<float>(t->woff[L]);
+    if (c.W > 1) NEST_NCCL(ncclCommSplit(c.comm, 0, c.rank, &t->comm, nullptr));
+  }
   {
     const char* dv = std::getenv("NEST_TOWER_DEFER_DW");
     t->defer_dw = !(dv && std::atoi(dv) == 0);
@@ -149,6 +180,7 @@ void tower_create(Ctx& c) {
     k_fill_bf16<<<1024, 256>>>(t->w + t->woff[l], int64_t(H) * fan_in, 1000 + l, 1.f / std::sqrt(float(fan_in)));
   }
   k_fill_bf16<<<1024, 256>>>(t->gtop, bmax * H, 77, 1.f / 1024.f);
+  if (t->train) k_widen_bf16<<<1024, 256>>>(t->w, t->w32, t->woff[L]);
   NEST_LAUNCH_CHECK();
   NEST_CUDA(cudaDeviceSynchronize());
 }
@@ -157,6 +189,7 @@ void tower_destroy(Ctx& c) {
   Tower* t = reinterpret_cast<Tower*>(c.tower);
   if (!t) return;
   if (t->h) cublasDestroy(t->h);
+  if (t->comm) ncclCommDestroy(t->comm);
   if (t->side) {
     cudaStreamSynchronize(t->side);
     cudaStreamDestroy(t->side);
@@ -286,9 +319,22 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
   const double flops_dw = 2.0 * M * (double(in0) * H + double(L - 1) * H * H);
   {
     ProfScope ps(c, ST_TOWER_DW, SK_AUX, ws);
-    for (int l = L - 1; l >= 0; --l)
-      gemm_rm(t, true, false, H, IN(l), M, DY(l), H, X(l), IN(l), t->dw, IN(l), CUDA_R_16BF, ws,
-              t->defer_dw ? t->ws_dw : t->ws);
+    for (int l = L - 1; l >= 0; --l) {
+      if (t->train)   // fp32 dW of every layer, kept for the AllReduce + update
+        gemm_rm(t, true, false, H, IN(l), M, DY(l), H, X(l), IN(l), t->dw32 + t->woff[l], IN(l), CUDA_R_32F,
+                ws, t->defer_dw ? t->ws_dw : t->ws);
+      else
+        gemm_rm(t, true, false, H, IN(l), M, DY(l), H, X(l), IN(l), t->dw, IN(l), CUDA_R_16BF, ws,
+                t->defer_dw ? t->ws_dw : t->ws);
+    }
+    if (t->train) {
+      // NEXT-4: dense gradients summed over the data-parallel ranks on the dW
+      // stream (the paper's communication-side AllReduce), then SGD
+      const int64_t n = t->woff[L];
+      if (t->comm) NEST_NCCL(ncclAllReduce(t->dw32, t->dw32, size_t(n), ncclFloat32, ncclSum, t->comm, ws));
+      k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, t->dw32, n, t->lr);
+      NEST_LAUNCH_CHECK();
+    }
     ps.bytes = flops_dw;
     ps.launches = 0;
   }
@@ -297,6 +343,26 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
     t->dw_pending = true;
   }
   return t->defer_dw ? 2.0 * flops_dw : 3.0 * flops_dw;   // FLOPs on `st` (fwd + dX [+ dW])
+}
+
+void tower_read(Ctx& c, int what, int layer, float* out, cudaStream_t st) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  NEST_CHECK(t != nullptr, NEST_ERR_INVALID, "no tower (tower_layers == 0)");
+  NEST_CHECK(out != nullptr, NEST_ERR_INVALID, "null out");
+  if (t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
+  if (what == NEST_TOWER_WEIGHTS) {
+    NEST_CHECK(layer >= 0 && layer < t->L, NEST_ERR_INVALID, "tower layer out of range");
+    const int64_t n = t->woff[layer + 1] - t->woff[layer];
+    if (t->train)
+      NEST_CUDA(cudaMemcpyAsync(out, t->w32 + t->woff[layer], sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+    else
+      k_widen_bf16<<<256, 256, 0, st>>>(t->w + t->woff[layer], out, n);
+  } else if (what == NEST_TOWER_TOP_GRAD) {
+    k_widen_bf16<<<256, 256, 0, st>>>(t->gtop, out, t->bmax * t->H);
+  } else {
+    throw Error{NEST_ERR_INVALID, "bad tower read kind"};
+  }
+  NEST_LAUNCH_CHECK();
 }
 
 // make `st` wait for outstanding dW GEMMs (context teardown / host reads)

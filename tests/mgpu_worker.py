@@ -47,6 +47,40 @@ def skewed_batches(cfg, B, T, world, seed=31):
     return out
 
 
+def tower_case(rank, world, dev):
+    """NEXT-4: the trained tower's dense gradients are summed over the ranks
+    (AllReduce) before the SGD step: W1 = W0 - lr * sum_r G^T X_r on every
+    rank, bitwise identical replicas."""
+    cfg = WL.CONFIGS["tiny"]
+    B, F, d, H, lr = 32, cfg.num_features, cfg.dim, 64, 0.01
+    obj = [unique_ids() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = NestContext(cfg.table_rows, d, world=world, rank=rank, max_keys=B * F * 3, max_batch=B,
+                      seed=2, nccl_uids=obj[0], device=dev, tower_layers=1, tower_hidden=H, tower_train=True,
+                      tower_lr=lr)
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    pooled = (torch.randn((B * F, d), generator=g, device=dev) * 0.5).to(torch.bfloat16)
+    dout = torch.empty((B * F, d), dtype=torch.float32, device=dev)
+    w0 = ctx.tower_read("weights", 0).cpu().double().numpy()
+    G = ctx.tower_read("top_grad").cpu().double().numpy()[:B]
+    ctx.tower_fwd_bwd(pooled, dout)
+    ctx.join()
+    torch.cuda.synchronize()
+    w1 = ctx.tower_read("weights", 0).cpu().numpy()
+    xs = [None] * world if rank == 0 else None
+    dist.gather_object((pooled.float().cpu().numpy(), w1), xs, dst=0)
+    ok = True
+    if rank == 0:
+        Xs = [x.astype(np.float64).reshape(B, F * d) for x, _ in xs]
+        ref = w0 - lr * sum(G.T @ X for X in Xs)
+        scale = np.abs(w0) + lr * sum(np.abs(G).T @ np.abs(X) for X in Xs)
+        ok = all(np.array_equal(xs[0][1], w) for _, w in xs) and \
+            bool(np.all(np.abs(xs[0][1].astype(np.float64) - ref) <= 1e-5 * scale + 1e-7))
+        print(f"[tower-train-allreduce] {'OK' if ok else 'FAIL'}", flush=True)
+    ctx.close()
+    return ok
+
+
 def run_case(name, cfg, B, N, T, init, dmode, lr, rank, world, dev, uids, gen=None, adagrad=None,
              tables="hbm"):
     F, d = cfg.num_features, cfg.dim
@@ -156,6 +190,7 @@ def main():
                                                               bag_repeats=True, dim=128),
                   512, 2, 3, "dyadic", "dyadic", 2.0 ** -12, None, None, "host"))
     all_ok = True
+    all_ok &= tower_case(rank, world, dev)
     for case in cases:
         obj = [unique_ids() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)

@@ -443,6 +443,39 @@ def test_edge_many_features_per_sample(d, N):
     _p1_check(cfg, batches, N=N)
 
 
+# --------------------------------------------------------------------------- trained tower (NEXT-4)
+def test_trained_tower_sgd_step_matches_definition():
+    """NEXT-4 at W=1: one tower call with tower_train applies W0 - lr * G^T X0
+    (L = 1: dW_0 = dY_0^T X_0 with dY_0 the fixed top gradient G) and returns
+    dX_0 = G W0, both against fp64 products of the same bf16 operands."""
+    cfg = WL.CONFIGS["tiny"]
+    B, F, d, H, lr = 32, cfg.num_features, cfg.dim, 64, 0.01
+    ctx = make_ctx(cfg, B, tower_layers=1, tower_hidden=H, tower_train=True, tower_lr=lr)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    pooled = (torch.randn((B * F, d), generator=g, device=DEV) * 0.5).to(torch.bfloat16)
+    dout = torch.empty((B * F, d), dtype=torch.float32, device=DEV)
+    w0 = ctx.tower_read("weights", 0).cpu().double().numpy()
+    G = ctx.tower_read("top_grad").cpu().double().numpy()[:B]
+    ctx.tower_fwd_bwd(pooled, dout)
+    ctx.join()
+    torch.cuda.synchronize()
+    w1 = ctx.tower_read("weights", 0).cpu().double().numpy()
+    X = pooled.float().cpu().double().numpy().reshape(B, F * d)
+    ref_w1 = w0 - lr * (G.T @ X)
+    assert np.all(np.abs(w1 - ref_w1) <= 1e-5 * (np.abs(w0) + lr * (np.abs(G).T @ np.abs(X))) + 1e-7)
+    ref_dx = G @ w0
+    got_dx = dout.cpu().double().numpy().reshape(B, F * d)
+    assert np.all(np.abs(got_dx - ref_dx) <= 1e-5 * (np.abs(G) @ np.abs(w0)) + 1e-7)
+    assert not np.array_equal(w1, w0)
+    # the fixed tower (default) leaves its weights alone
+    ctx2 = make_ctx(cfg, B, tower_layers=1, tower_hidden=H)
+    v0 = ctx2.tower_read("weights", 0).cpu().numpy()
+    ctx2.tower_fwd_bwd(pooled, dout)
+    ctx2.join()
+    torch.cuda.synchronize()
+    assert np.array_equal(ctx2.tower_read("weights", 0).cpu().numpy(), v0)
+
+
 # --------------------------------------------------------------------------- host-DRAM tier
 @pytest.mark.parametrize("N,pipelined,d", [(1, True, 16), (2, True, 16), (1, False, 128), (4, True, 128)])
 def test_host_tier_p1_bit_exact(N, pipelined, d):
