@@ -750,6 +750,11 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
 // range order.  Fixed ranges => a fixed summation order => bitwise
 // reproducible, whatever the grid; load balance does not depend on skew.
 constexpr int kSegRange = 256;
+// resident 256-thread blocks asked of ptxas for k_segsum_range (2: ~98
+// registers, 3: capped at 85)
+#ifndef NEST_SEGSUM_RANGE_MINB
+#define NEST_SEGSUM_RANGE_MINB 3
+#endif
 
 template <int D>
 __device__ __forceinline__ void finish_row(const PeerRows& out, int64_t k, float4 (&acc)[RowGeom<D>::VPL],
@@ -786,7 +791,7 @@ __device__ __forceinline__ void seg_finish(const PeerRows& out, int32_t k, int32
 // PRE: fused SGD (W == 1, N == 1, plain SGD) with the frozen rows prefetched
 // alongside the gradient row of the segment's first occurrence
 template <int D, int U, bool PRE>
-__global__ void __launch_bounds__(kRowThreads) k_segsum_range(int64_t Ki, const uint32_t* __restrict__ skey,
+__global__ void __launch_bounds__(kRowThreads, NEST_SEGSUM_RANGE_MINB) k_segsum_range(int64_t Ki, const uint32_t* __restrict__ skey,
                                                               uint32_t umask, const int32_t* __restrict__ pos,
                                                               const int32_t* __restrict__ sval,
                                                               const float* __restrict__ dout, const PeerRows out,
