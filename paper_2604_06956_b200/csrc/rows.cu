@@ -302,7 +302,12 @@ __device__ __forceinline__ uint32_t group_mask(const Grp<D>& gp) {
 // R8, pooled: lane group per sample of the micro-batch; bags of a sample are
 // contiguous in the batch's CSR, so the sample's occurrences are one run
 template <int D, bool W1, int U, typename OutT>
-__global__ void __launch_bounds__(kRowThreads) k_pool_stream(int64_t nsamp, int F,
+// resident blocks asked of ptxas: 4 (62 registers) measured best at W=1
+// (E step 1.43 ms; 5 blocks / 51 registers 1.46, 6 blocks / 40 + spills 1.47)
+#ifndef NEST_POOL_STREAM_MINB
+#define NEST_POOL_STREAM_MINB 4
+#endif
+__global__ void __launch_bounds__(kRowThreads, NEST_POOL_STREAM_MINB) k_pool_stream(int64_t nsamp, int F,
                                                              const int32_t* __restrict__ perm_mb,
                                                              const int32_t* __restrict__ bag_off,
                                                              const int32_t* __restrict__ inverse,
