@@ -49,17 +49,19 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
+    if not force and out == LIB and up_to_date():
         return LIB
     nv = _site_nvidia()
     nccl_inc, nccl_lib = os.path.join(nv, "nccl", "include"), os.path.join(nv, "nccl", "lib")
     cublas_inc, cublas_lib = os.path.join(nv, "cublas", "include"), os.path.join(nv, "cublas", "lib")
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--extended-lambda",
            "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
            "-Xptxas", "-warn-spills",
            "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-I", cublas_inc,
+           # NEST_NVCC_EXTRA: extra -D flags for tuning builds (e.g. -DNEST_SEG_RANGE=128)
+           *os.environ.get("NEST_NVCC_EXTRA", "").split(),
            *sources(),
            "-L", nccl_lib, "-L", cublas_lib, "-l:libnccl.so.2", "-l:libcublas.so.12", "-l:libcublasLt.so.12",
            "-Xlinker", f"-rpath={nccl_lib}:{cublas_lib}",
@@ -71,8 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
     if verbose and (r.stdout or r.stderr):
         print(r.stdout + r.stderr, file=sys.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

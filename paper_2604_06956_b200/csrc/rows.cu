@@ -754,7 +754,10 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
 // where it starts lists itself, and k_segsum_fix sums B[w] + A[w+1] + ... in
 // range order.  Fixed ranges => a fixed summation order => bitwise
 // reproducible, whatever the grid; load balance does not depend on skew.
-constexpr int kSegRange = 256;
+#ifndef NEST_SEG_RANGE
+#define NEST_SEG_RANGE 256
+#endif
+constexpr int kSegRange = NEST_SEG_RANGE;
 // resident 256-thread blocks asked of ptxas for k_segsum_range (2: ~98
 // registers, 3: capped at 85)
 #ifndef NEST_SEGSUM_RANGE_MINB
