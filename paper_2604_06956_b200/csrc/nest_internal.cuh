@@ -289,6 +289,26 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
 __device__ __forceinline__ float4 ldg_f4(const float* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
 }
+// read-only loads with an L2 eviction priority: evict_last for rows read again
+// soon (a bag's dout row, once per occurrence), evict_first for rows read once
+__device__ __forceinline__ float4 ldg_f4_hint(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ldg_f4_el(const float* p) { return ldg_f4_hint(p, l2_policy_evict_last()); }
+__device__ __forceinline__ float4 ldg_f4_ef(const float* p) { return ldg_f4_hint(p, l2_policy_evict_first()); }
 __device__ __forceinline__ float4 ld_f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st_f4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 // streaming store (evict-first) for write-once outputs

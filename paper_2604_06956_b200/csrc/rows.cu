@@ -754,6 +754,11 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
 // where it starts lists itself, and k_segsum_fix sums B[w] + A[w+1] + ... in
 // range order.  Fixed ranges => a fixed summation order => bitwise
 // reproducible, whatever the grid; load balance does not depend on skew.
+// L2 eviction hints in k_segsum_range: dout rows evict_last (read once per
+// occurrence), frozen rows evict_first (read once)
+#ifndef NEST_SEGSUM_L2HINT
+#define NEST_SEGSUM_L2HINT 0
+#endif
 #ifndef NEST_SEG_RANGE
 #define NEST_SEG_RANGE 256
 #endif
@@ -849,10 +854,14 @@ __global__ void __launch_bounds__(kRowThreads, NEST_SEGSUM_RANGE_MINB) k_segsum_
           ss[k] = PRE ? __shfl_sync(gm, s_l, sl, L) : 0;
           if (t < n) {
 #pragma unroll
-            for (int v = 0; v < VPL; ++v) x[k][v] = ldg_f4(dout + int64_t(r) * D + gp.col(v));
+            for (int v = 0; v < VPL; ++v)
+              x[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_el(dout + int64_t(r) * D + gp.col(v))
+                                           : ldg_f4(dout + int64_t(r) * D + gp.col(v));
             if (PRE && ((heads >> t) & 1u))
 #pragma unroll
-              for (int v = 0; v < VPL; ++v) ex[k][v] = ldg_f4(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v));
+              for (int v = 0; v < VPL; ++v)
+                ex[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_ef(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v))
+                                              : ldg_f4(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v));
           }
         }
 #pragma unroll
