@@ -307,6 +307,21 @@ def test_cluster_bit_exact_vs_oracle(case):
     assert np.array_equal(mbo.cpu().numpy(), ref_mbo)
 
 
+def test_cluster_hand_worked_example_gpu():
+    """R14 on the hand-worked multi-round example of
+    tests/test_oracle_pins.py::test_cluster_rounds_hand_worked (admission sizes
+    1, 1, 1, 2; ties broken by growth and by id): the GPU greedy gives the
+    hand-derived partition."""
+    from test_oracle_pins import HAND_KEYSETS, HAND_PERM
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(64,), bag_len=(1, 4))
+    keys = np.array([k for ks in HAND_KEYSETS for k in sorted(ks)], np.int64)     # table 0, row = key
+    offs = np.concatenate([[0], np.cumsum([len(ks) for ks in HAND_KEYSETS])]).astype(np.int32)
+    ctx = make_ctx(cfg, 12, N=2, K=len(keys))
+    perm, mbo = ctx.fwp_schedule(to_dev(keys, torch.int64), to_dev(offs, torch.int32), 12, 2, "clustered")
+    assert perm.cpu().numpy().tolist() == HAND_PERM
+    assert mbo.cpu().numpy().tolist() == [0, 6, 12]
+
+
 def test_cluster_repeated_batches_same_shape():
     """The captured round sequence is replayed for later batches of the same
     shape, including batches whose largest sample (smax, hence the number of
