@@ -225,7 +225,9 @@ def config_json(args, cfg, world):
                     "fixed seeded loss gradient of the pooled rows (N(0, 1e-2))",
             "parallelism": f"tables row-sharded over {world} GPU(s), data-parallel samples",
             "l2": "inputs larger than L2 (tables 4*rows*dim bytes, GB-scale per-step traffic)",
-            "pipelined": "DBP (route t+1 on aux stream) + FWP (comm/compute streams)",
+            "pipelined": "DBP (route t+1 on the aux stream)" + (
+                f" + FWP ({args.micro_batches} micro-batches, comm/compute streams)" if args.micro_batches > 1
+                else "; FWP off (1 micro-batch; FWP at N=2 measured alongside when W > 1)"),
             "tower_trained": bool(getattr(args, "tower_train", False)),
             "tables_in": "HBM" if getattr(args, "tables", "hbm") == "hbm" else
                          "pinned host DRAM (retrieval / refresh / write-back over PCIe)"}
@@ -309,7 +311,7 @@ def main():
             return torch.bfloat16
         return torch.float32
 
-    def make_dout_fn(variant):
+    def make_dout_fn(variant, n_mb):
         if variant == "et":
             douts = {}
 
@@ -318,6 +320,9 @@ def main():
                 if key not in douts:
                     douts[key] = torch.empty(pooled.shape, dtype=torch.float32, device=dev)
                 ctx.tower_fwd_bwd(pooled, douts[key], stream=torch.cuda.current_stream())  # dense lane
+                if i == n_mb - 1:
+                    # trained tower: one dense AllReduce + SGD per batch (no-op when fixed)
+                    ctx.tower_step(stream=torch.cuda.current_stream())
                 return douts[key]
             return fn
         fixed = {}
@@ -337,7 +342,7 @@ def main():
 
     def timed(runner, steps, t0, source=None, profile=False, variant=None):
         """Runs `steps` steps; returns device ms (max over ranks)."""
-        dout_fn = make_dout_fn(variant or args.variant)
+        dout_fn = make_dout_fn(variant or args.variant, runner.N)
         barrier()
         if profile:
             ctx.profile_enable(True)

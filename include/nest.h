@@ -114,12 +114,16 @@ typedef struct {
                                  kind and returns NEST_ERR_INVALID on a mismatch. */
   int32_t tower_train;        /* 0 (default): the stand-in tower is fixed (north_star).  1: trained
                                  (P:461-462 dense gradients AllReduced on the
-                                 communication side): after the weight-gradient GEMMs (fp32 out) the
-                                 library sums dW over the ranks (ncclAllReduce on a communicator
-                                 split from the window's) and applies W -= tower_lr * sum_r dW_r to
-                                 fp32 master weights (bf16 copies feed the GEMMs), all on its dW
+                                 communication side): the weight-gradient GEMMs of every tower call
+                                 of a batch (one per micro-batch) accumulate into one fp32 dW, so
+                                 all micro-batches of the window see the same frozen weights
+                                 (Prop. 2, Corollary 1); nest_tower_step then sums dW
+                                 over the ranks (ncclAllReduce on a communicator split from the
+                                 window's) and applies W -= tower_lr * sum_r dW_r to fp32 master
+                                 weights (bf16 copies feed the GEMMs) once, on the library's dW
                                  stream; the next tower call waits for it.  Collective: every rank
-                                 makes the same sequence of nest_tower_fwd_bwd* calls. */
+                                 makes the same sequence of nest_tower_fwd_bwd* / nest_tower_step
+                                 calls. */
   float tower_lr;             /* step size of the trained tower (fp32) */
 } nest_config_t;
 
@@ -258,8 +262,10 @@ NEST_API nest_status_t nest_lookup_prefetch(nest_ctx_t* ctx, int32_t slot, int32
  * to the owners.  After the last micro-batch (mb == N-1) every owner sums its
  * received gradients in (micro-batch, source) order and applies the
  * sparse SGD update e <- e - lr_over_B * g (Eq. 2),
- * writing the updated rows to the slot buffer and back to the shard
- * (write-back).  dout: fp32 [mb_out_rows, d] in out's layout.
+ * computed from the slot buffer's frozen rows and written back to the shard
+ * only (write-back): the slot buffer is not rewritten; the next slot's
+ * buffer receives the written-back rows of the shared keys from
+ * nest_dbp_refresh.  dout: fp32 [mb_out_rows, d] in out's layout.
  * lr_over_B = eta / |B_global|. */
 NEST_API nest_status_t nest_grad_bwd_update(nest_ctx_t* ctx, int32_t slot, int32_t mb,
                                    const float* dout, float lr_over_B,
@@ -302,6 +308,15 @@ NEST_API nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pool
  * without a tower or with a bad layer / what. */
 enum { NEST_TOWER_WEIGHTS = 0, NEST_TOWER_TOP_GRAD = 1 };
 NEST_API nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, float* out, void* stream);
+
+/* Trained tower (tower_train = 1, NEXT-4): apply the batch's accumulated
+ * dense gradient -- AllReduce over the ranks + one SGD step -- after the last
+ * micro-batch's nest_tower_fwd_bwd* call (one dense update per
+ * batch).  Enqueued behind the dW GEMMs on the library's dW stream, after the
+ * work queued on `stream`; the next tower call waits for it.  No-op for the
+ * fixed tower or when no tower call happened since the last step;
+ * NEST_ERR_INVALID without a tower. */
+NEST_API nest_status_t nest_tower_step(nest_ctx_t* ctx, void* stream);
 
 /* Make `stream` wait for all work the library queued on its internal streams
  * (the tower's deferred weight-gradient GEMMs).  Host-side enqueue only. */

@@ -159,6 +159,11 @@ class NestContext:
         fn = self.lib.nest_tower_fwd_bwd_bf16 if str(pooled.dtype) == "torch.bfloat16" else self.lib.nest_tower_fwd_bwd
         self._check(fn(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout), _stream(stream)))
 
+    def tower_step(self, stream=None) -> None:
+        """Trained tower: AllReduce + SGD of the batch's accumulated dW, once
+        after its last micro-batch (nest_tower_step; no-op for the fixed tower)."""
+        self._check(self.lib.nest_tower_step(self.ctx, _stream(stream)))
+
     def tower_read(self, what: str, layer: int = 0, stream=None):
         """The tower's layer weights [H, in_l] or its fixed top gradient
         [max_batch, H] as an fp32 device tensor (nest_tower_read)."""

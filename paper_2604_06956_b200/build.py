@@ -42,8 +42,21 @@ def headers():
         [os.path.join(ROOT, "include", "nest.h")]
 
 
+STAMP = LIB + ".cmd"   # the nvcc command line libnest.so was built with
+
+
+def _extra() -> list:
+    # NEST_NVCC_EXTRA: extra -D flags for tuning builds (e.g. -DNEST_SEG_RANGE=128)
+    return os.environ.get("NEST_NVCC_EXTRA", "").split()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    """libnest.so is newer than every source AND was built with the default
+    flags (a tuning build with NEST_NVCC_EXTRA writes a different stamp, so a
+    later default build() replaces it instead of silently reusing it)."""
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return False
+    if open(STAMP).read().strip() != " ".join(_extra()):
         return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
@@ -60,8 +73,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
            "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-shared",
            "-Xptxas", "-warn-spills",
            "-I", os.path.join(ROOT, "include"), "-I", nccl_inc, "-I", cublas_inc,
-           # NEST_NVCC_EXTRA: extra -D flags for tuning builds (e.g. -DNEST_SEG_RANGE=128)
-           *os.environ.get("NEST_NVCC_EXTRA", "").split(),
+           *_extra(),
            *sources(),
            "-L", nccl_lib, "-L", cublas_lib, "-l:libnccl.so.2", "-l:libcublas.so.12", "-l:libcublasLt.so.12",
            "-Xlinker", f"-rpath={nccl_lib}:{cublas_lib}",
@@ -74,6 +86,9 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
     if verbose and (r.stdout or r.stderr):
         print(r.stdout + r.stderr, file=sys.stderr)
     os.replace(tmp, out)
+    if out == LIB:
+        with open(STAMP, "w") as f:
+            f.write(" ".join(_extra()))
     return out
 
 

@@ -48,6 +48,9 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
              "bad table_location");
   NEST_CHECK(cfg->tower_train == 0 || (cfg->tower_train == 1 && cfg->tower_layers > 0), NEST_ERR_INVALID,
              "tower_train needs tower_layers > 0");
+  // checked here, before any collective initialisation (tower_create repeats it)
+  NEST_CHECK(cfg->tower_layers <= 0 || (cfg->tower_hidden >= 16 && cfg->tower_hidden % 16 == 0),
+             NEST_ERR_INVALID, "tower_hidden must be a positive multiple of 16");
   c.rows.assign(cfg->table_rows, cfg->table_rows + c.T);
   for (int t = 0; t < c.T; ++t)
     NEST_CHECK(c.rows[t] >= 1 && c.rows[t] <= int64_t(kRowMask), NEST_ERR_INVALID, "bad table_rows");
@@ -399,7 +402,9 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
     if (c->cfg.tower_layers > 0) tower_create(*c);
   });
   if (st != NEST_OK) {
-    delete c;
+    // release whatever was created before the failure (pinned mirrors, events,
+    // communicators, the IPC window, the tower): nest_destroy skips null members
+    nest_destroy(reinterpret_cast<nest_ctx_t*>(c));
     return st;
   }
   *out = reinterpret_cast<nest_ctx_t*>(c);
@@ -667,7 +672,7 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
       {
         ProfScope ps(*c, ST_SEGSUM, SK_COMPUTE, cs);
         launch_segsum_sgd(*c, s, dout, opt, cs);
-        ps.launches = s.info.mb_uniq[0] > 0 ? 7 : 0;
+        ps.launches = s.info.mb_uniq[0] > 0 ? segsum_launches(*c) : 0;
         // N7 + N8 without the gradient-row round trip: gradient rows read +
         // 4 K + frozen rows read + rows written back
         ps.bytes = row * double(s.info.mb_out_rows[0]) + 4.0 * double(s.info.mb_nnz[0]) +
@@ -702,7 +707,7 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
       } else {
         launch_segsum(*c, s, mb, dout, cs);
       }
-      ps.launches = s.info.mb_uniq[mb] > 0 ? 7 : 0;
+      ps.launches = s.info.mb_uniq[mb] > 0 ? segsum_launches(*c) : 0;
       if (fused) {
         // accounted as the gradient All2All: rows stored off-GPU
         const int64_t self = s.all[(size_t(c->rank) * c->W + c->rank) * (c->Nmax + 2) + 1 + mb];
@@ -804,6 +809,12 @@ nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, floa
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] { tower_read(*c, what, layer, out, S(stream)); });
+}
+
+nest_status_t nest_tower_step(nest_ctx_t* ctx, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { tower_step(*c, S(stream)); });
 }
 
 nest_status_t nest_join(nest_ctx_t* ctx, void* stream) {

@@ -307,8 +307,6 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ float4 ldg_f4_el(const float* p) { return ldg_f4_hint(p, l2_policy_evict_last()); }
-__device__ __forceinline__ float4 ldg_f4_ef(const float* p) { return ldg_f4_hint(p, l2_policy_evict_first()); }
 __device__ __forceinline__ float4 ld_f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st_f4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 // streaming store (evict-first) for write-once outputs
@@ -530,6 +528,7 @@ void launch_send_gather(Ctx& c, Slot& s, int mb, cudaStream_t st, float* out_row
 // out: fp32 rows, or bf16 rows (pooled sum only) when bf16
 void launch_pool(Ctx& c, Slot& s, int mb, void* out, bool bf16, cudaStream_t st);
 void launch_segsum(Ctx& c, Slot& s, int mb, const float* dout, cudaStream_t st);
+int segsum_launches(const Ctx& c);
 void launch_refresh(Ctx& c, Slot& a, Slot& p, cudaStream_t st);
 void launch_read_rows(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 void launch_schedule(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz, int B, int N, int mode,
@@ -613,6 +612,7 @@ void tower_destroy(Ctx& c);
 // in place (they must stay unmodified until the deferred dW GEMMs finish)
 double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, float* dout, cudaStream_t st);
 void tower_join(Ctx& c, cudaStream_t st);
+void tower_step(Ctx& c, cudaStream_t st);
 void tower_read(Ctx& c, int what, int layer, float* out, cudaStream_t st);
 
 }  // namespace nest

@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
 }
 
 // ---------------------------------------------------------------------------
-// One-sweep LSD radix (default): one histogram pass counts the digits of every
+// One-sweep LSD radix (NEST_RADIX=onesweep; not the default, see
+// radix_classic below): one histogram pass counts the digits of every
 // pass at once (digit counts do not depend on the order), then each pass is a
 // single scatter kernel.  Tiles take their index from an atomic counter (so
 // every tile a block waits for is already running), rank their items exactly

@@ -763,6 +763,8 @@ __global__ void __launch_bounds__(kRowThreads) k_segsum_hot_final(
 #define NEST_SEG_RANGE 256
 #endif
 constexpr int kSegRange = NEST_SEG_RANGE;
+// c.partial holds Pcap = 2 * Kcap / 32 + 64 rows (api.cu) >= 2 * ceil(K / R) for R >= 32
+static_assert(kSegRange >= 32, "NEST_SEG_RANGE must be >= 32 (partial-row capacity)");
 // resident 256-thread blocks asked of ptxas for k_segsum_range (2: ~98
 // registers, 3: capped at 85)
 #ifndef NEST_SEGSUM_RANGE_MINB
@@ -815,6 +817,9 @@ __global__ void __launch_bounds__(kRowThreads, NEST_SEGSUM_RANGE_MINB) k_segsum_
   constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
   const uint32_t gm = group_mask<D>(gp);
   const int64_t nr = (Ki + kSegRange - 1) / kSegRange;
+  // L2 policies created once per thread (NEST_SEGSUM_L2HINT builds only)
+  const uint64_t pol_el = NEST_SEGSUM_L2HINT ? l2_policy_evict_last() : 0;
+  const uint64_t pol_ef = NEST_SEGSUM_L2HINT ? l2_policy_evict_first() : 0;
   for (int64_t w = gp.g; w < nr; w += gp.ng) {
     const int64_t q0 = w * kSegRange, q1 = (q0 + kSegRange < Ki ? q0 + kSegRange : Ki);
     const uint32_t ufirst = __ldg(skey + q0) & umask;
@@ -855,12 +860,12 @@ __global__ void __launch_bounds__(kRowThreads, NEST_SEGSUM_RANGE_MINB) k_segsum_
           if (t < n) {
 #pragma unroll
             for (int v = 0; v < VPL; ++v)
-              x[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_el(dout + int64_t(r) * D + gp.col(v))
+              x[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_hint(dout + int64_t(r) * D + gp.col(v), pol_el)
                                            : ldg_f4(dout + int64_t(r) * D + gp.col(v));
             if (PRE && ((heads >> t) & 1u))
 #pragma unroll
               for (int v = 0; v < VPL; ++v)
-                ex[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_ef(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v))
+                ex[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_hint(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v), pol_ef)
                                               : ldg_f4(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v));
           }
         }
@@ -1171,6 +1176,10 @@ static bool segsum_chunks(const Ctx& c) {
   }();
   return v < 0 ? c.W > 1 : v == 1;
 }
+// kernels one launch_segsum* call issues for a non-empty micro-batch (profile
+// bookkeeping): range form = k_segsum_range + k_segsum_fix + k_segsum_fix_big;
+// chunked form = k_seg_heads + 3-kernel scan + cold + hot chunks + hot final
+int segsum_launches(const Ctx& c) { return segsum_chunks(c) ? 7 : 3; }
 void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows& out, cudaStream_t st) {
   const int64_t Ui = s.info.mb_uniq[mb];
   const int64_t Ki = s.info.mb_nnz[mb];

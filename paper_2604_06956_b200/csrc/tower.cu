@@ -38,6 +38,8 @@ struct Tower {
   std::vector<int64_t> xoff;
   __nv_bfloat16* dy = nullptr;      // dY_l for l = 0..L-2 (layer l's output), [L-1][bmax, H]
   __nv_bfloat16* dw = nullptr;      // [H, max in]
+  int acc = 0;                      // micro-batches accumulated into dw32 since the last tower_step
+  int64_t acc_rows = 0;             // their rows (the next call's top-gradient offset)
   __nv_bfloat16* gtop = nullptr;    // [bmax, H] fixed top gradient dY_{L-1}
   void* ws = nullptr;               // cuBLASLt workspace of the caller's stream
   void* ws_dw = nullptr;            // ... and of the dW stream
@@ -234,8 +236,8 @@ static GemmPlan& plan_for(Tower* t, bool ta, bool tb, int M, int N, int K, int l
 
 static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void* A, int lda,
                     const void* B, int ldb, void* C, int ldc, cudaDataType ctype, cudaStream_t st,
-                    void* ws) {
-  const float alpha = 1.f, beta = 0.f;
+                    void* ws, float beta = 0.f) {
+  const float alpha = 1.f;
   GemmPlan& p = plan_for(t, ta, tb, M, N, K, lda, ldb, ldc, ctype);
   if (!p.have_algo) {
     cublasLtMatmulPreference_t pref;
@@ -247,6 +249,15 @@ static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void*
     NEST_CUBLAS(cublasLtMatmulAlgoGetHeuristic(t->lt, p.op, p.a, p.b, p.c, p.c, pref, 8, res, &n));
     cublasLtMatmulPreferenceDestroy(pref);
     NEST_CHECK(n > 0, NEST_ERR_CUDA, "no cublasLt algorithm for a tower GEMM");
+    // timing runs overwrite C (beta 0); an accumulating call (beta 1) saves C
+    // first and restores it after tuning
+    const float tune_beta = 0.f;
+    void* saved = nullptr;
+    const size_t cbytes = size_t(M) * ldc * (ctype == CUDA_R_32F ? 4 : 2);
+    if (beta != 0.f) {
+      NEST_CUDA(cudaMallocAsync(&saved, cbytes, st));
+      NEST_CUDA(cudaMemcpyAsync(saved, C, cbytes, cudaMemcpyDeviceToDevice, st));
+    }
     cudaEvent_t e0, e1;
     NEST_CUDA(cudaEventCreate(&e0));
     NEST_CUDA(cudaEventCreate(&e1));
@@ -257,7 +268,7 @@ static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void*
       bool ok = true;
       for (int rep = 0; rep < 3 && ok; ++rep) {  // warm + 2 timed
         if (rep == 1) cudaEventRecord(e0, st);
-        ok = cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &beta, C, p.c, C, p.c, &res[i].algo, ws,
+        ok = cublasLtMatmul(t->lt, p.op, &alpha, B, p.a, A, p.b, &tune_beta, C, p.c, C, p.c, &res[i].algo, ws,
                             t->ws_bytes, st) == CUBLAS_STATUS_SUCCESS;
       }
       if (!ok) continue;
@@ -273,6 +284,10 @@ static void gemm_rm(Tower* t, bool ta, bool tb, int M, int N, int K, const void*
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     NEST_CHECK(best < 1e29f, NEST_ERR_CUDA, "no working cublasLt algorithm for a tower GEMM");
+    if (saved) {
+      NEST_CUDA(cudaMemcpyAsync(C, saved, cbytes, cudaMemcpyDeviceToDevice, st));
+      NEST_CUDA(cudaFreeAsync(saved, st));
+    }
     p.algo = res[bi].algo;
     p.have_algo = true;
   }
@@ -291,7 +306,13 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
                                   : t->x;
   auto X = [&](int l) { return l == 0 ? x0 : t->x + t->xoff[l]; };
   auto W = [&](int l) { return t->w + t->woff[l]; };
-  auto DY = [&](int l) { return l == L - 1 ? t->gtop : t->dy + int64_t(l) * t->bmax * H; };
+  // the fixed top gradient of a row is its position in the window: a trained
+  // tower's micro-batches take consecutive slices (rows accumulated since the
+  // last tower_step), so N micro-batches see the same top gradient as one
+  // full-batch call (sequential schedule); the fixed tower always starts at 0
+  const int64_t g0 = t->train ? t->acc_rows : 0;
+  NEST_CHECK(g0 + bm <= t->bmax, NEST_ERR_CAPACITY, "tower rows of one window exceed max_batch");
+  auto DY = [&](int l) { return l == L - 1 ? t->gtop + g0 * H : t->dy + int64_t(l) * t->bmax * H; };
   auto IN = [&](int l) { return l == 0 ? in0 : H; };
   // the previous call's dW GEMMs still read X and dY
   if (t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
@@ -319,21 +340,22 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
   const double flops_dw = 2.0 * M * (double(in0) * H + double(L - 1) * H * H);
   {
     ProfScope ps(c, ST_TOWER_DW, SK_AUX, ws);
+    // trained tower: the micro-batches of one window accumulate into the fp32
+    // dW (beta 0 on the first, 1 after: one gradient per batch, Prop. 2 /
+    // Corollary 1 -- every micro-batch sees the same frozen weights); the
+    // AllReduce + SGD run once, in tower_step after the window's last tower call
+    const float beta = t->acc > 0 ? 1.f : 0.f;
     for (int l = L - 1; l >= 0; --l) {
       if (t->train)   // fp32 dW of every layer, kept for the AllReduce + update
         gemm_rm(t, true, false, H, IN(l), M, DY(l), H, X(l), IN(l), t->dw32 + t->woff[l], IN(l), CUDA_R_32F,
-                ws, t->defer_dw ? t->ws_dw : t->ws);
+                ws, t->defer_dw ? t->ws_dw : t->ws, beta);
       else
         gemm_rm(t, true, false, H, IN(l), M, DY(l), H, X(l), IN(l), t->dw, IN(l), CUDA_R_16BF, ws,
                 t->defer_dw ? t->ws_dw : t->ws);
     }
     if (t->train) {
-      // NEXT-4: dense gradients summed over the data-parallel ranks on the dW
-      // stream (the paper's communication-side AllReduce), then SGD
-      const int64_t n = t->woff[L];
-      if (t->comm) NEST_NCCL(ncclAllReduce(t->dw32, t->dw32, size_t(n), ncclFloat32, ncclSum, t->comm, ws));
-      k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, t->dw32, n, t->lr);
-      NEST_LAUNCH_CHECK();
+      ++t->acc;
+      t->acc_rows += bm;
     }
     ps.bytes = flops_dw;
     ps.launches = 0;
@@ -343,6 +365,34 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
     t->dw_pending = true;
   }
   return t->defer_dw ? 2.0 * flops_dw : 3.0 * flops_dw;   // FLOPs on `st` (fwd + dX [+ dW])
+}
+
+// NEXT-4 update, once per batch after its last micro-batch: dense gradients
+// summed over the data-parallel ranks (the paper's communication-side
+// AllReduce) and SGD on the fp32 master weights + their bf16 copy,
+// on the dW stream behind the accumulated dW GEMMs; the next tower call waits
+// for it.  No-op for the fixed tower or when nothing was accumulated.
+void tower_step(Ctx& c, cudaStream_t st) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  NEST_CHECK(t != nullptr, NEST_ERR_INVALID, "no tower (tower_layers == 0)");
+  if (!t->train || t->acc == 0) return;
+  cudaStream_t ws = st;
+  if (t->defer_dw) {
+    // behind the accumulated dW GEMMs on the side stream (ev_dw) and the caller's work
+    NEST_CUDA(cudaEventRecord(t->ev_dx, st));
+    NEST_CUDA(cudaStreamWaitEvent(t->side, t->ev_dx, 0));
+    ws = t->side;
+  }
+  const int64_t n = t->woff[t->L];
+  if (t->comm) NEST_NCCL(ncclAllReduce(t->dw32, t->dw32, size_t(n), ncclFloat32, ncclSum, t->comm, ws));
+  k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, t->dw32, n, t->lr);
+  NEST_LAUNCH_CHECK();
+  t->acc = 0;
+  t->acc_rows = 0;
+  if (t->defer_dw) {
+    NEST_CUDA(cudaEventRecord(t->ev_dw, t->side));
+    t->dw_pending = true;
+  }
 }
 
 void tower_read(Ctx& c, int what, int layer, float* out, cudaStream_t st) {

@@ -64,6 +64,7 @@ def tower_case(rank, world, dev):
     w0 = ctx.tower_read("weights", 0).cpu().double().numpy()
     G = ctx.tower_read("top_grad").cpu().double().numpy()[:B]
     ctx.tower_fwd_bwd(pooled, dout)
+    ctx.tower_step()
     ctx.join()
     torch.cuda.synchronize()
     w1 = ctx.tower_read("weights", 0).cpu().numpy()

@@ -474,6 +474,11 @@ def test_trained_tower_sgd_step_matches_definition():
     ctx.tower_fwd_bwd(pooled, dout)
     ctx.join()
     torch.cuda.synchronize()
+    # no update before nest_tower_step (the window's micro-batches accumulate)
+    assert np.array_equal(ctx.tower_read("weights", 0).cpu().double().numpy(), w0)
+    ctx.tower_step()
+    ctx.join()
+    torch.cuda.synchronize()
     w1 = ctx.tower_read("weights", 0).cpu().double().numpy()
     X = pooled.float().cpu().double().numpy().reshape(B, F * d)
     ref_w1 = w0 - lr * (G.T @ X)
@@ -486,9 +491,44 @@ def test_trained_tower_sgd_step_matches_definition():
     ctx2 = make_ctx(cfg, B, tower_layers=1, tower_hidden=H)
     v0 = ctx2.tower_read("weights", 0).cpu().numpy()
     ctx2.tower_fwd_bwd(pooled, dout)
+    ctx2.tower_step()
     ctx2.join()
     torch.cuda.synchronize()
     assert np.array_equal(ctx2.tower_read("weights", 0).cpu().numpy(), v0)
+
+
+@pytest.mark.parametrize("L", [1, 3])
+def test_trained_tower_micro_batches_accumulate(L):
+    """ADVICE r01 / Prop. 2: with FWP the tower runs once per
+    micro-batch, but the window's weights stay frozen and the batch makes ONE
+    dense update -- N = 2 micro-batch calls + tower_step reach the weights of
+    one full-batch call + tower_step (fp32 dW accumulation: same terms, other
+    rounding order), and both micro-batches' input gradients use W0."""
+    cfg = WL.CONFIGS["tiny"]
+    B, F, d, H, lr = 32, cfg.num_features, cfg.dim, 64, 0.05
+    g = torch.Generator(device=DEV).manual_seed(5)
+    pooled = (torch.randn((B * F, d), generator=g, device=DEV) * 0.5).to(torch.bfloat16)
+    res = []
+    for N in (1, 2):
+        ctx = make_ctx(cfg, B, tower_layers=L, tower_hidden=H, tower_train=True, tower_lr=lr)
+        dout = torch.empty((B * F, d), dtype=torch.float32, device=DEV)
+        rows = B * F // N
+        for i in range(N):
+            ctx.tower_fwd_bwd(pooled[i * rows:(i + 1) * rows], dout[i * rows:(i + 1) * rows])
+        ctx.tower_step()
+        ctx.join()
+        torch.cuda.synchronize()
+        res.append(([ctx.tower_read("weights", l).cpu().double().numpy() for l in range(L)],
+                    dout.cpu().double().numpy()))
+        w0 = make_ctx(cfg, B, tower_layers=L, tower_hidden=H, tower_train=True,
+                      tower_lr=lr).tower_read("weights", 0).cpu().double().numpy()
+        assert not np.allclose(res[-1][0][0], w0)
+    (wa, da), (wb, db) = res
+    for a, b in zip(wa, wb):
+        assert np.allclose(a, b, rtol=1e-4, atol=1e-6), float(np.abs(a - b).max())
+    # the input gradients of both micro-batches came from the same weights
+    # (the top gradient is per row of the batch, so the halves match the full run)
+    assert np.allclose(da, db, rtol=1e-3, atol=1e-5)
 
 
 # --------------------------------------------------------------------------- host-DRAM tier
