@@ -174,13 +174,47 @@ NEST_API nest_status_t nest_workspace_bytes(const nest_config_t* cfg, size_t* ta
 NEST_API int64_t nest_shard_rows(const nest_config_t* cfg);
 
 /* Creates a context.  nccl_uids: host, 2 x 128 bytes (main and aux
- * communicator) from nest_get_unique_id on rank 0, or NULL when world == 1.
- * Collective over all ranks (ncclCommInitRank).  table_mem / work_mem: device
- * buffers of at least the queried sizes, 256-byte aligned. */
+ * communicator) from nest_get_unique_id on rank 0 -- collective over all ranks
+ * (ncclCommInitRank), the exchange windows are connected through NCCL -- or
+ * NULL.  NULL with world == 1: no communication at all.  NULL with world > 1:
+ * no NCCL (every exchange of the path -- count exchange, key All2All (R2),
+ * embedding and gradient All2All (R7, R11), the trained tower's dense
+ * AllReduce -- runs over the peer-mapped exchange windows, P:343, P:349,
+ * P:354); the caller then connects the ranks with nest_window_export /
+ * nest_window_connect before the first nest_route.  That mode also runs
+ * several ranks on ONE device (in one process or several): the peers' windows
+ * are plain device memory there.  It needs the fused or ce transport
+ * (NEST_A2A != nccl), else NEST_ERR_INVALID.  table_mem / work_mem: device
+ * buffers of at least the queried sizes, 256-byte aligned.  On failure every
+ * resource already created is released. */
 NEST_API nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids,
                           void* table_mem, void* work_mem, void* stream,
                           nest_ctx_t** out);
 NEST_API nest_status_t nest_destroy(nest_ctx_t* ctx);
+
+/* Exchange-window record of one rank (host bytes; plain data the caller moves
+ * between ranks with any transport, e.g. torch.distributed.all_gather_object):
+ * the window's device pointer and CUDA IPC handle plus its geometry. */
+typedef struct {
+  uint64_t magic;
+  int32_t pid, rank, world, device;
+  uint64_t ptr;                  /* device address (used directly by same-process peers) */
+  uint8_t ipc[64];               /* cudaIpcMemHandle_t (other processes) */
+  uint64_t bytes, off_own, off_cnt, off_key, off_twr, off_flags;
+  uint64_t src_stride, cnt_stride, key_stride;
+} nest_window_rec_t;
+
+/* This rank's window record (context created with nccl_uids == NULL and
+ * world > 1).  rec: host, sizeof(nest_window_rec_t).  NEST_ERR_INVALID when the
+ * context has no window. */
+NEST_API nest_status_t nest_window_export(const nest_ctx_t* ctx, nest_window_rec_t* rec);
+
+/* Maps every rank's window (recs: host, world records in rank order, from
+ * nest_window_export on each rank).  Same-process peers are addressed
+ * directly, others through cudaIpcOpenMemHandle.  Host-side only; call once,
+ * on every rank, before the first nest_route.  NEST_ERR_INVALID on records of
+ * another world / geometry, NEST_ERR_ORDER if already connected. */
+NEST_API nest_status_t nest_window_connect(nest_ctx_t* ctx, const nest_window_rec_t* recs);
 
 /* PRF initialisation of the whole shard: row of key k gets init_row(seed, k,
  * d). */

@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 from . import _lib as L
 from ._lib import NestError  # noqa: F401
 
-__all__ = ["NestContext", "NestError", "unique_ids"]
+__all__ = ["NestContext", "NestError", "unique_ids", "connect_windows"]
 
 
 def _ptr(t) -> Optional[int]:
@@ -85,16 +85,33 @@ class NestContext:
             self.shard = self.table_mem.view(torch.float32)[: self.shard_rows * dim].view(self.shard_rows, dim)
             ctx = C.c_void_p()
             uid = None
-            if world > 1:
-                if nccl_uids is None or len(nccl_uids) != 256:
-                    raise ValueError("world > 1 needs the 256-byte nccl_uids from rank 0")
+            if world > 1 and nccl_uids is not None:
+                if len(nccl_uids) != 256:
+                    raise ValueError("nccl_uids must be the 256 bytes of unique_ids() from rank 0")
                 uid = C.create_string_buffer(nccl_uids, 256)
+            # world > 1 without nccl_uids: no NCCL, exchanges over the peer
+            # windows; connect them with window_export / window_connect
             st = torch.cuda.current_stream(self.device)
             L.check(self.lib.nest_create(C.byref(self.cfg), uid, _ptr(self.table_mem), _ptr(self.work_mem),
                                          st.cuda_stream, C.byref(ctx)))
             self.ctx = ctx
             if init_tables:
                 self.init_tables(st)
+
+    # -- NCCL-free mode: exchange-window rendezvous -----------------------------
+    def window_export(self) -> bytes:
+        """This rank's window record (nest_window_export), to be moved to every
+        rank by the caller (torch.distributed.all_gather_object, or in-process)."""
+        rec = L.WindowRec()
+        self._check(self.lib.nest_window_export(self.ctx, C.byref(rec)))
+        return bytes(rec)
+
+    def window_connect(self, recs: Sequence[bytes]) -> None:
+        """Map every rank's window (records in rank order; nest_window_connect)."""
+        arr = (L.WindowRec * len(recs))()
+        for i, r in enumerate(recs):
+            C.memmove(C.byref(arr, i * C.sizeof(L.WindowRec)), r, C.sizeof(L.WindowRec))
+        self._check(self.lib.nest_window_connect(self.ctx, arr))
 
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
@@ -274,3 +291,11 @@ def _memcpy_d2h(dst: int, src: int, nbytes: int) -> None:
     rc = _cudart.cudaMemcpy(dst, src, nbytes, 2)  # cudaMemcpyDeviceToHost
     if rc != 0:
         raise NestError(2, f"cudaMemcpy failed ({rc})")
+
+
+def connect_windows(contexts) -> None:
+    """Connect the ranks of one process (e.g. several ranks on one device,
+    each driven by its own thread): every context maps every other's window."""
+    recs = [c.window_export() for c in contexts]
+    for c in contexts:
+        c.window_connect(recs)

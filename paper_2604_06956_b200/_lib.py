@@ -23,7 +23,7 @@ MAX_MICRO_BATCHES = 8
 
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
-           "nest_create", "nest_destroy", "nest_init_tables", "nest_fwp_schedule", "nest_route",
+           "nest_create", "nest_destroy", "nest_window_export", "nest_window_connect", "nest_init_tables", "nest_fwp_schedule", "nest_route",
            "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_lookup_fwd_bf16",
            "nest_grad_bwd_update", "nest_grad_bwd_update_adagrad", "nest_tower_fwd_bwd",
            "nest_tower_fwd_bwd_bf16", "nest_tower_step", "nest_join", "nest_read_state", "nest_tower_read",
@@ -88,6 +88,15 @@ class ProfileSummary(C.Structure):
                 ("a2a_exposed_ms", C.c_double), ("compute_busy_ms", C.c_double), ("launches", C.c_int64)]
 
 
+class WindowRec(C.Structure):
+    """nest_window_rec_t: one rank's exchange-window record (plain bytes)."""
+    _fields_ = [("magic", C.c_uint64), ("pid", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("device", C.c_int32), ("ptr", C.c_uint64), ("ipc", C.c_uint8 * 64),
+                ("bytes", C.c_uint64), ("off_own", C.c_uint64), ("off_cnt", C.c_uint64),
+                ("off_key", C.c_uint64), ("off_twr", C.c_uint64), ("off_flags", C.c_uint64),
+                ("src_stride", C.c_uint64), ("cnt_stride", C.c_uint64), ("key_stride", C.c_uint64)]
+
+
 _lib = None
 
 
@@ -108,6 +117,8 @@ def load() -> C.CDLL:
         "nest_shard_rows": ([C.POINTER(Config)], i64),
         "nest_create": ([C.POINTER(Config), vp, vp, vp, vp, C.POINTER(vp)], i32),
         "nest_destroy": ([vp], i32),
+        "nest_window_export": ([vp, C.POINTER(WindowRec)], i32),
+        "nest_window_connect": ([vp, C.POINTER(WindowRec)], i32),
         "nest_init_tables": ([vp, vp], i32),
         "nest_fwp_schedule": ([vp, vp, vp, i64, i32, i32, i32, vp, vp, vp], i32),
         "nest_route": ([vp, i32, vp, vp, i64, i32, vp, vp, i32, vp], i32),

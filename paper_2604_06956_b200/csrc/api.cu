@@ -384,8 +384,21 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
     NEST_CUDA(cudaEventCreateWithFlags(&c->ev_scratch, cudaEventDisableTiming));
     if (c->cl_u) NEST_CUDA(cudaMallocHost(&c->cl_hmax, sizeof(int32_t)));
     NEST_CUDA(cudaStreamSynchronize(st0));
-    if (c->W > 1) {
-      NEST_CHECK(nccl_uids != nullptr, NEST_ERR_INVALID, "world > 1 needs NCCL unique ids");
+    if (c->W > 1 && c->cfg.tower_train && c->cfg.tower_layers > 0 && nccl_uids == nullptr) {
+      // the trained tower's dense AllReduce goes through the window too
+      const int64_t H = c->cfg.tower_hidden, L = c->cfg.tower_layers;
+      const int64_t n = int64_t(c->F) * c->D * H + (L - 1) * H * H;
+      c->twr_elems = (n + c->W - 1) / c->W * c->W;
+    }
+    if (c->W > 1 && nccl_uids == nullptr) {
+      // no NCCL: every exchange over the peer-mapped windows; the caller
+      // connects them (nest_window_export / nest_window_connect)
+      NEST_CHECK(xfer_wanted(c->W), NEST_ERR_INVALID,
+                 "world > 1 without NCCL ids needs the fused or ce transport (NEST_A2A != nccl)");
+      c->route_window = true;
+      xfer_alloc(*c, st0);
+      NEST_CUDA(cudaStreamSynchronize(st0));
+    } else if (c->W > 1) {
       ncclUniqueId id0, id1;
       std::memcpy(&id0, nccl_uids, sizeof(id0));
       std::memcpy(&id1, reinterpret_cast<const char*>(nccl_uids) + sizeof(id0), sizeof(id1));
@@ -397,7 +410,13 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       cfg1.maxCTAs = mc ? std::atoi(mc) : 8;
       NEST_NCCL(ncclCommInitRankConfig(&c->comm, c->W, id0, c->rank, &cfg0));
       NEST_NCCL(ncclCommInitRankConfig(&c->comm_aux, c->W, id1, c->rank, &cfg1));
-      if (xfer_wanted(c->W)) xfer_setup(*c, st0);
+      if (xfer_wanted(c->W)) {
+        // NEST_ROUTE_XCHG=window: the count exchange and key All2All over the
+        // window as well (peer stores + flags) instead of NCCL
+        const char* rx = std::getenv("NEST_ROUTE_XCHG");
+        c->route_window = rx && std::strcmp(rx, "window") == 0;
+        xfer_setup(*c, st0);
+      }
     }
     if (c->cfg.tower_layers > 0) tower_create(*c);
   });
@@ -409,6 +428,18 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
   }
   *out = reinterpret_cast<nest_ctx_t*>(c);
   return NEST_OK;
+}
+
+nest_status_t nest_window_export(const nest_ctx_t* ctx, nest_window_rec_t* rec) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(ctx);
+  if (!c || !rec) return NEST_ERR_INVALID;
+  return guard(const_cast<Ctx*>(c), [&] { xfer_export(*c, rec); });
+}
+
+nest_status_t nest_window_connect(nest_ctx_t* ctx, const nest_window_rec_t* recs) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !recs) return NEST_ERR_INVALID;
+  return guard(c, [&] { xfer_connect(*c, recs); });
 }
 
 nest_status_t nest_destroy(nest_ctx_t* ctx) {
@@ -486,6 +517,8 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
     NEST_CHECK(B % N == 0, NEST_ERR_DIVISIBILITY, "B mod N != 0");
     NEST_CHECK(perm != nullptr || N == 1, NEST_ERR_INVALID, "N > 1 needs perm from nest_fwp_schedule");
     NEST_CHECK(bag_offsets != nullptr && (keys != nullptr || nnz == 0), NEST_ERR_INVALID, "null batch");
+    NEST_CHECK(c->W == 1 || c->connected || c->comm != nullptr, NEST_ERR_ORDER,
+               "exchange windows not connected (nest_window_connect) before the first route");
     (void)mb_offsets;  // micro-batches are equal: mb_offsets[i] = i * B / N
     cudaStream_t st = S(stream);
     s.routed = false;

@@ -98,6 +98,7 @@ struct Slot {
   std::vector<int64_t> key_soff, key_roff;       // key All2All offsets
   int ubits = 0;
   uint32_t epoch = 0;              // window sequence number (same on every rank)
+  uint32_t xep = 0;                // route exchange sequence number of this slot's batch (route_window)
   uint32_t prefetched = 0;         // micro-batches whose embedding All2All is issued
   bool routed = false, updated = false;
   // early push (fused transport, W > 1): the owner pushed every requested row
@@ -220,7 +221,21 @@ struct Ctx {
   int a2a_mode = 0;                // A2AMode
   void* xwin = nullptr;            // library-owned, IPC-exported exchange window
   size_t xwin_bytes = 0, xoff_own = 0, xoff_flags = 0;
-  uint32_t* xflags = nullptr;      // [2 slots][3 kinds][Nmax][W] epoch flags written by peers
+  uint32_t* xflags = nullptr;      // [2 slots][XK_COUNT kinds][Nmax][W] epoch flags written by peers
+  // route exchange over the window (count exchange + key All2All by peer
+  // stores; no NCCL): always without NCCL communicators, NEST_ROUTE_XCHG=window otherwise
+  bool route_window = false;
+  bool connected = false;          // peers' windows mapped (nest_window_connect / NCCL exchange)
+  size_t xoff_cnt = 0, xoff_key = 0, xoff_twr = 0, xcnt_stride = 0, xkey_stride = 0;
+  uint32_t xepoch = 0;             // route exchanges so far (same sequence on every rank)
+  std::vector<int32_t*> peer_cnt[2];   // each peer's count area of slot 0 / 1
+  std::vector<int64_t*> peer_key[2];   // each peer's received-key area of slot 0 / 1
+  // trained tower without NCCL: dW reduce-scatter / all-gather through the
+  // window ([2][twr_elems] f32: partial chunks from every rank | summed dW)
+  int64_t twr_elems = 0;
+  float* twr = nullptr;
+  std::vector<float*> peer_twr;
+  uint32_t twr_epoch = 0;
   int early_push = 0;              // EarlyPush: embedding rows pushed at route time (fused transport)
   float* send_stage = nullptr;     // [OMBcap][d] early push send rows (copy-engine early push)
   bool grad_ce = false;            // fused transport, gradients by copy engine (NEST_GRAD_PUSH=ce)
@@ -602,7 +617,16 @@ void xfer_destroy(Ctx& c);
 void xfer_push_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, cudaEvent_t after_self,
                    const float* send_rows = nullptr);
 // flag kinds: 0 embedding rows, 1 gradient rows, 2 re-pushed embedding rows
-enum XferKind : int { XK_EMB = 0, XK_GRAD = 1, XK_REPUSH = 2, XK_COUNT = 3 };
+// 3 route counts, 4 route keys (mb 0; route_window), 5 / 6 trained-tower
+// reduce-scatter / all-gather (slot 0, mb 0; window AllReduce)
+enum XferKind : int { XK_EMB = 0, XK_GRAD = 1, XK_REPUSH = 2, XK_CNT = 3, XK_KEY = 4, XK_TRS = 5, XK_TAG = 6,
+                      XK_COUNT = 7 };
+constexpr uint64_t kWinMagic = 0x314e495754534e45ull;   // "ENSTWIN1"
+void xfer_alloc(Ctx& c, cudaStream_t st);
+void xfer_export(const Ctx& c, nest_window_rec_t* r);
+void xfer_connect(Ctx& c, const nest_window_rec_t* all);
+void xfer_signal_raw(Ctx& c, int slot, int kind, int mb, uint32_t value, cudaStream_t st);
+void xfer_wait_raw(Ctx& c, int slot, int kind, int mb, uint32_t value, cudaStream_t st);
 void xfer_wait_emb(Ctx& c, Slot& s, int mb, cudaStream_t st, int kind = XK_EMB);
 void xfer_push_grad(Ctx& c, Slot& s, int mb, cudaStream_t st);
 void xfer_wait_grads(Ctx& c, Slot& s, cudaStream_t st);

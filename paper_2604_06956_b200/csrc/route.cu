@@ -627,6 +627,35 @@ __global__ void k_pack(const int32_t* __restrict__ Uptr, const int64_t* __restri
     packed[u] = uniq[u] | (int64_t(mask[u]) << 56);
 }
 
+// R2 over the exchange window (route_window): this rank's count row stored
+// straight into every peer's count area of the slot (same offset)
+struct PeerI32 {
+  int32_t* p[NEST_MAX_WORLD];
+};
+__global__ void k_push_counts(int W, int me, const int32_t* __restrict__ row, int n, PeerI32 dst) {
+  for (int i = threadIdx.x; i < W * n; i += blockDim.x) {
+    const int p = i / n, j = i % n;
+    if (p != me) dst.p[p][j] = row[j];
+  }
+  __threadfence_system();
+}
+
+// R2 key All2All over the exchange window: uniq is sorted by owner, so owner
+// p's keys are uniq[off[p] .. off[p+1]); each lands at this rank's receive
+// offset in p's key area (blockIdx.y = owner; the self part is a local copy)
+struct KeyDst {
+  int64_t* base[NEST_MAX_WORLD];   // owner p's key area + this rank's receive offset there
+  int32_t off[NEST_MAX_WORLD + 1];
+};
+__global__ void k_pack_push(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ mask, KeyDst kd) {
+  const int p = blockIdx.y;
+  const int32_t a = kd.off[p], n = kd.off[p + 1] - a;
+  int64_t* dst = kd.base[p];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = uniq[a + i] | (int64_t(mask[a + i]) << 56);
+  __threadfence_system();
+}
+
 __global__ void k_owner_mark(int64_t R, const int64_t* __restrict__ recv, int T, int W, int rank,
                              const int64_t* __restrict__ rows, const int64_t* __restrict__ lbase,
                              uint32_t* __restrict__ r_ldom, uint32_t* __restrict__ bm,
@@ -775,7 +804,17 @@ void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offs
                                       xfer + int64_t(c.rank) * W * Nc);
   NEST_LAUNCH_CHECK();
   // R2: count exchange (every rank's counts and error flags to every rank)
-  if (W > 1) {
+  if (W > 1 && c.route_window) {
+    // over the window: store the row into every peer, flag, wait for theirs
+    const int si = slot_index(c, s);
+    s.xep = ++c.xepoch;
+    PeerI32 dst{};
+    for (int p = 0; p < W; ++p) dst.p[p] = c.peer_cnt[si][p] + int64_t(c.rank) * W * Nc;
+    k_push_counts<<<1, 256, 0, st>>>(W, c.rank, xfer + int64_t(c.rank) * W * Nc, W * Nc, dst);
+    NEST_LAUNCH_CHECK();
+    xfer_signal_raw(c, si, XK_CNT, 0, s.xep, st);
+    xfer_wait_raw(c, si, XK_CNT, 0, s.xep, st);
+  } else if (W > 1) {
     NEST_NCCL(ncclAllGather(xfer + int64_t(c.rank) * W * Nc, xfer, size_t(W) * Nc, ncclInt32,
                             c.comm_aux, st));
   }
@@ -890,6 +929,28 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     {
       // ---- R2: key All2All (key | mask << 56), grouped send/recv ----
       ProfScope ps(c, ST_KEY_A2A, SK_AUX, st);
+      if (c.route_window) {
+        // keys stored straight into every owner's key area at this rank's
+        // receive offset there (sources in rank order), then flagged
+        const int si = slot_index(c, s);
+        KeyDst kd{};
+        int64_t mx = 1;
+        for (int p = 0; p < W; ++p) {
+          int64_t roff = 0;
+          for (int r = 0; r < c.rank; ++r) roff += s.all[(size_t(r) * W + p) * Nc];
+          kd.base[p] = c.peer_key[si][p] + roff;
+          kd.off[p] = int32_t(s.key_soff[p]);
+          mx = std::max<int64_t>(mx, s.key_soff[p + 1] - s.key_soff[p]);
+        }
+        kd.off[W] = int32_t(s.key_soff[W]);
+        k_pack_push<<<dim3(unsigned(std::min<int64_t>((mx + 255) / 256, 148 * 2)), unsigned(W)), 256, 0, st>>>(
+            s.uniq, s.mask, kd);
+        NEST_LAUNCH_CHECK();
+        xfer_signal_raw(c, si, XK_KEY, 0, s.xep, st);
+        xfer_wait_raw(c, si, XK_KEY, 0, s.xep, st);
+        ps.launches = 1;
+        ps.bytes = 8.0 * double(U - (s.key_soff[c.rank + 1] - s.key_soff[c.rank]));  // off-GPU
+      } else {
       k_pack<<<grid_for(c.Kcap, 256, 148 * 8), 256, 0, st>>>(s.off + W, s.uniq, s.mask, c.packed);
       NEST_LAUNCH_CHECK();
       NEST_NCCL(ncclGroupStart());
@@ -901,6 +962,7 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
       }
       NEST_NCCL(ncclGroupEnd());
       ps.bytes = 8.0 * double(U - (s.key_soff[c.rank + 1] - s.key_soff[c.rank]));  // off-GPU
+      }
     }
     {
       // ---- R3: owner dedup on the local domain ----

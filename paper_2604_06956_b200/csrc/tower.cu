@@ -148,7 +148,9 @@ void tower_create(Ctx& c) {
   if (t->train) {
     t->w32 = w.take<float>(t->woff[L]);
     t->dw32 = w.take<float>(t->woff[L]);
-    if (c.W > 1) NEST_NCCL(ncclCommSplit(c.comm, 0, c.rank, &t->comm, nullptr));
+    if (c.W > 1 && c.comm) NEST_NCCL(ncclCommSplit(c.comm, 0, c.rank, &t->comm, nullptr));
+    // without NCCL the dense AllReduce runs through the exchange window
+    NEST_CHECK(c.W == 1 || c.comm || c.twr, NEST_ERR_INVALID, "trained tower at world > 1 needs NCCL or a window");
   }
   {
     const char* dv = std::getenv("NEST_TOWER_DEFER_DW");
@@ -367,6 +369,30 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
   return t->defer_dw ? 2.0 * flops_dw : 3.0 * flops_dw;   // FLOPs on `st` (fwd + dX [+ dW])
 }
 
+// window AllReduce of the trained tower's dW (no NCCL): chunk p of this
+// rank's dW goes to rank p's partial area at row `me`; rank p sums the W
+// partial chunks in rank order and stores the sum into every rank's sum area
+struct PeerF32 {
+  float* p[NEST_MAX_WORLD];
+};
+__global__ void k_twr_push_rs(const float* __restrict__ dw, int64_t n, int64_t chunk, int me, PeerF32 part) {
+  const int p = blockIdx.y;
+  float* dst = part.p[p] + int64_t(me) * chunk;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < chunk; j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t g = int64_t(p) * chunk + j;
+    dst[j] = g < n ? dw[g] : 0.f;
+  }
+  __threadfence_system();
+}
+__global__ void k_twr_reduce_ag(const float* __restrict__ part, int64_t chunk, int W, int me, PeerF32 sum) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < chunk; j += int64_t(gridDim.x) * blockDim.x) {
+    float a = 0.f;
+    for (int r = 0; r < W; ++r) a += part[int64_t(r) * chunk + j];
+    for (int p = 0; p < W; ++p) sum.p[p][int64_t(me) * chunk + j] = a;
+  }
+  __threadfence_system();
+}
+
 // NEXT-4 update, once per batch after its last micro-batch: dense gradients
 // summed over the data-parallel ranks (the paper's communication-side
 // AllReduce) and SGD on the fp32 master weights + their bf16 copy,
@@ -384,8 +410,36 @@ void tower_step(Ctx& c, cudaStream_t st) {
     ws = t->side;
   }
   const int64_t n = t->woff[t->L];
-  if (t->comm) NEST_NCCL(ncclAllReduce(t->dw32, t->dw32, size_t(n), ncclFloat32, ncclSum, t->comm, ws));
-  k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, t->dw32, n, t->lr);
+  if (t->comm) {
+    NEST_NCCL(ncclAllReduce(t->dw32, t->dw32, size_t(n), ncclFloat32, ncclSum, t->comm, ws));
+    k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, t->dw32, n, t->lr);
+  } else if (c.W > 1) {
+    // window AllReduce: reduce-scatter by peer stores (rank r sums chunk r in
+    // rank order, so the sum is deterministic), all-gather of the summed
+    // chunks, then the same SGD on every replica (bitwise equal replicas)
+    const int W = c.W, me = c.rank;
+    const int64_t chunk = c.twr_elems / W;
+    NEST_CHECK(chunk * W >= n, NEST_ERR_INVALID, "tower window area too small");
+    const uint32_t ep = ++c.twr_epoch;
+    PeerF32 part{}, sum{};
+    for (int p = 0; p < W; ++p) {
+      part.p[p] = c.peer_twr[p];
+      sum.p[p] = c.peer_twr[p] + c.twr_elems;
+    }
+    k_twr_push_rs<<<dim3(unsigned(std::min<int64_t>((chunk + 255) / 256, 148)), unsigned(W)), 256, 0, ws>>>(
+        t->dw32, n, chunk, me, part);
+    NEST_LAUNCH_CHECK();
+    xfer_signal_raw(c, 0, XK_TRS, 0, ep, ws);
+    xfer_wait_raw(c, 0, XK_TRS, 0, ep, ws);
+    k_twr_reduce_ag<<<unsigned(std::min<int64_t>((chunk + 255) / 256, 148 * 2)), 256, 0, ws>>>(
+        c.twr, chunk, W, me, sum);
+    NEST_LAUNCH_CHECK();
+    xfer_signal_raw(c, 0, XK_TAG, 0, ep, ws);
+    xfer_wait_raw(c, 0, XK_TAG, 0, ep, ws);
+    k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, c.twr + c.twr_elems, n, t->lr);
+  } else {
+    k_dense_sgd<<<148 * 4, 256, 0, ws>>>(t->w32, t->w, t->dw32, n, t->lr);
+  }
   NEST_LAUNCH_CHECK();
   t->acc = 0;
   t->acc_rows = 0;

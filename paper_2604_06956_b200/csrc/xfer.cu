@@ -26,6 +26,8 @@
 // reading the slot's window.
 #include <cuda.h>
 
+#include <unistd.h>
+
 #include <cstring>
 
 #include "nest_internal.cuh"
@@ -71,10 +73,15 @@ static int early_push_wanted() {
 }
 
 // window layout: [src_rows of slot 0 (| slot 1 with early push) MBcap*D f32 |
-//                 own_rows OMBcap*D f32 | flags [2][3][Nmax][W] u32]
-void xfer_setup(Ctx& c, cudaStream_t st) {
+//                 own_rows OMBcap*D f32 |
+//                 route counts [2 slots][W*W*Nc + Nmax + 1] i32 (route_window) |
+//                 received keys [2 slots][Rcap] i64 (route_window) |
+//                 tower dW exchange [2][n] f32 (trained tower without NCCL) |
+//                 flags [2][XK_COUNT][Nmax][W] u32]
+void xfer_alloc(Ctx& c, cudaStream_t st) {
   load_driver_ops();
   c.a2a_mode = a2a_mode_wanted(c.W);
+  NEST_CHECK(c.a2a_mode != A2A_NCCL, NEST_ERR_INVALID, "xfer_alloc needs the fused or ce transport");
   c.early_push = c.a2a_mode == A2A_FUSED ? early_push_wanted() : EP_OFF;
   {
     // gradients under the fused transport: segment-sum stores into the
@@ -84,63 +91,140 @@ void xfer_setup(Ctx& c, cudaStream_t st) {
   }
   if (c.early_push == EP_CE)
     NEST_CUDA(cudaMalloc(&c.send_stage, std::max<size_t>(size_t(c.OMBcap) * c.D * sizeof(float), 256)));
+  const int Nc = c.Nmax + 2;
   const size_t src1 = align_up(size_t(c.MBcap) * c.D * sizeof(float), 4096);
   const size_t src_b = c.early_push ? 2 * src1 : src1;
   const size_t own_b = align_up(size_t(c.OMBcap) * c.D * sizeof(float), 4096);
+  const size_t cnt1 = align_up(sizeof(int32_t) * (size_t(c.W) * c.W * Nc + c.Nmax + 1), 256);
+  const size_t key1 = align_up(sizeof(int64_t) * size_t(c.Rcap), 256);
+  const size_t cnt_b = c.route_window ? 2 * cnt1 : 0;
+  const size_t key_b = c.route_window ? align_up(2 * key1, 4096) : 0;
+  const size_t twr_b = align_up(sizeof(float) * 2 * size_t(c.twr_elems), 4096);
   const size_t flg_b = align_up(size_t(2) * XK_COUNT * c.Nmax * c.W * sizeof(uint32_t), 4096);
   c.src_slot_stride = c.early_push ? int64_t(src1 / sizeof(float)) : 0;
-  c.xwin_bytes = src_b + own_b + flg_b;
-  NEST_CUDA(cudaMalloc(&c.xwin, c.xwin_bytes));
-  NEST_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(c.xwin) + src_b + own_b, 0, flg_b, st));
   c.xoff_own = src_b;
-  c.xoff_flags = src_b + own_b;
-  c.src_rows = reinterpret_cast<float*>(c.xwin);
-  c.own_rows = reinterpret_cast<float*>(reinterpret_cast<char*>(c.xwin) + src_b);
-  c.xflags = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c.xwin) + c.xoff_flags);
-  // exchange IPC handles (+ window geometry) through the aux communicator
-  struct Rec {
-    cudaIpcMemHandle_t h;
-    uint64_t own, flags, bytes, src_stride;
-  };
-  Rec mine{};
-  NEST_CUDA(cudaIpcGetMemHandle(&mine.h, c.xwin));
-  mine.src_stride = uint64_t(c.src_slot_stride);
-  mine.own = c.xoff_own;
-  mine.flags = c.xoff_flags;
-  mine.bytes = c.xwin_bytes;
-  char* dbuf = nullptr;
-  NEST_CUDA(cudaMalloc(&dbuf, sizeof(Rec) * (c.W + 1)));
-  NEST_CUDA(cudaMemcpyAsync(dbuf + sizeof(Rec) * c.rank, &mine, sizeof(Rec), cudaMemcpyHostToDevice, st));
-  NEST_NCCL(ncclAllGather(dbuf + sizeof(Rec) * c.rank, dbuf, sizeof(Rec), ncclUint8, c.comm_aux, st));
-  std::vector<Rec> all(c.W);
-  NEST_CUDA(cudaMemcpyAsync(all.data(), dbuf, sizeof(Rec) * c.W, cudaMemcpyDeviceToHost, st));
-  NEST_CUDA(cudaStreamSynchronize(st));
-  NEST_CUDA(cudaFree(dbuf));
+  c.xoff_cnt = src_b + own_b;
+  c.xoff_key = c.xoff_cnt + cnt_b;
+  c.xoff_twr = c.xoff_key + key_b;
+  c.xoff_flags = c.xoff_twr + twr_b;
+  c.xcnt_stride = cnt1;
+  c.xkey_stride = key1;
+  c.xwin_bytes = c.xoff_flags + flg_b;
+  NEST_CUDA(cudaMalloc(&c.xwin, c.xwin_bytes));
+  char* base = reinterpret_cast<char*>(c.xwin);
+  NEST_CUDA(cudaMemsetAsync(base + c.xoff_flags, 0, flg_b, st));
+  c.src_rows = reinterpret_cast<float*>(base);
+  c.own_rows = reinterpret_cast<float*>(base + src_b);
+  c.xflags = reinterpret_cast<uint32_t*>(base + c.xoff_flags);
+  if (c.route_window) {
+    // the count exchange and the key All2All land in the window: peers store
+    // their counts / keys straight into this rank's slot areas
+    for (int si = 0; si < 2; ++si) {
+      c.slot[si].xfer = reinterpret_cast<int32_t*>(base + c.xoff_cnt + si * cnt1);
+      c.slot[si].recv = reinterpret_cast<int64_t*>(base + c.xoff_key + si * key1);
+    }
+  }
+  c.twr = c.twr_elems ? reinterpret_cast<float*>(base + c.xoff_twr) : nullptr;
+}
+
+void xfer_export(const Ctx& c, nest_window_rec_t* r) {
+  NEST_CHECK(c.xwin != nullptr, NEST_ERR_INVALID, "no exchange window (world == 1 or NEST_A2A=nccl)");
+  std::memset(r, 0, sizeof(*r));
+  r->magic = kWinMagic;
+  r->pid = int32_t(getpid());
+  r->rank = c.rank;
+  r->world = c.W;
+  int dev = 0;
+  NEST_CUDA(cudaGetDevice(&dev));
+  r->device = dev;
+  r->ptr = reinterpret_cast<uint64_t>(c.xwin);
+  cudaIpcMemHandle_t h;
+  NEST_CUDA(cudaIpcGetMemHandle(&h, c.xwin));
+  static_assert(sizeof(h) <= sizeof(r->ipc), "ipc handle size");
+  std::memcpy(r->ipc, &h, sizeof(h));
+  r->bytes = c.xwin_bytes;
+  r->off_own = c.xoff_own;
+  r->off_cnt = c.xoff_cnt;
+  r->off_key = c.xoff_key;
+  r->off_twr = c.xoff_twr;
+  r->off_flags = c.xoff_flags;
+  r->src_stride = uint64_t(c.src_slot_stride);
+  r->cnt_stride = c.xcnt_stride;
+  r->key_stride = c.xkey_stride;
+}
+
+// map every peer's window: the same process (in-process ranks sharing one
+// device) uses the raw pointer, another process opens the CUDA IPC handle
+void xfer_connect(Ctx& c, const nest_window_rec_t* all) {
+  NEST_CHECK(c.xwin != nullptr, NEST_ERR_INVALID, "no exchange window (world == 1 or NEST_A2A=nccl)");
+  NEST_CHECK(!c.connected, NEST_ERR_ORDER, "window already connected");
+  for (int p = 0; p < c.W; ++p) {
+    const nest_window_rec_t& r = all[p];
+    NEST_CHECK(r.magic == kWinMagic && r.world == c.W && r.rank == p, NEST_ERR_INVALID,
+               "window records must be this world's, in rank order");
+    NEST_CHECK(r.bytes == c.xwin_bytes && r.off_flags == c.xoff_flags && r.off_key == c.xoff_key,
+               NEST_ERR_INVALID, "peer window geometry differs (every rank needs the same config)");
+  }
+  NEST_CHECK(all[c.rank].ptr == reinterpret_cast<uint64_t>(c.xwin), NEST_ERR_INVALID,
+             "own window record does not match this context");
   c.peer_win.assign(c.W, nullptr);
   c.peer_src.assign(c.W, nullptr);
   c.peer_own.assign(c.W, nullptr);
   c.peer_flags.assign(c.W, nullptr);
-  c.peer_src_slot[0].assign(c.W, nullptr);
-  c.peer_src_slot[1].assign(c.W, nullptr);
+  c.peer_twr.assign(c.W, nullptr);
+  for (int si = 0; si < 2; ++si) {
+    c.peer_src_slot[si].assign(c.W, nullptr);
+    c.peer_cnt[si].assign(c.W, nullptr);
+    c.peer_key[si].assign(c.W, nullptr);
+  }
+  const int32_t me_pid = int32_t(getpid());
   for (int p = 0; p < c.W; ++p) {
+    const nest_window_rec_t& r = all[p];
     char* base;
     if (p == c.rank) {
       base = reinterpret_cast<char*>(c.xwin);
+    } else if (r.pid == me_pid) {
+      base = reinterpret_cast<char*>(r.ptr);   // same process: one address space
     } else {
       void* ptr = nullptr;
-      NEST_CUDA(cudaIpcOpenMemHandle(&ptr, all[p].h, cudaIpcMemLazyEnablePeerAccess));
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, r.ipc, sizeof(h));
+      NEST_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
       base = reinterpret_cast<char*>(ptr);
       c.peer_win[p] = ptr;
     }
     c.peer_src[p] = reinterpret_cast<float*>(base);
     c.peer_src_slot[0][p] = c.peer_src[p];
-    c.peer_src_slot[1][p] = c.peer_src[p] + all[p].src_stride;
-    c.peer_own[p] = reinterpret_cast<float*>(base + all[p].own);
-    c.peer_flags[p] = reinterpret_cast<uint32_t*>(base + all[p].flags);
+    c.peer_src_slot[1][p] = c.peer_src[p] + r.src_stride;
+    c.peer_own[p] = reinterpret_cast<float*>(base + r.off_own);
+    c.peer_flags[p] = reinterpret_cast<uint32_t*>(base + r.off_flags);
+    c.peer_twr[p] = reinterpret_cast<float*>(base + r.off_twr);
+    for (int si = 0; si < 2; ++si) {
+      c.peer_cnt[si][p] = reinterpret_cast<int32_t*>(base + r.off_cnt + si * r.cnt_stride);
+      c.peer_key[si][p] = reinterpret_cast<int64_t*>(base + r.off_key + si * r.key_stride);
+    }
   }
   // (no barrier needed: the first push happens after the first route's count
-  // exchange, a collective every rank enters after this setup)
+  // exchange, which every rank enters after connecting)
   c.xfer_ce = true;
+  c.connected = true;
+}
+
+// NCCL mode: the records travel through the aux communicator
+void xfer_setup(Ctx& c, cudaStream_t st) {
+  xfer_alloc(c, st);
+  nest_window_rec_t mine;
+  xfer_export(c, &mine);
+  char* dbuf = nullptr;
+  const size_t rb = sizeof(nest_window_rec_t);
+  NEST_CUDA(cudaMalloc(&dbuf, rb * (c.W + 1)));
+  NEST_CUDA(cudaMemcpyAsync(dbuf + rb * c.rank, &mine, rb, cudaMemcpyHostToDevice, st));
+  NEST_NCCL(ncclAllGather(dbuf + rb * c.rank, dbuf, rb, ncclUint8, c.comm_aux, st));
+  std::vector<nest_window_rec_t> all(c.W);
+  NEST_CUDA(cudaMemcpyAsync(all.data(), dbuf, rb * c.W, cudaMemcpyDeviceToHost, st));
+  NEST_CUDA(cudaStreamSynchronize(st));
+  NEST_CUDA(cudaFree(dbuf));
+  xfer_connect(c, all.data());
 }
 
 void xfer_destroy(Ctx& c) {
@@ -153,8 +237,32 @@ void xfer_destroy(Ctx& c) {
   c.send_stage = nullptr;
 }
 
+static inline size_t flag_at(const Ctx& c, int slot, int kind, int mb, int src) {
+  return ((size_t(slot) * XK_COUNT + kind) * c.Nmax + mb) * c.W + src;
+}
 static inline size_t flag_index(const Ctx& c, const Slot& s, int kind, int mb, int src) {
-  return ((size_t(slot_index(c, s)) * XK_COUNT + kind) * c.Nmax + mb) * c.W + src;
+  return flag_at(c, slot_index(c, s), kind, mb, src);
+}
+
+// flag (slot, kind, mb) := value in every peer's window, after the work queued on st
+void xfer_signal_raw(Ctx& c, int slot, int kind, int mb, uint32_t value, cudaStream_t st) {
+  for (int p = 0; p < c.W; ++p) {
+    if (p == c.rank) continue;
+    CUresult r = g_write(reinterpret_cast<CUstream>(st),
+                         reinterpret_cast<CUdeviceptr>(c.peer_flags[p] + flag_at(c, slot, kind, mb, c.rank)),
+                         cuuint32_t(value), 0);
+    NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWriteValue32 failed");
+  }
+}
+// st waits until every peer wrote flag (slot, kind, mb) >= value into this window
+void xfer_wait_raw(Ctx& c, int slot, int kind, int mb, uint32_t value, cudaStream_t st) {
+  for (int o = 0; o < c.W; ++o) {
+    if (o == c.rank) continue;
+    CUresult r = g_wait(reinterpret_cast<CUstream>(st),
+                        reinterpret_cast<CUdeviceptr>(c.xflags + flag_at(c, slot, kind, mb, o)),
+                        cuuint32_t(value), CU_STREAM_WAIT_VALUE_GEQ);
+    NEST_CHECK(r == CUDA_SUCCESS, NEST_ERR_CUDA, "cuStreamWaitValue32 failed");
+  }
 }
 
 // rows: [W][W][Nc] counts of the slot; base_of(p, i) = row base of micro-batch

@@ -30,10 +30,15 @@ TRANSPORTS = {"fused-early": {}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
               "fused-early-gradce": {"NEST_GRAD_PUSH": "ce"},
               "fused-early-range": {"NEST_SEGSUM": "range"},
               "fused-window": {"NEST_EARLY_PUSH": "0"}, "ce": {"NEST_A2A": "ce"},
-              "nccl": {"NEST_A2A": "nccl"}}
+              "nccl": {"NEST_A2A": "nccl"},
+              # count exchange + key All2All over the windows too (no NCCL on the route)
+              "fused-early-routewin": {"NEST_ROUTE_XCHG": "window"},
+              # no NCCL at all: windows connected through torch.distributed
+              "no-nccl": {"NEST_MGPU_NO_NCCL": "1"}}
 
 
-@pytest.mark.parametrize("world,transport", [(2, t) for t in TRANSPORTS] + [(4, "fused-early")])
+@pytest.mark.parametrize("world,transport", [(2, t) for t in TRANSPORTS] +
+                         [(4, "fused-early"), (4, "no-nccl"), (8, "fused-early"), (8, "no-nccl")])
 def test_multi_rank_parity(world, transport):
     if _ndev() < world:
         pytest.skip(f"needs >= {world} CUDA devices")
