@@ -1,3 +1,3 @@
 export CUDA_VISIBLE_DEVICES=0
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+timeout 1500 python -m pytest tests -m gpu -x -q -rs 2>&1 | tail -15
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1

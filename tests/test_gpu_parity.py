@@ -675,6 +675,46 @@ def test_genrec_full_tables_unpooled_sampled():
     ctx.close()
 
 
+def test_dlrm_full_size_bench_path_p1_every_row():
+    """BASELINE configs[1] (26 tables, 103.3M rows, d=128, 65,536 samples) at
+    W=1 on the bench's exact call path -- pipelined DBP (route of t+1 on the
+    aux lane, prefetch gather skipping the pending update's keys + refresh),
+    nest_lookup_fwd_bf16 (bf16 pooled rows for the dense consumer), the fused
+    segment-sum + SGD of N=1 -- for 3 steps in regime P1 (dyadic rows and
+    gradients, s = 2^-12: every sum exact in fp32).  EVERY pooled row of every
+    step equals bf16(oracle pooled) bit for bit, and EVERY row touched by the 3
+    steps equals the oracle's E_3 bit for bit (oracle.step.sync_step)."""
+    cfg = WL.CONFIGS["dlrm"]
+    B, F, d, T, lr = cfg.batch_local, cfg.num_features, cfg.dim, 3, 2.0 ** -12
+    batches = [WL.gen_batch(cfg, 7, t, 0) for t in range(T)]
+    douts = [WL.gen_dout(7, t, 0, B * F, d, "dyadic") for t in range(T)]
+    K = max(len(k) for k, _ in batches)
+    ctx = NestContext(cfg.table_rows, d, max_keys=K, max_batch=B, seed=9, init_mode="dyadic", device=DEV)
+    run = Runner(ctx, N=1, pipelined=True, lr_over_B=lr, pooled_dtype=torch.bfloat16)
+    db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), B) for k, o in batches]
+    got_pooled = []
+    for t in range(T):
+        dd = to_dev(douts[t], torch.float32)
+        outs = run.step(db[t], db[t + 1] if t + 1 < T else None, lambda tt, i, p, dd=dd: dd)
+        run.join()
+        torch.cuda.synchronize()
+        assert outs[0].dtype == torch.bfloat16
+        got_pooled.append(outs[0].cpu().view(torch.int16).numpy())
+        del dd
+    touched = np.unique(np.concatenate([k for k, _ in batches]))
+    got_rows = ctx.read_rows(to_dev(touched, torch.int64)).cpu().numpy()
+    ctx.close()
+    tab = OS.LazyTable(9, d, "dyadic")
+    for t in range(T):
+        res = OS.sync_step(tab, [batches[t]], [douts[t]], lr)
+        ref = torch.from_numpy(res.pooled[0]).to(torch.bfloat16).view(torch.int16).numpy()
+        bad = np.nonzero((got_pooled[t] != ref).any(axis=1))[0]
+        assert len(bad) == 0, f"step {t}: {len(bad)} pooled rows differ, first {bad[:5]}"
+    ref_rows = tab.get(touched)
+    bad = np.nonzero((got_rows != ref_rows).any(axis=1))[0]
+    assert len(bad) == 0, f"{len(bad)} of {len(touched)} touched rows differ"
+
+
 @pytest.mark.parametrize("N", [1, 4])
 def test_dlrm_full_size_w1_sampled(N):
     """BASELINE configs[1] at W=1 (N = 1 is the bench launch configuration:
