@@ -377,6 +377,8 @@ def main():
         if profile:
             ctx.profile_enable(False)
             prof = ctx.profile_read()
+            if args.trace:
+                prof["records"] = ctx.profile_records()
         if world > 1:
             tt = torch.tensor([ms], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -390,6 +392,7 @@ def main():
     clocks.start()
     ms, prof, _, _ = timed(runner, args.steps, args.warmup, profile=True)
     clk = clocks.stop()
+    trace_records = prof.get("records")
     value = B * world * args.steps / (ms / 1e3)
     # FWP payload of the last routed batch: sum_i |K(M_i)| vs |K(B)|
     info = ctx.slot_info(runner.t % 2)
@@ -570,7 +573,7 @@ def main():
         if host_tier is not None:
             line["host_tier"] = host_tier
         if args.trace:
-            json.dump({"stages": st, "summary": summ}, open(args.trace, "w"), indent=1)
+            json.dump({"stages": st, "summary": summ, "records": trace_records}, open(args.trace, "w"), indent=1)
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

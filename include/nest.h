@@ -256,6 +256,23 @@ NEST_API nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* 
                          const int32_t* perm, const int32_t* mb_offsets, int32_t N,
                          void* stream);
 
+/* nest_route in two halves, so the caller's thread is not blocked while it
+ * still has window work to enqueue.  nest_route_begin enqueues the source
+ * side (dedup, owner bucketing, masks, the count exchange and its copy to the
+ * host) on `stream` and returns; nest_route_end performs the one host sync
+ * (the counts), then enqueues the rest (key All2All, owner dedup, gather,
+ * early push, occurrence sort) on the same stream.  Between the two no other
+ * nest_route_begin / nest_fwp_schedule may be issued (they share the routing
+ * scratch: NEST_ERR_ORDER) and the slot is not usable.  The gather-skipping
+ * decision above is taken at nest_route_begin: "the other slot's update is
+ * still to come" means not yet issued when the route began.
+ * nest_route(...) == nest_route_begin(...) + nest_route_end(ctx, slot). */
+NEST_API nest_status_t nest_route_begin(nest_ctx_t* ctx, int32_t slot, const int64_t* keys,
+                                        const int32_t* bag_offsets, int64_t nnz, int32_t B,
+                                        const int32_t* perm, const int32_t* mb_offsets, int32_t N,
+                                        void* stream);
+NEST_API nest_status_t nest_route_end(nest_ctx_t* ctx, int32_t slot);
+
 /* Dual-buffer synchronization: for every key k in both
  * the active slot's and the prefetch slot's owner key sets, copy the active
  * (already updated, written-back) row into the prefetch slot's buffer -- the
@@ -353,7 +370,8 @@ NEST_API nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t la
 NEST_API nest_status_t nest_tower_step(nest_ctx_t* ctx, void* stream);
 
 /* Make `stream` wait for all work the library queued on its internal streams
- * (the tower's deferred weight-gradient GEMMs).  Host-side enqueue only. */
+ * (the tower's deferred weight-gradient GEMMs, the occurrence sorts of
+ * nest_route_end).  Host-side enqueue only. */
 NEST_API nest_status_t nest_join(nest_ctx_t* ctx, void* stream);
 
 /* Host-known counts of a slot (valid after nest_route). */
@@ -425,6 +443,18 @@ NEST_API nest_status_t nest_profile_enable(nest_ctx_t* ctx, int32_t on);
  * (may be NULL) and the summary (may be NULL). */
 NEST_API nest_status_t nest_profile_read(nest_ctx_t* ctx, nest_profile_stage_t* stages,
                                          nest_profile_summary_t* summary);
+
+/* The raw stage intervals of the trace (a timeline): record i = {stage index
+ * (nest_profile_stage_t order), stream kind, start ms, end ms} relative to
+ * the trace start.  out: host, room for `cap` records (NULL: count only);
+ * *n = the number of records (all of them, even beyond cap).  Synchronises
+ * the device. */
+typedef struct {
+  int32_t stage, stream;
+  double t0_ms, t1_ms;
+} nest_profile_record_t;
+NEST_API nest_status_t nest_profile_records(nest_ctx_t* ctx, nest_profile_record_t* out, int64_t cap,
+                                            int64_t* n);
 
 /* Message of the last error of ctx (or of the last failed nest_create when ctx is NULL). */
 NEST_API const char* nest_last_error(const nest_ctx_t* ctx);

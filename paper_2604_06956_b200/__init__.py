@@ -147,6 +147,16 @@ class NestContext:
         self._check(self.lib.nest_route(self.ctx, slot, _ptr(keys), _ptr(bag_offsets), int(keys.numel()),
                                         B, _ptr(perm), _ptr(mb_offsets), N, _stream(stream)))
 
+    def route_begin(self, slot: int, keys, bag_offsets, B: int, perm=None, mb_offsets=None, N: int = 1,
+                    stream=None) -> None:
+        """First half of route (no host sync): nest_route_begin."""
+        self._check(self.lib.nest_route_begin(self.ctx, slot, _ptr(keys), _ptr(bag_offsets), int(keys.numel()),
+                                              B, _ptr(perm), _ptr(mb_offsets), N, _stream(stream)))
+
+    def route_end(self, slot: int) -> None:
+        """Second half of route (the host sync on the counts): nest_route_end."""
+        self._check(self.lib.nest_route_end(self.ctx, slot))
+
     def dbp_refresh(self, active: int, prefetch: int, stream=None) -> None:
         self._check(self.lib.nest_dbp_refresh(self.ctx, active, prefetch, _stream(stream)))
 
@@ -231,6 +241,16 @@ class NestContext:
                                               "launches": s.launches, "ms": s.ms, "bytes": s.bytes,
                                               "units": s.units}
         return out
+
+    def profile_records(self) -> list:
+        """The trace's raw stage intervals: [(stage name, stream kind, t0 ms, t1 ms)]."""
+        n = C.c_int64()
+        self._check(self.lib.nest_profile_records(self.ctx, None, 0, C.byref(n)))
+        recs = (L.ProfileRecord * max(1, n.value))()
+        self._check(self.lib.nest_profile_records(self.ctx, recs, n.value, C.byref(n)))
+        names = list(self.profile_read()["stages"].keys())
+        kinds = {0: "compute", 1: "comm", 2: "aux"}
+        return [(names[r.stage], kinds.get(r.stream, str(r.stream)), r.t0_ms, r.t1_ms) for r in recs[:n.value]]
 
     def route_view(self, slot: int) -> dict:
         """Copies of a slot's routing results (host numpy) for parity checks."""

@@ -23,12 +23,12 @@ MAX_MICRO_BATCHES = 8
 
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
-           "nest_create", "nest_destroy", "nest_window_export", "nest_window_connect", "nest_init_tables", "nest_fwp_schedule", "nest_route",
+           "nest_create", "nest_destroy", "nest_window_export", "nest_window_connect", "nest_init_tables", "nest_fwp_schedule", "nest_route", "nest_route_begin", "nest_route_end",
            "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_lookup_fwd_bf16",
            "nest_grad_bwd_update", "nest_grad_bwd_update_adagrad", "nest_tower_fwd_bwd",
            "nest_tower_fwd_bwd_bf16", "nest_tower_step", "nest_join", "nest_read_state", "nest_tower_read",
            "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
-           "nest_profile_read", "nest_last_error"]
+           "nest_profile_read", "nest_profile_records", "nest_last_error"]
 PROFILE_STAGES = 16
 
 
@@ -83,6 +83,10 @@ class ProfileStage(C.Structure):
                 ("units", C.c_double)]
 
 
+class ProfileRecord(C.Structure):
+    _fields_ = [("stage", C.c_int32), ("stream", C.c_int32), ("t0_ms", C.c_double), ("t1_ms", C.c_double)]
+
+
 class ProfileSummary(C.Structure):
     _fields_ = [("span_ms", C.c_double), ("a2a_ms", C.c_double), ("a2a_union_ms", C.c_double),
                 ("a2a_exposed_ms", C.c_double), ("compute_busy_ms", C.c_double), ("launches", C.c_int64)]
@@ -122,6 +126,8 @@ def load() -> C.CDLL:
         "nest_init_tables": ([vp, vp], i32),
         "nest_fwp_schedule": ([vp, vp, vp, i64, i32, i32, i32, vp, vp, vp], i32),
         "nest_route": ([vp, i32, vp, vp, i64, i32, vp, vp, i32, vp], i32),
+        "nest_route_begin": ([vp, i32, vp, vp, i64, i32, vp, vp, i32, vp], i32),
+        "nest_route_end": ([vp, i32], i32),
         "nest_dbp_refresh": ([vp, i32, i32, vp], i32),
         "nest_lookup_prefetch": ([vp, i32, i32, vp, vp], i32),
         "nest_lookup_fwd": ([vp, i32, i32, vp, vp, vp], i32),
@@ -140,6 +146,7 @@ def load() -> C.CDLL:
         "nest_exchange_plan": ([C.POINTER(Config), i32, vp, C.POINTER(ExchangePlan)], i32),
         "nest_profile_enable": ([vp, i32], i32),
         "nest_profile_read": ([vp, C.POINTER(ProfileStage), C.POINTER(ProfileSummary)], i32),
+        "nest_profile_records": ([vp, C.POINTER(ProfileRecord), i64, C.POINTER(i64)], i32),
         "nest_last_error": ([vp], C.c_char_p),
     }
     for name, (args, res) in sig.items():

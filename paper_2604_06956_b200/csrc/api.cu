@@ -114,6 +114,30 @@ static size_t layout(Ctx& c, char* base) {
   c.hist = w.take<uint32_t>(int64_t(1 << kRadixMaxDigit) * radix_blocks(K) + 2);
   c.radix_aux = w.take<uint32_t>(kRadixAux);
   c.scan_tmp = w.take<char>(scan_bytes);
+  // the clustering sort (aux stream) and the occurrence sorts (sort stream)
+  // have separate scratch: they run concurrently
+  c.rx_aux.tkey[0] = c.tkey[0];
+  c.rx_aux.tkey[1] = c.tkey[1];
+  c.rx_aux.tval[0] = c.tval[0];
+  c.rx_aux.tval[1] = c.tval[1];
+  c.rx_aux.hist = c.hist;
+  c.rx_aux.scan_tmp = c.scan_tmp;
+  c.rx_aux.aux = c.radix_aux;
+  {
+    uint32_t* hs = w.take<uint32_t>(int64_t(1 << kRadixMaxDigit) * radix_blocks(K) + 2);
+    uint32_t* as = w.take<uint32_t>(kRadixAux);
+    char* ss = w.take<char>(scan_bytes);
+    for (int si = 0; si < 2; ++si) {
+      RadixScratch& rx = c.slot[si].rx;
+      for (int i = 0; i < 2; ++i) {
+        rx.tkey[i] = w.take<uint32_t>(K);
+        rx.tval[i] = w.take<int32_t>(K);
+      }
+      rx.hist = hs;
+      rx.aux = as;
+      rx.scan_tmp = ss;
+    }
+  }
   c.scan_tmp_win = w.take<char>(scan_bytes);
   c.samp_scratch = w.take<int32_t>(B + 2);
   c.packed = w.take<int64_t>(W > 1 ? K : 1);
@@ -382,6 +406,12 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       }
     }
     NEST_CUDA(cudaEventCreateWithFlags(&c->ev_scratch, cudaEventDisableTiming));
+    {
+      int lo = 0, hi = 0;
+      NEST_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      NEST_CUDA(cudaStreamCreateWithPriority(&c->sort_stream, cudaStreamNonBlocking, lo));
+      NEST_CUDA(cudaEventCreateWithFlags(&c->ev_sort_join, cudaEventDisableTiming));
+    }
     if (c->cl_u) NEST_CUDA(cudaMallocHost(&c->cl_hmax, sizeof(int32_t)));
     NEST_CUDA(cudaStreamSynchronize(st0));
     if (c->W > 1 && c->cfg.tower_train && c->cfg.tower_layers > 0 && nccl_uids == nullptr) {
@@ -452,6 +482,8 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
   if (c->ev_scratch) cudaEventDestroy(c->ev_scratch);
+  if (c->sort_stream) cudaStreamDestroy(c->sort_stream);
+  if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->cl_hmax) cudaFreeHost(c->cl_hmax);
   for (auto& kv : c->cl_graphs) cudaGraphExecDestroy(kv.second);
   for (auto& s : c->slot) {
@@ -485,6 +517,7 @@ nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int3
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] {
+    NEST_CHECK(c->route_open < 0, NEST_ERR_ORDER, "a route is open (nest_route_end first)");
     NEST_CHECK(N >= 1 && N <= c->Nmax, NEST_ERR_INVALID, "N out of range");
     NEST_CHECK(B >= 0 && B <= c->Bcap, NEST_ERR_INVALID, "B out of range");
     NEST_CHECK(B % N == 0, NEST_ERR_DIVISIBILITY, "B mod N != 0");
@@ -504,13 +537,14 @@ nest_status_t nest_fwp_schedule(nest_ctx_t* ctx, const int64_t* keys, const int3
   });
 }
 
-nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, const int32_t* bag_offsets,
-                         int64_t nnz, int32_t B, const int32_t* perm, const int32_t* mb_offsets,
-                         int32_t N, void* stream) {
+nest_status_t nest_route_begin(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, const int32_t* bag_offsets,
+                               int64_t nnz, int32_t B, const int32_t* perm, const int32_t* mb_offsets,
+                               int32_t N, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] {
     Slot& s = slot_of(*c, slot);
+    NEST_CHECK(c->route_open < 0, NEST_ERR_ORDER, "a route is already open (nest_route_end first)");
     NEST_CHECK(N >= 1 && N <= c->Nmax, NEST_ERR_INVALID, "N out of range");
     NEST_CHECK(B >= 1 && B <= c->Bcap, NEST_ERR_INVALID, "B out of range");
     NEST_CHECK(nnz >= 0 && nnz <= c->Kcap, NEST_ERR_CAPACITY, "nnz exceeds max_keys");
@@ -522,18 +556,45 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
     (void)mb_offsets;  // micro-batches are equal: mb_offsets[i] = i * B / N
     cudaStream_t st = S(stream);
     s.routed = false;
+    // the pipelined call order (route(t+1) inside window t, before update(t)
+    // is issued): the gather will skip K(t) and the refresh supplies it
+    {
+      Slot& o = c->slot[1 - slot];
+      s.skip_planned = c->gather_skip && o.routed && !o.updated;
+    }
     // the slot's previous batch must be fully consumed (window + refresh), and
     // its write-back done before this gather reads the shard (reading Q8)
     NEST_CUDA(cudaStreamWaitEvent(st, s.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, s.ev_free, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, c->ev_scratch, 0));
-    int pid = prof_begin(*c, ST_ROUTE, SK_AUX, st);
+    c->route_pid = prof_begin(*c, ST_ROUTE, SK_AUX, st);
     route_phase_a(*c, s, keys, bag_offsets, nnz, B, perm, N, st);
-    prof_end(*c, pid, st, 0.0, nullptr, 0.0, c->cfg.pooling == NEST_POOL_SUM ? 12 : 15);
+    prof_end(*c, c->route_pid, st, 0.0, nullptr, 0.0, c->cfg.pooling == NEST_POOL_SUM ? 12 : 15);
+    c->route_open = slot;
+    c->route_stream = st;
+  });
+}
+
+nest_status_t nest_route_end(nest_ctx_t* ctx, int32_t slot) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    Slot& s = slot_of(*c, slot);
+    NEST_CHECK(c->route_open == slot, NEST_ERR_ORDER, "nest_route_end without nest_route_begin on this slot");
+    c->route_open = -1;
+    cudaStream_t st = c->route_stream;
+    const int N = s.N;
     NEST_CUDA(cudaEventSynchronize(s.ev_sync));  // the one host sync (All2All sizes)
+    route_plan(*c, s);
+    // the occurrence sort (needed from this batch's backward on) on the
+    // library's lowest-priority stream: it overlaps phase B and the window
+    // (its input is phase A's, its scratch this slot's own)
+    NEST_CUDA(cudaStreamWaitEvent(c->sort_stream, s.ev_sync, 0));
+    route_sort(*c, s, c->sort_stream);
+    NEST_CUDA(cudaEventRecord(s.ev_sorted, c->sort_stream));
     route_phase_b(*c, s, st);
     // 12 K + 8 U_s (keys + inverse + uniq)
-    prof_add_bytes(*c, pid, 12.0 * double(s.info.nnz) + 8.0 * double(s.info.uniq));
+    prof_add_bytes(*c, c->route_pid, 12.0 * double(s.info.nnz) + 8.0 * double(s.info.uniq));
     NEST_CUDA(cudaEventRecord(s.ev_gather, st));
     s.routed = true;
     s.updated = false;
@@ -570,10 +631,16 @@ nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, con
       s.early = true;
       s.prefetched = (1u << N) - 1u;
     }
-    route_sort(*c, s, st);   // needed from this batch's backward on
-    NEST_CUDA(cudaEventRecord(s.ev_sorted, st));
     NEST_CUDA(cudaEventRecord(c->ev_scratch, st));
   });
+}
+
+
+nest_status_t nest_route(nest_ctx_t* ctx, int32_t slot, const int64_t* keys, const int32_t* bag_offsets,
+                         int64_t nnz, int32_t B, const int32_t* perm, const int32_t* mb_offsets,
+                         int32_t N, void* stream) {
+  const nest_status_t st = nest_route_begin(ctx, slot, keys, bag_offsets, nnz, B, perm, mb_offsets, N, stream);
+  return st != NEST_OK ? st : nest_route_end(ctx, slot);
 }
 
 nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t prefetch_slot, void* stream) {
@@ -853,7 +920,12 @@ nest_status_t nest_tower_step(nest_ctx_t* ctx, void* stream) {
 nest_status_t nest_join(nest_ctx_t* ctx, void* stream) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
-  return guard(c, [&] { tower_join(*c, S(stream)); });
+  return guard(c, [&] {
+    tower_join(*c, S(stream));
+    // ... and the occurrence sorts on the library's sort stream
+    NEST_CUDA(cudaEventRecord(c->ev_sort_join, c->sort_stream));
+    NEST_CUDA(cudaStreamWaitEvent(S(stream), c->ev_sort_join, 0));
+  });
 }
 
 nest_status_t nest_slot_info(const nest_ctx_t* ctx, int32_t slot, nest_slot_info_t* info) {
@@ -922,6 +994,12 @@ nest_status_t nest_profile_read(nest_ctx_t* ctx, nest_profile_stage_t* stages,
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] { profile_read(*c, stages, summary); });
+}
+
+nest_status_t nest_profile_records(nest_ctx_t* ctx, nest_profile_record_t* out, int64_t cap, int64_t* n) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !n) return NEST_ERR_INVALID;
+  return guard(c, [&] { profile_records(*c, out, cap, n); });
 }
 
 const char* nest_last_error(const nest_ctx_t* ctx) {

@@ -503,11 +503,11 @@ void launch_cluster(Ctx& c, const int64_t* keys, const int32_t* bag_offsets, int
                             [=] __device__(int64_t i, int32_t v) { wr[i] = v; }, c.scan_tmp, st);
   }
   k_cl_keyid<<<grid(nnz, 256), 256, 0, st>>>(nnz, keys, c.T, c.W, c.d_rows, c.d_seg_base, c.cl_bm, c.cl_wr, 0,
-                                            nullptr, c.tkey[0], c.tval[0], c.d_err);
+                                            nullptr, c.rx_aux.tkey[0], c.rx_aux.tval[0], c.d_err);
   k_cl_sample_of<<<grid(nbags, 256), 256, 0, st>>>(nbags, F, bag_offsets, samp);
   int kbits = 0;
   while ((int64_t(1) << kbits) < c.Kcap) ++kbits;
-  radix_sort_pairs(c, c.tkey[0], c.tval[0], c.cl_sk, c.cl_sv, nnz, kbits, st);
+  radix_sort_pairs(c.rx_aux, c.rx_aux.tkey[0], c.rx_aux.tval[0], c.cl_sk, c.cl_sv, nnz, kbits, st);
   k_cl_first<<<grid(nnz, 256), 256, 0, st>>>(nnz, c.cl_sk, c.cl_sv, samp, c.cl_u, c.cl_kstart);
   NEST_CUDA(cudaMemsetAsync(c.cl_small, 0, sizeof(int64_t) * 4, st));
   int32_t* maxsz = reinterpret_cast<int32_t*>(c.cl_small);

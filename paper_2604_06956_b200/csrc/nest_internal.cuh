@@ -65,6 +65,19 @@ constexpr uint32_t kRowFieldMask = (1u << kMbShift) - 1;
 // ----------------------------------------------------------------------------
 // context
 // ----------------------------------------------------------------------------
+// scratch of one LSD radix sort: ping-pong pairs, per-block digit
+// histograms, scan block sums, one-sweep aux words.  Two users run on
+// different streams, so each has its own: the clustering schedule (aux
+// stream, Ctx::rx_aux) and the occurrence sorts (the sort stream: per-slot
+// ping-pong pairs, shared histogram / scan / aux -- one sort at a time there)
+struct RadixScratch {
+  uint32_t* tkey[2] = {nullptr, nullptr};
+  int32_t* tval[2] = {nullptr, nullptr};
+  uint32_t* hist = nullptr;
+  void* scan_tmp = nullptr;
+  uint32_t* aux = nullptr;
+};
+
 struct Slot {
   // source side (this rank as requester)
   int64_t* uniq = nullptr;         // [Kcap]
@@ -72,6 +85,7 @@ struct Slot {
   uint32_t* mask = nullptr;        // [Kcap]
   int32_t* pos = nullptr;          // [Nmax][Kcap+1]
   uint32_t* skey = nullptr;        // [Kcap] sorted (mb << ubits | u)
+  RadixScratch rx;                 // the occurrence sort's scratch (rx.tkey[0] / tval[0]: its input)
   int32_t* sval = nullptr;         // [Kcap] sorted dout row of the occurrence
   int32_t* perm = nullptr;         // [Bcap]
   int32_t* bag_off = nullptr;      // [Bcap*F+1]
@@ -108,6 +122,7 @@ struct Slot {
   // the prefetch gather skipped the rows the other slot's pending update
   // writes (K(t) cap K(t+1)); nest_dbp_refresh supplies them
   bool refresh_pending = false;
+  bool skip_planned = false;       // nest_route_begin: the other slot's update was not yet issued
   cudaEvent_t ev_early = nullptr, ev_repush = nullptr;
   cudaEvent_t ev_sorted = nullptr;  // occurrences sorted (the segment-sum's input)
   cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
@@ -171,6 +186,9 @@ struct Ctx {
   int32_t* tval[2] = {nullptr, nullptr};
   uint32_t* hist = nullptr;        // [2^kRadixMaxDigit * radix blocks + 2] (one-sweep: tile status words)
   uint32_t* radix_aux = nullptr;   // [kRadixAux] one-sweep: global digit histograms of every pass + tile counter
+  RadixScratch rx_aux;             // the clustering schedule's radix sort (aux stream)
+  cudaStream_t sort_stream = nullptr;  // library stream (lowest priority): the occurrence sorts
+  cudaEvent_t ev_sort_join = nullptr;
   void* scan_tmp = nullptr;        // scan block sums, route-side streams (bytes)
   void* scan_tmp_win = nullptr;    // scan block sums, window-side streams
   int32_t* samp_scratch = nullptr; // [Bcap+1] unpooled sample prefix (route)
@@ -228,6 +246,9 @@ struct Ctx {
   bool connected = false;          // peers' windows mapped (nest_window_connect / NCCL exchange)
   size_t xoff_cnt = 0, xoff_key = 0, xoff_twr = 0, xcnt_stride = 0, xkey_stride = 0;
   uint32_t xepoch = 0;             // route exchanges so far (same sequence on every rank)
+  int route_open = -1;             // slot between nest_route_begin and nest_route_end (-1: none)
+  cudaStream_t route_stream = nullptr;
+  int route_pid = -1;              // its profile record
   std::vector<int32_t*> peer_cnt[2];   // each peer's count area of slot 0 / 1
   std::vector<int64_t*> peer_key[2];   // each peer's received-key area of slot 0 / 1
   // trained tower without NCCL: dW reduce-scatter / all-gather through the
@@ -321,6 +342,11 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+// bulk L2 prefetch of `bytes` (multiple of 16, 16-byte aligned) by the TMA
+// unit: no registers, no shared memory; the later register loads hit L2
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ float4 ld_f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ void st_f4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
@@ -522,9 +548,9 @@ inline int radix_blocks(int64_t n) { return int(n <= 0 ? 1 : (n + kRadixTile - 1
 // one-sweep aux words: 4 passes x 256 global digit counts + tile counter
 constexpr int kRadixAux = 4 * 256 + 32;
 
-void radix_sort_pairs_shifts(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
-                             int64_t n, const std::vector<int>& shifts, cudaStream_t st);
-void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+void radix_sort_pairs_shifts(const RadixScratch& rx, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+                             int32_t* vout, int64_t n, const std::vector<int>& shifts, cudaStream_t st);
+void radix_sort_pairs(const RadixScratch& rx, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                       int32_t* vout, int64_t n, int bits, cudaStream_t st);
 int radix_digit_bits(int bits);
 
@@ -533,6 +559,7 @@ int radix_digit_bits(int bits);
 // ----------------------------------------------------------------------------
 void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offsets, int64_t nnz,
                    int B, const int32_t* perm, int N, cudaStream_t st);
+void route_plan(Ctx& c, Slot& s);
 void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
 void route_sort(Ctx& c, Slot& s, cudaStream_t st);
 void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p);
@@ -556,6 +583,7 @@ void prof_add_bytes(Ctx& c, int id, double bytes) noexcept;
 void profile_enable(Ctx& c, bool on);
 void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* sum);
 void profile_destroy(Ctx& c);
+void profile_records(Ctx& c, nest_profile_record_t* out, int64_t cap, int64_t* n);
 struct ProfScope {
   Ctx& c;
   int id;

@@ -150,6 +150,20 @@ void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* 
   }
 }
 
+void profile_records(Ctx& c, nest_profile_record_t* out, int64_t cap, int64_t* n) {
+  Profiler& p = c.prof;
+  NEST_CUDA(cudaDeviceSynchronize());
+  *n = int64_t(p.recs.size());
+  if (!out) return;
+  for (int64_t i = 0; i < *n && i < cap; ++i) {
+    const ProfRec& r = p.recs[size_t(i)];
+    float t0 = 0, t1 = 0;
+    NEST_CUDA(cudaEventElapsedTime(&t0, p.ref, r.e0));
+    NEST_CUDA(cudaEventElapsedTime(&t1, p.ref, r.e1));
+    out[i] = nest_profile_record_t{r.stage, r.kind, double(t0), double(t1)};
+  }
+}
+
 void profile_destroy(Ctx& c) {
   Profiler& p = c.prof;
   for (auto e : p.pool) cudaEventDestroy(e);

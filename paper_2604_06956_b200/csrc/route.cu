@@ -296,19 +296,19 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_onesweep(
 }
 
 template <int DB>
-static void radix_pass(Ctx& c, const uint32_t* sk, const int32_t* sv, uint32_t* dk, int32_t* dv, int64_t n,
-                       int shift, int nb, cudaStream_t st) {
+static void radix_pass(const RadixScratch& rx, const uint32_t* sk, const int32_t* sv, uint32_t* dk, int32_t* dv,
+                       int64_t n, int shift, int nb, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     NEST_CUDA(cudaFuncSetAttribute(k_radix_scatter<DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(radix_scatter_smem<DB>())));
     attr = true;
   }
-  k_radix_hist<DB><<<nb, kRadixThreads, 0, st>>>(sk, n, shift, c.hist, nb);
-  uint32_t* h = c.hist;
+  k_radix_hist<DB><<<nb, kRadixThreads, 0, st>>>(sk, n, shift, rx.hist, nb);
+  uint32_t* h = rx.hist;
   scan_exclusive<uint32_t>([=] __device__(int64_t i) { return h[i]; }, int64_t(1u << DB) * nb,
-                           [=] __device__(int64_t i, uint32_t v) { h[i] = v; }, c.scan_tmp, st);
-  k_radix_scatter<DB><<<nb, kRadixThreads, radix_scatter_smem<DB>(), st>>>(sk, sv, n, shift, c.hist, nb, dk, dv);
+                           [=] __device__(int64_t i, uint32_t v) { h[i] = v; }, rx.scan_tmp, st);
+  k_radix_scatter<DB><<<nb, kRadixThreads, radix_scatter_smem<DB>(), st>>>(sk, sv, n, shift, rx.hist, nb, dk, dv);
   NEST_LAUNCH_CHECK();
 }
 
@@ -322,8 +322,8 @@ int radix_digit_bits(int bits) {
 
 // stable LSD sort by the 8-bit digits at the given shifts, in order (the
 // classic per-pass histogram + scan + scatter)
-void radix_sort_pairs_shifts(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout, int32_t* vout,
-                             int64_t n, const std::vector<int>& shifts, cudaStream_t st) {
+void radix_sort_pairs_shifts(const RadixScratch& rx, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+                             int32_t* vout, int64_t n, const std::vector<int>& shifts, cudaStream_t st) {
   if (n <= 0 || shifts.empty()) return;
   const int nb = radix_blocks(n);
   const uint32_t* sk = kin;
@@ -335,11 +335,11 @@ void radix_sort_pairs_shifts(Ctx& c, const uint32_t* kin, const int32_t* vin, ui
       dk = kout;
       dv = vout;
     } else {
-      const int t = (sk == c.tkey[0]) ? 1 : 0;
-      dk = c.tkey[t];
-      dv = c.tval[t];
+      const int t = (sk == rx.tkey[0]) ? 1 : 0;
+      dk = rx.tkey[t];
+      dv = rx.tval[t];
     }
-    radix_pass<8>(c, sk, sv, dk, dv, n, shifts[p], nb, st);
+    radix_pass<8>(rx, sk, sv, dk, dv, n, shifts[p], nb, st);
     sk = dk;
     sv = dv;
   }
@@ -358,7 +358,7 @@ static bool radix_classic() {
   return v;
 }
 
-void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
+void radix_sort_pairs(const RadixScratch& rx, const uint32_t* kin, const int32_t* vin, uint32_t* kout,
                       int32_t* vout, int64_t n, int bits, cudaStream_t st) {
   if (n <= 0) return;
   const int db = radix_digit_bits(bits);
@@ -371,8 +371,8 @@ void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t*
                                      int(radix_scatter_smem<8>())));
       attr = true;
     }
-    uint32_t* ghist = c.radix_aux;
-    uint32_t* ctr = c.radix_aux + 4 * 256;
+    uint32_t* ghist = rx.aux;
+    uint32_t* ctr = rx.aux + 4 * 256;
     NEST_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * passes * 256, st));
     k_radix_hist_all<<<std::min(nb, 148 * 4), kRadixThreads, 0, st>>>(kin, n, passes, db, ghist);
     const uint32_t* sk = kin;
@@ -384,14 +384,14 @@ void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t*
         dk = kout;
         dv = vout;
       } else {
-        const int t = (sk == c.tkey[0]) ? 1 : 0;
-        dk = c.tkey[t];
-        dv = c.tval[t];
+        const int t = (sk == rx.tkey[0]) ? 1 : 0;
+        dk = rx.tkey[t];
+        dv = rx.tval[t];
       }
-      NEST_CUDA(cudaMemsetAsync(c.hist, 0, sizeof(uint32_t) * 256 * size_t(nb), st));
+      NEST_CUDA(cudaMemsetAsync(rx.hist, 0, sizeof(uint32_t) * 256 * size_t(nb), st));
       NEST_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
       k_radix_onesweep<8><<<nb, kRadixThreads, radix_scatter_smem<8>(), st>>>(sk, sv, n, db * p, ghist + p * 256,
-                                                                            c.hist, ctr, dk, dv);
+                                                                            rx.hist, ctr, dk, dv);
       NEST_LAUNCH_CHECK();
       sk = dk;
       sv = dv;
@@ -407,12 +407,12 @@ void radix_sort_pairs(Ctx& c, const uint32_t* kin, const int32_t* vin, uint32_t*
       dk = kout;
       dv = vout;
     } else {
-      const int t = (sk == c.tkey[0]) ? 1 : 0;
-      dk = c.tkey[t];
-      dv = c.tval[t];
+      const int t = (sk == rx.tkey[0]) ? 1 : 0;
+      dk = rx.tkey[t];
+      dv = rx.tval[t];
     }
     static_assert(kRadixMaxDigit == 8, "instantiate radix_pass for the wider digits");
-    radix_pass<8>(c, sk, sv, dk, dv, n, db * p, nb, st);
+    radix_pass<8>(rx, sk, sv, dk, dv, n, db * p, nb, st);
     sk = dk;
     sv = dv;
   }
@@ -795,10 +795,10 @@ void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offs
   s.ubits = bits_for(c.Kcap);
   if (N == 1)
     k_inverse<true><<<grid_for(nnz, 256), 256, 0, st>>>(nnz, c.occ_dom, c.occ_mbrow, bm, wr, s.ubits, s.inverse,
-                                                        s.mask, c.tkey[0], c.tval[0]);
+                                                        s.mask, s.rx.tkey[0], s.rx.tval[0]);
   else
     k_inverse<false><<<grid_for(nnz, 256), 256, 0, st>>>(nnz, c.occ_dom, c.occ_mbrow, bm, wr, s.ubits, s.inverse,
-                                                         s.mask, c.tkey[0], c.tval[0]);
+                                                         s.mask, s.rx.tkey[0], s.rx.tval[0]);
   k_mb_counts<<<grid_for(c.Kcap, 256, 148 * 4), 256, 0, st>>>(s.off, W, N, s.mask, c.d_cnt_scratch);
   k_finalize_counts<<<1, 64, 0, st>>>(W, N, Nc, s.off, c.d_cnt_scratch, c.d_err,
                                       xfer + int64_t(c.rank) * W * Nc);
@@ -875,9 +875,9 @@ void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t
 }
 
 // after the host sync: plan from the counts, then R1 tail, R2 keys, R3, R4
-void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
-  const int W = c.W, N = s.N, Nc = c.Nmax + 2, D = c.D;
-  // ---- host plan ----
+// after the host sync: the batch's All2All plan from the gathered counts
+void route_plan(Ctx& c, Slot& s) {
+  const int W = c.W, N = s.N, Nc = c.Nmax + 2;
   s.all.assign(size_t(W) * W * Nc, 0);
   for (size_t i = 0; i < s.all.size(); ++i) s.all[i] = s.h_xfer[i];
   const int32_t* hmbnnz = s.h_xfer + int64_t(W) * W * Nc;
@@ -907,11 +907,16 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
   info.nnz = nnz;
   s.key_soff.assign(plan.key_send_off, plan.key_send_off + W + 1);
   s.key_roff.assign(plan.key_recv_off, plan.key_recv_off + W + 1);
+}
 
+// after route_plan: R1 tail, R2 keys, R3, R4 on `st`
+void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
+  const int W = c.W, N = s.N, Nc = c.Nmax + 2, D = c.D;
+  const int64_t U = s.info.uniq, R = s.info.recv;
   // ---- R1 tail: per micro-batch positions among its keys (the pool needs
-  // them); the occurrence sort follows the row traffic (route_sort) ----
+  // them); the occurrence sort runs on the sort stream (route_sort) ----
   {
-    ProfScope ps(c, ST_SORT, SK_AUX, st);
+    ProfScope ps(c, ST_ROUTE, SK_AUX, st);
     for (int i = 0; i < N; ++i) {
       const uint32_t* mk = s.mask;
       int32_t* pos = s.pos + int64_t(i) * (c.Kcap + 1);
@@ -1001,7 +1006,7 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     // this gather never waits for -- nor races -- that update; otherwise the
     // gather follows the other slot's update and reads its written-back rows
     Slot& o = c.slot[&s == &c.slot[0] ? 1 : 0];
-    const bool skip = c.gather_skip && o.routed && !o.updated;
+    const bool skip = s.skip_planned && o.routed;   // decided at nest_route_begin
     if (!skip && o.routed) NEST_CUDA(cudaStreamWaitEvent(st, o.ev_update, 0));
     s.refresh_pending = skip;
     ProfScope ps(c, ST_GATHER, SK_AUX, st);
@@ -1027,7 +1032,7 @@ void route_sort(Ctx& c, Slot& s, cudaStream_t st) {
   const int ub = std::min(bits_for(std::max<int64_t>(s.info.uniq, 2)), s.ubits);
   int passes;
   if (mbbits == 0) {
-    radix_sort_pairs(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, ub, st);
+    radix_sort_pairs(s.rx, s.rx.tkey[0], s.rx.tval[0], s.skey, s.sval, nnz, ub, st);
     const int db = radix_digit_bits(ub);
     passes = ub <= db ? 1 : (ub + db - 1) / db;
   } else {
@@ -1036,7 +1041,7 @@ void route_sort(Ctx& c, Slot& s, cudaStream_t st) {
     std::vector<int> shifts;
     for (int sh = 0; sh < ub; sh += kRadixMaxDigit) shifts.push_back(sh);
     shifts.push_back(s.ubits);
-    radix_sort_pairs_shifts(c, c.tkey[0], c.tval[0], s.skey, s.sval, nnz, shifts, st);
+    radix_sort_pairs_shifts(s.rx, s.rx.tkey[0], s.rx.tval[0], s.skey, s.sval, nnz, shifts, st);
     passes = int(shifts.size());
   }
   ps.launches = nnz > 0 ? 5 * passes : 0;

@@ -34,9 +34,20 @@ struct Tower {
   int64_t bmax = 0;
   __nv_bfloat16* w = nullptr;       // weights, layer l at woff[l], [H, in_l] row-major
   std::vector<int64_t> woff;
-  __nv_bfloat16* x = nullptr;       // activations X_0..X_{L-1}, X_l at xoff[l]
+  __nv_bfloat16* x = nullptr;       // activations X_0..X_{L-1}, X_l at xoff[l] (of the current buffer set)
   std::vector<int64_t> xoff;
   __nv_bfloat16* dy = nullptr;      // dY_l for l = 0..L-2 (layer l's output), [L-1][bmax, H]
+  // fixed tower: two activation / dY buffer sets used by alternate calls, so
+  // call k's forward overwrites the set of call k-2 and waits only for call
+  // k-2's deferred dW GEMMs (they read X and dY), not for call k-1's: the dW
+  // GEMMs of one batch overlap the next batch's pool and forward.  A trained
+  // tower has one set (its next forward needs the updated weights anyway).
+  __nv_bfloat16* xs[2] = {nullptr, nullptr};
+  __nv_bfloat16* dys[2] = {nullptr, nullptr};
+  int nsets = 1;
+  int64_t calls = 0;
+  cudaEvent_t ev_dwb[2] = {nullptr, nullptr};
+  bool pend_b[2] = {false, false};
   __nv_bfloat16* dw = nullptr;      // [H, max in]
   int acc = 0;                      // micro-batches accumulated into dw32 since the last tower_step
   int64_t acc_rows = 0;             // their rows (the next call's top-gradient offset)
@@ -69,9 +80,10 @@ size_t tower_workspace_bytes(const Ctx& c) {
   const int L = c.cfg.tower_layers, H = c.cfg.tower_hidden;
   if (L <= 0) return 0;
   const int64_t in0 = int64_t(c.F) * c.D, bmax = c.Bcap;
+  const int sets = c.cfg.tower_train ? 1 : 2;          // activation / dY buffer sets
   int64_t elems = H * in0 + int64_t(L - 1) * H * H;   // weights
-  elems += bmax * in0 + int64_t(L - 1) * bmax * H;   // activations
-  elems += int64_t(std::max(L - 1, 1)) * bmax * H;   // dY of layers 0..L-2 (>= 1: forward scratch)
+  elems += sets * (bmax * in0 + int64_t(L - 1) * bmax * H);   // activations
+  elems += sets * int64_t(std::max(L - 1, 1)) * bmax * H;     // dY of layers 0..L-2 (>= 1: forward scratch)
   elems += int64_t(H) * std::max<int64_t>(H, in0);   // dw
   elems += bmax * H;                                 // top gradient
   const int64_t wel = H * in0 + int64_t(L - 1) * H * H;
@@ -137,8 +149,13 @@ void tower_create(Ctx& c) {
   t->w = w.take<__nv_bfloat16>(t->woff[L]);
   t->xoff.assign(L + 1, 0);
   for (int l = 0; l < L; ++l) t->xoff[l + 1] = t->xoff[l] + bmax * (l == 0 ? in0 : H);
-  t->x = w.take<__nv_bfloat16>(t->xoff[L]);
-  t->dy = w.take<__nv_bfloat16>(int64_t(std::max(L - 1, 1)) * bmax * H);
+  t->nsets = c.cfg.tower_train ? 1 : 2;
+  for (int b = 0; b < t->nsets; ++b) {
+    t->xs[b] = w.take<__nv_bfloat16>(t->xoff[L]);
+    t->dys[b] = w.take<__nv_bfloat16>(int64_t(std::max(L - 1, 1)) * bmax * H);
+  }
+  t->x = t->xs[0];
+  t->dy = t->dys[0];
   t->dw = w.take<__nv_bfloat16>(int64_t(H) * std::max<int64_t>(H, in0));
   t->gtop = w.take<__nv_bfloat16>(bmax * H);
   t->ws = w.take<char>(int64_t(t->ws_bytes));
@@ -160,6 +177,7 @@ void tower_create(Ctx& c) {
     NEST_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, lo));   // lowest priority
     NEST_CUDA(cudaEventCreateWithFlags(&t->ev_dx, cudaEventDisableTiming));
     NEST_CUDA(cudaEventCreateWithFlags(&t->ev_dw, cudaEventDisableTiming));
+    for (auto& e : t->ev_dwb) NEST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   NEST_CUBLAS(cublasCreate(&t->h));
   NEST_CUBLAS(cublasSetWorkspace(t->h, t->ws, t->ws_bytes));
@@ -200,6 +218,8 @@ void tower_destroy(Ctx& c) {
   }
   if (t->ev_dx) cudaEventDestroy(t->ev_dx);
   if (t->ev_dw) cudaEventDestroy(t->ev_dw);
+  for (auto e : t->ev_dwb)
+    if (e) cudaEventDestroy(e);
   for (auto& kv : t->plans) {
     cublasLtMatmulDescDestroy(kv.second.op);
     cublasLtMatrixLayoutDestroy(kv.second.a);
@@ -303,6 +323,19 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
   if (bm == 0) return 0.0;
   NEST_CHECK(bm <= t->bmax, NEST_ERR_CAPACITY, "tower batch exceeds max_batch");
   const int L = t->L, H = t->H, in0 = t->in0, M = int(bm);
+  // buffer set of this call; its previous user's dW GEMMs still read X and dY
+  // (trained tower: one set, and the next forward also needs the updated weights)
+  const int bset = int(t->calls % t->nsets);
+  ++t->calls;
+  t->x = t->xs[bset];
+  t->dy = t->dys[bset];
+  if (t->nsets == 1) {
+    if (t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
+    t->dw_pending = false;
+  } else if (t->pend_b[bset]) {
+    NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dwb[bset], 0));
+    t->pend_b[bset] = false;
+  }
   // input of layer l (X_0: the caller's bf16 rows in place, or the cast copy)
   __nv_bfloat16* x0 = pooled_bf16 ? const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(pooled))
                                   : t->x;
@@ -316,9 +349,6 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
   NEST_CHECK(g0 + bm <= t->bmax, NEST_ERR_CAPACITY, "tower rows of one window exceed max_batch");
   auto DY = [&](int l) { return l == L - 1 ? t->gtop + g0 * H : t->dy + int64_t(l) * t->bmax * H; };
   auto IN = [&](int l) { return l == 0 ? in0 : H; };
-  // the previous call's dW GEMMs still read X and dY
-  if (t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));
-  t->dw_pending = false;
   if (!pooled_bf16) {
     k_cast_bf16<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const float*>(pooled), t->x, bm * in0 / 4);
     NEST_LAUNCH_CHECK();
@@ -365,6 +395,8 @@ double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, flo
   if (t->defer_dw) {
     NEST_CUDA(cudaEventRecord(t->ev_dw, t->side));
     t->dw_pending = true;
+    NEST_CUDA(cudaEventRecord(t->ev_dwb[bset], t->side));
+    t->pend_b[bset] = true;
   }
   return t->defer_dw ? 2.0 * flops_dw : 3.0 * flops_dw;   // FLOPs on `st` (fwd + dX [+ dW])
 }

@@ -118,6 +118,13 @@ class Runner:
         perm, mbo = self._schedule(slot, keys, offs, B, stream)
         self.ctx.route(slot, keys, offs, B, perm=perm, mb_offsets=mbo, N=self.N, stream=stream)
 
+    def _route_begin(self, slot, keys, offs, B, stream):
+        """DBP route of the next batch, first half (enqueue only): its host
+        sync happens in route_end, after the window's backward is enqueued, so
+        the compute lane never idles while the host waits for the counts."""
+        perm, mbo = self._schedule(slot, keys, offs, B, stream)
+        self.ctx.route_begin(slot, keys, offs, B, perm=perm, mb_offsets=mbo, N=self.N, stream=stream)
+
     def out_buffers(self, slot) -> List[torch.Tensor]:
         info = self.ctx.slot_info(slot)
         outs = []
@@ -144,9 +151,10 @@ class Runner:
         outs = self.out_buffers(a)
         self.outs = outs if keep_outputs else []
         # a dense consumer may read the pooled rows after this call returns
-        # (the tower's deferred dW GEMMs): keep them allocated until the next
-        # step has enqueued its own tower calls, which wait for those GEMMs
-        prev, self._hold = self._hold, outs
+        # (the tower's deferred dW GEMMs, which alternate two buffer sets):
+        # keep them allocated until the step after next has enqueued its tower
+        # calls, which wait for those GEMMs
+        self._hold = (self._hold + [outs])[-3:]
         if self.lanes == 2:
             return self._step_two_lanes(a, p, outs, next_batch, dout_fn)
         # embedding lane: pool_0, pool_1, seg_0, pool_2, seg_1, ... (pool of
@@ -160,16 +168,20 @@ class Runner:
                 ctx.lookup_prefetch(a, i + 1, cs, ms)
                 ctx.lookup_fwd(a, i + 1, outs[i + 1], cs, ms)
                 self._ev_pool[i + 1].record(cs)
+            route_next = i == self.N - 1 and self.pipelined and next_batch is not None
+            if route_next:
+                # DBP: route + retrieval of batch t+1 on the aux lane, inside window t
+                nk, no, nB = next_batch
+                self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
+                self._route_begin(p, nk, no, nB, self.aux)
             ds.wait_event(self._ev_pool[i])
             with torch.cuda.stream(ds):
                 dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
             self._ev_dense[i].record(ds)
             cs.wait_event(self._ev_dense[i])
-            if i == self.N - 1 and self.pipelined and next_batch is not None:
-                nk, no, nB = next_batch
-                self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
-                self._route(p, nk, no, nB, self.aux)      # host blocks for counts here
             self._grad(a, i, dout, cs, ms)
+            if route_next:
+                ctx.route_end(p)      # host blocks for the counts here, the window is queued
         if self.pipelined and next_batch is not None:
             ctx.dbp_refresh(a, p, cs)
         self.t += 1
@@ -188,13 +200,16 @@ class Runner:
         for i in range(self.N):
             if i + 1 < self.N:
                 ctx.lookup_prefetch(a, i + 1, cs, ms)
-            with torch.cuda.stream(cs):
-                dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
-            if i == self.N - 1 and self.pipelined and next_batch is not None:
+            route_next = i == self.N - 1 and self.pipelined and next_batch is not None
+            if route_next:
                 nk, no, nB = next_batch
                 self.aux.wait_stream(torch.cuda.current_stream(ctx.device))
-                self._route(p, nk, no, nB, self.aux)
+                self._route_begin(p, nk, no, nB, self.aux)
+            with torch.cuda.stream(cs):
+                dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
             self._grad(a, i, dout, cs, ms)
+            if route_next:
+                ctx.route_end(p)
             if i + 1 < self.N:
                 ctx.lookup_fwd(a, i + 1, outs[i + 1], cs, ms)
         if self.pipelined and next_batch is not None:
