@@ -85,6 +85,19 @@ def peaks():
     return 6650.0, 1400.0, "fallback"
 
 
+HBM_STAGES = ["route", "sort", "owner_dedup", "gather", "refresh", "send_gather", "pool", "segsum", "update"]
+
+
+def whole_step_hbm(st, steps, ms_step):
+    """Algorithmic HBM bytes of every stage of the step (SURVEY §8(d) per-kernel
+    formulas, summed) over the step time, against the measured copy peak."""
+    hbm_peak, _, src = peaks()
+    b = sum(st[n]["bytes"] for n in HBM_STAGES if n in st and st[n]["records"]) / steps
+    gbs = b / (ms_step * 1e6)
+    return {"bytes_per_step": b, "gbs": gbs, "peak": hbm_peak, "frac": gbs / hbm_peak, "peak_source": src,
+            "stages": [n for n in HBM_STAGES if n in st and st[n]["records"]]}
+
+
 def roofline_from(st, key_prefix):
     """HBM roofline of the dominant single-kernel stage of a profiled run:
     algorithmic bytes per launch / event-measured time per launch."""
@@ -172,11 +185,44 @@ def oracle_sample_step(cfg, seed, rank, samples, step=0):
     from oracle import step as OS
     keys, offs = WL.gen_batch(cfg, seed, step, rank, batch=samples)
     dout = WL.gen_dout(seed, step, rank, samples * cfg.num_features, cfg.dim, "realistic")
+    # the table rows exist before the step (PRF initialisation is table
+    # creation, not step work): materialise them outside the timed region
+    tab = OS.LazyTable(seed, cfg.dim)
+    tab.get(np.unique(keys))
     t0 = time.perf_counter()
     OR.route_source(keys, 1)
-    tab = OS.LazyTable(seed, cfg.dim)
     OS.sync_step(tab, [(keys, offs)], [dout], 1e-3, pooling=cfg.pooling)
     return time.perf_counter() - t0
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def tiny_oracle_baseline(seed, steps=10):
+    """SURVEY §8(d) oracle timing on the tiny config: 10 synchronous steps of
+    the global batch (W = 2 shards x 32 samples), routing + Eq. 1/2 step."""
+    from oracle import routing as OR
+    from oracle import step as OS
+    cfg = WL.CONFIGS["tiny"]
+    W = 2
+    tab = OS.LazyTable(seed, cfg.dim)
+    t0 = time.perf_counter()
+    for t in range(steps):
+        batches = [WL.gen_batch(cfg, seed, t, r) for r in range(W)]
+        douts = [WL.gen_dout(seed, t, r, cfg.batch_local * cfg.num_features, cfg.dim, "realistic") for r in range(W)]
+        OR.route_all(batches, W)
+        OS.sync_step(tab, batches, douts, 1e-3)
+    dt = time.perf_counter() - t0
+    return {"value": steps * W * cfg.batch_local / dt, "unit": UNIT, "steps": steps,
+            "sample": f"tiny config, {steps} steps of the global batch ({W} x {cfg.batch_local} samples), "
+                      f"oracle route_all + sync_step, {dt:.3f} s"}
 
 
 def cpu_baseline(cfg, seed, min_s=10.0):
@@ -188,15 +234,18 @@ def cpu_baseline(cfg, seed, min_s=10.0):
         samples = min(cfg.batch_local, samples * 4)
         dt = oracle_sample_step(cfg, seed, 0, samples)
     return {"value": samples / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "host_cpus": len(os.sched_getaffinity(0)),
+            "host_cpus": len(os.sched_getaffinity(0)), "cpu_model": cpu_model(),
             "sample": f"{samples} of {cfg.batch_local} samples of one rank's {cfg.name} batch; "
-                      f"oracle route_source + sync_step (numpy fp64, single thread), {dt:.2f} s"}
+                      f"oracle route_source + sync_step (numpy fp64, single thread), {dt:.2f} s",
+            "tiny_10_steps": tiny_oracle_baseline(seed)}
 
 
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    samples = 1024
+    # ~1.4 s of oracle work per step: the driver's --steps K --warmup W run
+    # stays within a few minutes
+    samples = 2048
     for t in range(args.warmup):
         oracle_sample_step(cfg, args.seed, 0, samples, t)
     tot = 0.0
@@ -209,7 +258,8 @@ def run_reference(args, cfg, rank, world):
             "data": "synthetic", "config": config_json(args, cfg, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{samples} samples per step of one rank's {cfg.name} batch "
-                                       "(oracle route_source + sync_step, numpy fp64, 1 thread)"},
+                                       "(oracle route_source + sync_step, numpy fp64, 1 thread; table rows "
+                                       "materialised before the timer)", "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -451,6 +501,7 @@ def main():
                 "samples_per_s": B * world * args.steps / (ms1 / 1e3),
                 # the same roofline kernel without the tower's GEMMs beside it
                 "roofline": roofline_from(st1, f"{cfg.name}/W{world}/N{Nv}"),
+                "whole_step_hbm": whole_step_hbm(st1, args.steps, ms1 / args.steps),
                 "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in st1.items() if v["records"]}}
 
     # host-DRAM tier (NEXT-3): the retrieval's PCIe rate against the measured
@@ -554,7 +605,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_json(args, cfg, world), "roofline": roofline, "cpu_baseline": cpu,
+                "config": config_json(args, cfg, world), "roofline": roofline,
+                "whole_step_hbm": whole_step_hbm(st, steps, ms / steps), "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": int(summ["launches"]), "clocks": clk, "a2a": a2a,
                 "stages": stages,
                 "trace": {"span_ms_per_step": summ["span_ms"] / steps,
