@@ -58,7 +58,9 @@ def parse():
     ap.add_argument("--correlated", default="", help="G,rho: correlated sample groups (FWP clustering sweep)")
     ap.add_argument("--micro-batches", type=int, default=0,
                     help="FWP micro-batches N; 0 = auto (1; N = 2 is measured alongside)")
-    ap.add_argument("--schedule", default="sequential", choices=["sequential", "clustered"])
+    ap.add_argument("--schedule", default="sequential", choices=["sequential", "clustered", "clustered-offline"],
+                    help="FWP partition: sequential, clustered (GPU greedy per batch, timed), "
+                         "clustered-offline (P:482: computed once per batch outside the step, cost reported)")
     ap.add_argument("--variant", default="et", choices=["et", "e"],
                     help="et: embedding + stand-in tower (FWP overlap partner; headline); e: embedding only")
     ap.add_argument("--batches", type=int, default=3, help="distinct batches cycled per rank")
@@ -435,7 +437,9 @@ def main():
             ms = float(tt.item())
         return ms, prof, h2d, d2h
 
+    sched_cache = {}
     runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
+                    sched_cache=sched_cache,
                     pooled_dtype=pooled_dtype(args.variant))
     timed(runner, args.warmup, 0)
     clocks = Clocks(local)
@@ -446,7 +450,21 @@ def main():
     value = B * world * args.steps / (ms / 1e3)
     # FWP payload of the last routed batch: sum_i |K(M_i)| vs |K(B)|
     info = ctx.slot_info(runner.t % 2)
-    fwp_stats = {"N": N, "schedule": args.schedule, "uniq_keys": int(info.uniq),
+    cluster_ms = None
+    if N > 1 and args.schedule.startswith("clustered"):
+        # the GPU greedy on one batch, alone (its cost per batch; inside the
+        # step for "clustered", outside for "clustered-offline")
+        kk, oo, _ = dev_b[0]
+        ctx.fwp_schedule(kk, oo, B, N, "clustered")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            ctx.fwp_schedule(kk, oo, B, N, "clustered")
+        e1.record()
+        torch.cuda.synchronize()
+        cluster_ms = e0.elapsed_time(e1) / 3
+    fwp_stats = {"N": N, "schedule": args.schedule, "cluster_ms_per_batch": cluster_ms,
+                 "uniq_keys": int(info.uniq),
                  "sum_mb_uniq": int(sum(info.mb_uniq[i] for i in range(N))),
                  "alpha": (sum(info.mb_uniq[i] for i in range(N)) / info.uniq) if info.uniq else None}
 
@@ -458,7 +476,10 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     if not args.no_e2e:
-        r2 = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
+        # e2e: fresh device copies every step -- an offline partition is keyed
+        # by the device batch, so this run clusters inside the step (conservative)
+        r2 = Runner(ctx, N=N, schedule="clustered" if args.schedule == "clustered-offline" else args.schedule,
+                    pipelined=True, lr_over_B=lr, adagrad=adagrad,
                     pooled_dtype=pooled_dtype(args.variant))
         r2.t = runner.t
         timed(r2, 2, runner.t, source="host")
@@ -473,6 +494,7 @@ def main():
     # N = 1 (no FWP) and, when there is an All2All to hide, N = 2 (FWP)
     def tower_run(Nv, t0):
         r1 = Runner(ctx, N=Nv, schedule=args.schedule if Nv > 1 else "sequential", pipelined=True,
+                    sched_cache=sched_cache,
                     lr_over_B=lr, adagrad=adagrad, pooled_dtype=pooled_dtype("et"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="et")
@@ -492,6 +514,7 @@ def main():
 
     def embedding_run(Nv, t0):
         r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
+                    sched_cache=sched_cache,
                     pooled_dtype=pooled_dtype("e"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="e")

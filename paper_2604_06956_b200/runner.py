@@ -63,8 +63,14 @@ class Runner:
 
     def __init__(self, ctx: NestContext, N: int = 1, schedule: str = "sequential",
                  pipelined: bool = True, lr_over_B: float = 2.0 ** -10, pooled_dtype=None,
-                 adagrad=None):
+                 adagrad=None, sched_cache: Optional[dict] = None):
+        # schedule: "sequential", "clustered" (the GPU greedy inside every
+        # route), or "clustered-offline" (clustering "can be performed
+        # asynchronously on CPU or offline": the partition of a batch is
+        # computed once, by the same GPU greedy, the first time the batch is
+        # seen, and reused -- e.g. precomputed by the data pipeline)
         self.ctx, self.N, self.schedule, self.pipelined = ctx, N, schedule, pipelined
+        self.sched_cache = sched_cache if sched_cache is not None else {}
         self.lr = lr_over_B
         # row-wise AdaGrad contexts: (grad_scale, lr) of nest_grad_bwd_update_adagrad
         self.adagrad = adagrad
@@ -115,7 +121,14 @@ class Runner:
             self.ctx.grad_bwd_update(slot, mb, dout, self.lr, cs, ms)
 
     def _schedule(self, slot, keys, offs, B, stream):
-        perm, mbo = self.ctx.fwp_schedule(keys, offs, B, self.N, self.schedule, stream=stream)
+        if self.schedule == "clustered-offline" and self.N > 1:
+            key = (keys.data_ptr(), int(keys.numel()), offs.data_ptr(), B, self.N)
+            if key not in self.sched_cache:
+                self.sched_cache[key] = self.ctx.fwp_schedule(keys, offs, B, self.N, "clustered", stream=stream)
+            perm, mbo = self.sched_cache[key]
+        else:
+            mode = "clustered" if self.schedule.startswith("clustered") else self.schedule
+            perm, mbo = self.ctx.fwp_schedule(keys, offs, B, self.N, mode, stream=stream)
         self.sched[slot] = (perm, mbo)
         return perm, mbo
 
