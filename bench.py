@@ -68,6 +68,8 @@ def parse():
                     help="sparse update: SGD of Eq. 2 (default) or row-wise AdaGrad (SURVEY NEXT-2)")
     ap.add_argument("--tables", default="hbm", choices=["hbm", "host"],
                     help="table tier: HBM (default) or pinned host DRAM over PCIe (SURVEY NEXT-3)")
+    ap.add_argument("--tower-layers", type=int, default=0,
+                    help="stand-in tower depth L (0: the config's, 4); the FWP sweep runs L in {2, 4, 8} (P:832-835)")
     ap.add_argument("--tower-train", action="store_true",
                     help="train the stand-in tower: dense dW AllReduce + SGD on the dW stream (SURVEY NEXT-4)")
     ap.add_argument("--seed", type=int, default=0)
@@ -291,6 +293,8 @@ def main():
     cfg = WL.CONFIGS[args.config]
     if args.zipf > 0:
         cfg = cfg.with_(zipf=args.zipf)
+    if args.tower_layers > 0:
+        cfg = cfg.with_(tower_layers=args.tower_layers)
     if cfg.pooling == "none":
         args.variant = "e"     # the stand-in tower is defined on pooled rows only
     rank = int(os.environ.get("RANK", "0"))
