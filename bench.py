@@ -330,10 +330,12 @@ def main():
     # exchanged per micro-batch (sum_i U_{s,i} <= min(K, N * U_s))
     U = max(len(np.unique(k)) for k, _ in batches)
     if world > 1:
+        # one configuration on every rank (the exchange windows and the
+        # capacity decisions of the count exchange must agree)
         import torch.distributed as dist_
-        t = torch.tensor([U], device=dev)
+        t = torch.tensor([U, K], device=dev)
         dist_.all_reduce(t, op=dist_.ReduceOp.MAX)
-        U = int(t.item())
+        U, K = int(t[0].item()), int(t[1].item())
     Nctx = max(N, 2) if world > 1 else N      # room for the FWP comparison run
     with_tower = cfg.pooling == "sum" and (args.variant == "et" or not args.no_fwp_compare)
     mb_rows = min(K, Nctx * U) + 1024

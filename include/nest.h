@@ -192,6 +192,15 @@ NEST_API nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_ui
                           nest_ctx_t** out);
 NEST_API nest_status_t nest_destroy(nest_ctx_t* ctx);
 
+/* Checked mode (environment NEST_GUARD=1 when the context is sized and
+ * created): every workspace buffer is followed by a 256-byte guard band filled
+ * with a pattern at nest_create; this call counts the guard words that no
+ * longer hold it, i.e. out-of-bounds writes into the workspace since creation
+ * (a substitute for compute-sanitizer memcheck, unavailable on the GPU pool).
+ * Enqueued on `stream` after its work, then synchronises it.  *bad_words = 0
+ * when every band is intact.  NEST_ERR_INVALID outside checked mode. */
+NEST_API nest_status_t nest_check_guards(nest_ctx_t* ctx, void* stream, int64_t* bad_words);
+
 /* Exchange-window record of one rank (host bytes; plain data the caller moves
  * between ranks with any transport, e.g. torch.distributed.all_gather_object):
  * the window's device pointer and CUDA IPC handle plus its geometry. */

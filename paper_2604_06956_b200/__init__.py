@@ -113,6 +113,13 @@ class NestContext:
             C.memmove(C.byref(arr, i * C.sizeof(L.WindowRec)), r, C.sizeof(L.WindowRec))
         self._check(self.lib.nest_window_connect(self.ctx, arr))
 
+    def check_guards(self, stream=None) -> int:
+        """Checked mode (NEST_GUARD=1 at creation): number of overwritten guard
+        words after the workspace buffers (nest_check_guards; 0 = intact)."""
+        n = C.c_int64()
+        self._check(self.lib.nest_check_guards(self.ctx, _stream(stream), C.byref(n)))
+        return int(n.value)
+
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
         if getattr(self, "ctx", None):

@@ -23,7 +23,7 @@ MAX_MICRO_BATCHES = 8
 
 # every symbol include/nest.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_shard_rows",
-           "nest_create", "nest_destroy", "nest_window_export", "nest_window_connect", "nest_init_tables", "nest_fwp_schedule", "nest_route", "nest_route_begin", "nest_route_end",
+           "nest_create", "nest_destroy", "nest_window_export", "nest_window_connect", "nest_check_guards", "nest_init_tables", "nest_fwp_schedule", "nest_route", "nest_route_begin", "nest_route_end",
            "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_lookup_fwd_bf16",
            "nest_grad_bwd_update", "nest_grad_bwd_update_adagrad", "nest_tower_fwd_bwd",
            "nest_tower_fwd_bwd_bf16", "nest_tower_step", "nest_join", "nest_read_state", "nest_tower_read",
@@ -122,6 +122,7 @@ def load() -> C.CDLL:
         "nest_create": ([C.POINTER(Config), vp, vp, vp, vp, C.POINTER(vp)], i32),
         "nest_destroy": ([vp], i32),
         "nest_window_export": ([vp, C.POINTER(WindowRec)], i32),
+        "nest_check_guards": ([vp, vp, C.POINTER(i64)], i32),
         "nest_window_connect": ([vp, C.POINTER(WindowRec)], i32),
         "nest_init_tables": ([vp, vp], i32),
         "nest_fwp_schedule": ([vp, vp, vp, i64, i32, i32, i32, vp, vp, vp], i32),

@@ -87,6 +87,7 @@ static void derive(Ctx& c, const nest_config_t* cfg) {
     c.OMBcap = cfg->max_owner_mb_rows > 0 ? cfg->max_owner_mb_rows
                                           : (c.Nmax > 1 ? 2 * c.Rcap : c.Rcap);
   c.Pcap = 2 * c.Kcap / 32 + 64;   // partial rows for chunk length >= 32
+  if (const char* g = std::getenv("NEST_GUARD")) c.guard = std::atoi(g) != 0;
   if (const char* e = std::getenv("NEST_SEG_CHUNK")) c.seg_chunk = std::max(32, std::atoi(e));
 }
 
@@ -95,6 +96,8 @@ void tower_bind(Ctx& c, char* mem);
 
 static size_t layout(Ctx& c, char* base) {
   Carver w{base};
+  c.guard_offs.clear();
+  if (c.guard) w.guards = &c.guard_offs;
   const int64_t K = c.Kcap, B = c.Bcap, R = c.Rcap, Uo = c.Uocap, D = c.D, W = c.W, Nm = c.Nmax;
   const int Nc = c.Nmax + 2;
   int64_t maxn = std::max<int64_t>({c.words + 2, c.owords + 2, K + 2, R + 2, B + 2,
@@ -384,6 +387,17 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       zero_f32(c->opt_state, std::max<int64_t>(c->Vo, 1), S(stream));
     }
     layout(*c, reinterpret_cast<char*>(work_mem));
+    c->work_base = reinterpret_cast<char*>(work_mem);
+    if (c->guard && !c->guard_offs.empty()) {
+      const size_t ng = c->guard_offs.size();
+      NEST_CUDA(cudaMalloc(&c->d_guard_offs, sizeof(uint64_t) * ng));
+      NEST_CUDA(cudaMalloc(&c->d_guard_bad, sizeof(unsigned long long)));
+      std::vector<uint64_t> go(c->guard_offs.begin(), c->guard_offs.end());
+      NEST_CUDA(cudaMemcpyAsync(c->d_guard_offs, go.data(), sizeof(uint64_t) * ng, cudaMemcpyHostToDevice,
+                                S(stream)));
+      guards_fill(*c, S(stream));
+      NEST_CUDA(cudaStreamSynchronize(S(stream)));
+    }
     cudaStream_t st0 = S(stream);
     NEST_CUDA(cudaMemcpyAsync(c->d_rows, c->rows.data(), sizeof(int64_t) * c->T, cudaMemcpyHostToDevice, st0));
     NEST_CUDA(cudaMemcpyAsync(c->d_seg_base, c->seg_base.data(), sizeof(int64_t) * c->seg_base.size(),
@@ -472,10 +486,21 @@ nest_status_t nest_window_connect(nest_ctx_t* ctx, const nest_window_rec_t* recs
   return guard(c, [&] { xfer_connect(*c, recs); });
 }
 
+nest_status_t nest_check_guards(nest_ctx_t* ctx, void* stream, int64_t* bad_words) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !bad_words) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CHECK(c->guard, NEST_ERR_INVALID, "context not created in checked mode (NEST_GUARD=1)");
+    *bad_words = guards_check(*c, S(stream));
+  });
+}
+
 nest_status_t nest_destroy(nest_ctx_t* ctx) {
   if (!ctx) return NEST_OK;
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   cudaDeviceSynchronize();
+  if (c->d_guard_offs) cudaFree(c->d_guard_offs);
+  if (c->d_guard_bad) cudaFree(c->d_guard_bad);
   if (c->tower) tower_destroy(*c);
   profile_destroy(*c);
   xfer_destroy(*c);

@@ -234,6 +234,12 @@ struct Ctx {
   // records it, whatever stream the caller uses
   cudaEvent_t ev_scratch = nullptr;
   int seg_chunk = 32;              // segment-sum: cold threshold = hot chunk length (>= 32)
+  // checked mode (NEST_GUARD=1): guard band offsets in work_mem, device copy, mismatch counter
+  bool guard = false;
+  std::vector<size_t> guard_offs;
+  uint64_t* d_guard_offs = nullptr;
+  unsigned long long* d_guard_bad = nullptr;
+  char* work_base = nullptr;
   // copy-engine / fused All2All transports (xfer.cu)
   bool xfer_ce = false;            // peer windows mapped (CE or fused mode)
   int a2a_mode = 0;                // A2AMode
@@ -287,14 +293,26 @@ inline float* peer_src_of(const Ctx& c, const Slot& s, int p) { return c.peer_sr
 constexpr int kClHistLog = 14, kClHistBins = 1 << kClHistLog, kClIds = 1024;
 
 // bump allocator over a caller-owned buffer (base == nullptr: size only)
+// Checked mode (NEST_GUARD=1): a guard band of kGuardBytes follows every
+// buffer; nest_create fills the bands with kGuardWord and nest_check_guards
+// counts the words some kernel overwrote (out-of-bounds writes into the
+// workspace; compute-sanitizer is not available on the GPU pool)
+constexpr size_t kGuardBytes = 256;
+constexpr uint32_t kGuardWord = 0xA5C3A5C3u;
 struct Carver {
   char* base;
   size_t off = 0;
+  std::vector<size_t>* guards = nullptr;   // guard band offsets (checked mode)
   template <class T>
   T* take(int64_t n) {
     off = (off + 255) & ~size_t(255);
     T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
     off += size_t(std::max<int64_t>(n, 1)) * sizeof(T);
+    if (guards) {
+      off = (off + 255) & ~size_t(255);
+      guards->push_back(off);
+      off += kGuardBytes;
+    }
     return p;
   }
 };
@@ -583,6 +601,8 @@ void prof_add_bytes(Ctx& c, int id, double bytes) noexcept;
 void profile_enable(Ctx& c, bool on);
 void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* sum);
 void profile_destroy(Ctx& c);
+void guards_fill(Ctx& c, cudaStream_t st);
+int64_t guards_check(Ctx& c, cudaStream_t st);
 void profile_records(Ctx& c, nest_profile_record_t* out, int64_t cap, int64_t* n);
 struct ProfScope {
   Ctx& c;

@@ -164,6 +164,35 @@ void profile_records(Ctx& c, nest_profile_record_t* out, int64_t cap, int64_t* n
   }
 }
 
+// checked mode: guard bands after every workspace buffer
+__global__ void k_guard_fill(char* base, const uint64_t* __restrict__ offs, int64_t n) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    uint32_t* g = reinterpret_cast<uint32_t*>(base + offs[i]);
+    for (int j = threadIdx.x; j < int(kGuardBytes / 4); j += blockDim.x) g[j] = kGuardWord;
+  }
+}
+__global__ void k_guard_check(const char* base, const uint64_t* __restrict__ offs, int64_t n,
+                              unsigned long long* bad) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t* g = reinterpret_cast<const uint32_t*>(base + offs[i]);
+    for (int j = threadIdx.x; j < int(kGuardBytes / 4); j += blockDim.x)
+      if (g[j] != kGuardWord) atomicAdd(bad, 1ull);
+  }
+}
+void guards_fill(Ctx& c, cudaStream_t st) {
+  k_guard_fill<<<148, 64, 0, st>>>(c.work_base, c.d_guard_offs, int64_t(c.guard_offs.size()));
+  NEST_LAUNCH_CHECK();
+}
+int64_t guards_check(Ctx& c, cudaStream_t st) {
+  NEST_CUDA(cudaMemsetAsync(c.d_guard_bad, 0, sizeof(unsigned long long), st));
+  k_guard_check<<<148, 64, 0, st>>>(c.work_base, c.d_guard_offs, int64_t(c.guard_offs.size()), c.d_guard_bad);
+  NEST_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  NEST_CUDA(cudaMemcpyAsync(&h, c.d_guard_bad, sizeof(h), cudaMemcpyDeviceToHost, st));
+  NEST_CUDA(cudaStreamSynchronize(st));
+  return int64_t(h);
+}
+
 void profile_destroy(Ctx& c) {
   Profiler& p = c.prof;
   for (auto e : p.pool) cudaEventDestroy(e);

@@ -53,12 +53,18 @@ def run_case(case, rank, world, dev):
     connect(ctx, world)
     pooled = MR.run_rank(case, ctx, rank, batches, douts, dev)
     res = (pooled,) + MR.collect(case, ctx, rank, world, batches, dev)
+    guard_ok = True
+    if os.environ.get("NEST_GUARD") == "1":   # checked mode: no out-of-bounds workspace write
+        bad = ctx.check_guards()
+        guard_ok = bad == 0
+        print(f"[{case.name}] rank {rank}: guard bands {'intact' if guard_ok else f'{bad} words overwritten'}",
+              flush=True)
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(res, gathered, dst=0)
     ok = MR.verify(case, world, batches, douts, gathered) if rank == 0 else True
     ctx.close()
-    flag = flag_tensor(ok, dev)
-    dist.broadcast(flag, 0)
+    flag = flag_tensor(ok and guard_ok, dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     return bool(flag.item())
 
 

@@ -458,6 +458,33 @@ def test_edge_many_features_per_sample(d, N):
     _p1_check(cfg, batches, N=N)
 
 
+# --------------------------------------------------------------------------- checked mode
+@pytest.mark.parametrize("N", [1, 2])
+def test_checked_mode_guard_bands(monkeypatch, N):
+    """Checked mode (NEST_GUARD=1): after pipelined multi-step runs with hot
+    segments, ragged bags and empty bags, every guard band after the workspace
+    buffers is intact (no out-of-bounds write), and the check does detect a
+    clobbered workspace (negative control)."""
+    monkeypatch.setenv("NEST_GUARD", "1")
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(4000, 50, 9, 2000), zipf=1.3, bag_len=(0, 6), bag_repeats=True,
+                                   dim=64)
+    batches = [WL.gen_batch(cfg, 40 + t, t, 0, batch=128) for t in range(4)]
+    _p1_check(cfg, batches, N=N)
+    ctx = make_ctx(cfg, 128, N=N, K=max(len(k) for k, _ in batches))
+    run = Runner(ctx, N=N, pipelined=True, lr_over_B=2.0 ** -10)
+    db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), 128) for k, o in batches]
+    F, d, cap = cfg.num_features, cfg.dim, 128 // N
+    dd = torch.ones((128 * F, d), device=DEV)
+    for t in range(4):
+        run.step(db[t], db[t + 1] if t + 1 < 4 else None, lambda tt, i, p: dd[i * cap * F:(i + 1) * cap * F])
+    run.join()
+    torch.cuda.synchronize()
+    assert ctx.check_guards() == 0
+    ctx.work_mem.zero_()                      # negative control: clobber the workspace
+    torch.cuda.synchronize()
+    assert ctx.check_guards() > 0
+
+
 # --------------------------------------------------------------------------- trained tower (NEXT-4)
 def test_trained_tower_sgd_step_matches_definition():
     """NEXT-4 at W=1: one tower call with tower_train applies W0 - lr * G^T X0
