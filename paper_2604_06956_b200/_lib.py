@@ -8,7 +8,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnest.so")
+# NEST_LIB: an alternative in-tree build (tuning variants built with
+# build.build(out=...)); default: the libnest.so build() writes
+LIB_PATH = os.environ.get("NEST_LIB") or os.path.join(HERE, "libnest.so")
 
 NEST_OK = 0
 STATUS = {0: "NEST_OK", 1: "NEST_ERR_INVALID", 2: "NEST_ERR_CUDA", 3: "NEST_ERR_NCCL",

@@ -1221,7 +1221,7 @@ void launch_segsum_to(Ctx& c, Slot& s, int mb, const float* dout, const PeerRows
           k_segsum_range<D, SU, false><<<emb_blocks(nr, gpb), kRowThreads, 0, st>>>(
               Ki, skey, umask, pos, sval, dout, out, c.partial, c.hot_list, c.seg_tot, pf_mask() & 1);
       });
-      k_segsum_fix<D, 4><<<blocks_for_rows(nr / 4 + 1, gpb, 148 * 2), kRowThreads, 0, st>>>(
+      k_segsum_fix<D, 4><<<blocks_for_rows(nr / 4 + 1, gpb, 148 * 8), kRowThreads, 0, st>>>(
           Ki, skey, umask, pos, c.hot_list, c.seg_tot, c.partial, out, c.seg_aux, c.seg_tot + 1);
       k_segsum_fix_big<D><<<148, kRowThreads, 0, st>>>(Ki, c.seg_aux, c.seg_tot + 1, c.partial, out);
     });
