@@ -369,6 +369,13 @@ NEST_API nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pool
 enum { NEST_TOWER_WEIGHTS = 0, NEST_TOWER_TOP_GRAD = 1 };
 NEST_API nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, float* out, void* stream);
 
+/* Replace the library's internal streams with the caller's (NULL keeps
+ * one): the occurrence sorts of nest_route_end and the tower's deferred dW
+ * GEMMs -- e.g. streams of green contexts that split the SMs between the
+ * embedding lanes and the dense tower.  The caller keeps them alive until
+ * nest_destroy.  Synchronises the device first. */
+NEST_API nest_status_t nest_set_streams(nest_ctx_t* ctx, void* sort_stream, void* tower_dw_stream);
+
 /* Trained tower (tower_train = 1, NEXT-4): apply the batch's accumulated
  * dense gradient -- AllReduce over the ranks + one SGD step -- after the last
  * micro-batch's nest_tower_fwd_bwd* call (one dense update per

@@ -507,7 +507,7 @@ nest_status_t nest_destroy(nest_ctx_t* ctx) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_aux) ncclCommDestroy(c->comm_aux);
   if (c->ev_scratch) cudaEventDestroy(c->ev_scratch);
-  if (c->sort_stream) cudaStreamDestroy(c->sort_stream);
+  if (c->sort_stream && c->sort_stream_owned) cudaStreamDestroy(c->sort_stream);
   if (c->ev_sort_join) cudaEventDestroy(c->ev_sort_join);
   if (c->cl_hmax) cudaFreeHost(c->cl_hmax);
   for (auto& kv : c->cl_graphs) cudaGraphExecDestroy(kv.second);
@@ -934,6 +934,20 @@ nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, floa
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] { tower_read(*c, what, layer, out, S(stream)); });
+}
+
+nest_status_t nest_set_streams(nest_ctx_t* ctx, void* sort_stream, void* tower_dw_stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] {
+    NEST_CUDA(cudaDeviceSynchronize());
+    if (sort_stream) {
+      if (c->sort_stream_owned) NEST_CUDA(cudaStreamDestroy(c->sort_stream));
+      c->sort_stream = S(sort_stream);
+      c->sort_stream_owned = false;
+    }
+    if (tower_dw_stream) tower_set_side(*c, S(tower_dw_stream));
+  });
 }
 
 nest_status_t nest_tower_step(nest_ctx_t* ctx, void* stream) {

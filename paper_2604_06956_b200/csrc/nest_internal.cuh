@@ -188,6 +188,7 @@ struct Ctx {
   uint32_t* radix_aux = nullptr;   // [kRadixAux] one-sweep: global digit histograms of every pass + tile counter
   RadixScratch rx_aux;             // the clustering schedule's radix sort (aux stream)
   cudaStream_t sort_stream = nullptr;  // library stream (lowest priority): the occurrence sorts
+  bool sort_stream_owned = true;
   cudaEvent_t ev_sort_join = nullptr;
   void* scan_tmp = nullptr;        // scan block sums, route-side streams (bytes)
   void* scan_tmp_win = nullptr;    // scan block sums, window-side streams
@@ -685,6 +686,7 @@ void tower_destroy(Ctx& c);
 double tower_run(Ctx& c, const void* pooled, bool pooled_bf16, int64_t rows, float* dout, cudaStream_t st);
 void tower_join(Ctx& c, cudaStream_t st);
 void tower_step(Ctx& c, cudaStream_t st);
+void tower_set_side(Ctx& c, cudaStream_t st);
 void tower_read(Ctx& c, int what, int layer, float* out, cudaStream_t st);
 
 }  // namespace nest

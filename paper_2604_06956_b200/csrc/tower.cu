@@ -57,6 +57,7 @@ struct Tower {
   size_t ws_bytes = 32u << 20;
   bool defer_dw = true;
   cudaStream_t side = nullptr;      // dW GEMMs
+  bool side_owned = true;           // false: the caller's stream (nest_set_streams)
   cudaEvent_t ev_dx = nullptr, ev_dw = nullptr;
   bool dw_pending = false;
   char* mem = nullptr;
@@ -214,7 +215,7 @@ void tower_destroy(Ctx& c) {
   if (t->comm) ncclCommDestroy(t->comm);
   if (t->side) {
     cudaStreamSynchronize(t->side);
-    cudaStreamDestroy(t->side);
+    if (t->side_owned) cudaStreamDestroy(t->side);
   }
   if (t->ev_dx) cudaEventDestroy(t->ev_dx);
   if (t->ev_dw) cudaEventDestroy(t->ev_dw);
@@ -502,6 +503,17 @@ void tower_read(Ctx& c, int what, int layer, float* out, cudaStream_t st) {
 }
 
 // make `st` wait for outstanding dW GEMMs (context teardown / host reads)
+// the dW GEMMs on the caller's stream instead of the library's (e.g. one of a
+// green context holding the dense lane's SMs)
+void tower_set_side(Ctx& c, cudaStream_t st) {
+  Tower* t = reinterpret_cast<Tower*>(c.tower);
+  if (!t || !st) return;
+  NEST_CUDA(cudaStreamSynchronize(t->side));
+  if (t->side_owned) NEST_CUDA(cudaStreamDestroy(t->side));
+  t->side = st;
+  t->side_owned = false;
+}
+
 void tower_join(Ctx& c, cudaStream_t st) {
   Tower* t = reinterpret_cast<Tower*>(c.tower);
   if (t && t->dw_pending) NEST_CUDA(cudaStreamWaitEvent(st, t->ev_dw, 0));

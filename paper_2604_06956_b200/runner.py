@@ -90,10 +90,14 @@ class Runner:
         if green > 0:
             # hard SM partition (green contexts): the sparse lanes (embedding,
             # comm, DBP lookahead) get `green` SMs, the dense tower the rest
-            sparse_s, dense_s = _green_streams(dev, green, [pe, pc, 0], [pd])
-            self.compute, comm, self.aux = sparse_s
+            sparse_s, dense_s = _green_streams(dev, green, [pe, pc, -5, 0], [pd, 0])
+            self.compute, comm, self.aux, sort_s = sparse_s
             self.comm = comm if ctx.world > 1 else self.compute
-            self.dense = dense_s[0]
+            self.dense, dw_s = dense_s
+            # the library's sort stream with the sparse lanes, the tower's dW
+            # stream with the dense lane
+            ctx.set_streams(sort_stream=sort_s, tower_dw_stream=dw_s if ctx.cfg.tower_layers > 0 else None)
+            self._green_keep = (sort_s, dw_s)
         else:
             self.compute = torch.cuda.Stream(device=dev, priority=pe)            # embedding lane
             self.comm = torch.cuda.Stream(device=dev, priority=pc) if ctx.world > 1 else self.compute
