@@ -172,11 +172,13 @@ class Runner:
             self.primed = True
         outs = self.out_buffers(a)
         self.outs = outs if keep_outputs else []
-        # a dense consumer may read the pooled rows after this call returns
-        # (the tower's deferred dW GEMMs, which alternate two buffer sets):
-        # keep them allocated until the step after next has enqueued its tower
-        # calls, which wait for those GEMMs
-        self._hold = (self._hold + [outs])[-3:]
+        # a bf16 dense consumer reads the pooled rows in place after this call
+        # returns (the tower's deferred dW GEMMs, which alternate two buffer
+        # sets): keep them allocated until the step after next has enqueued its
+        # tower calls, which wait for those GEMMs (fp32 rows are cast into the
+        # tower's own buffer first: nothing to hold)
+        keep = 3 if self.pooled_dtype == torch.bfloat16 else 1
+        self._hold = (self._hold + [outs])[-keep:]
         if self.lanes == 2:
             return self._step_two_lanes(a, p, outs, next_batch, dout_fn)
         # embedding lane: pool_0, pool_1, seg_0, pool_2, seg_1, ... (pool of
