@@ -52,6 +52,12 @@ def test_host_only_calls(lib):
     cfg.table_location = 7
     assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 1  # INVALID
     assert b"table_location" in lib.nest_last_error(None)
+    # tower width checked before any collective initialisation (nest_create)
+    cfg.table_location = L.TABLE_HBM
+    cfg.tower_layers, cfg.tower_hidden = 2, 8
+    assert lib.nest_workspace_bytes(C.byref(cfg), C.byref(tb), C.byref(wb)) == 1  # INVALID
+    assert b"tower_hidden" in lib.nest_last_error(None)
+    cfg.tower_layers = 0
     assert lib.nest_version().startswith(b"nestpipe")
 
 

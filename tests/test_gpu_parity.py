@@ -636,6 +636,59 @@ def test_error_paths():
         ctx.route(0, to_dev(keys, torch.int64), to_dev(offs, torch.int32), 32)
 
 
+def test_route_split_and_window_misuse():
+    """nest_route_begin / nest_route_end ordering, and the NCCL-free window
+    rendezvous: out-of-order calls are NEST_ERR_ORDER, foreign or misordered
+    records NEST_ERR_INVALID, checked-mode queries outside checked mode
+    NEST_ERR_INVALID -- and a context stays usable after a host-side error."""
+    cfg = WL.CONFIGS["tiny"]
+    keys, offs = WL.gen_batch(cfg, 0, 0, 0, batch=32)
+    kd, od = to_dev(keys, torch.int64), to_dev(offs, torch.int32)
+    ctx = make_ctx(cfg, 32, N=2)
+    with pytest.raises(NestError) as e:
+        ctx.route_end(0)                               # no route begun
+    assert e.value.status == "NEST_ERR_ORDER"
+    ctx.route_begin(0, kd, od, 32)
+    with pytest.raises(NestError) as e:
+        ctx.route_begin(1, kd, od, 32)                 # scratch in use
+    assert e.value.status == "NEST_ERR_ORDER"
+    with pytest.raises(NestError) as e:
+        ctx.fwp_schedule(kd, od, 32, 2, "clustered")   # scratch in use
+    assert e.value.status == "NEST_ERR_ORDER"
+    out = torch.empty((32 * cfg.num_features, cfg.dim), device=DEV)
+    with pytest.raises(NestError) as e:
+        ctx.lookup_fwd(0, 0, out)                      # slot not routed until route_end
+    assert e.value.status == "NEST_ERR_ORDER"
+    ctx.route_end(0)
+    ctx.lookup_fwd(0, 0, out)                          # usable again
+    torch.cuda.synchronize()
+    ref = OS.forward(OS.LazyTable(1, cfg.dim, "dyadic"), keys, offs)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    with pytest.raises(NestError) as e:
+        ctx.check_guards()
+    assert e.value.status == "NEST_ERR_INVALID"
+    # NCCL-free world of 2 in one process: route before connect, bad records
+    c0 = make_ctx(cfg, 32, world=2, rank=0)
+    c1 = make_ctx(cfg, 32, world=2, rank=1)
+    with pytest.raises(NestError) as e:
+        c0.route(0, kd, od, 32)
+    assert e.value.status == "NEST_ERR_ORDER"
+    r0, r1 = c0.window_export(), c1.window_export()
+    with pytest.raises(NestError) as e:
+        c0.window_connect([r1, r0])                    # not in rank order
+    assert e.value.status == "NEST_ERR_INVALID"
+    c2 = make_ctx(cfg.with_(dim=32), 32, world=2, rank=1)
+    with pytest.raises(NestError) as e:
+        c0.window_connect([r0, c2.window_export()])    # another geometry
+    assert e.value.status == "NEST_ERR_INVALID"
+    c0.window_connect([r0, r1])
+    with pytest.raises(NestError) as e:
+        c0.window_connect([r0, r1])
+    assert e.value.status == "NEST_ERR_ORDER"
+    for c in (c2, c1, c0, ctx):
+        c.close()
+
+
 def test_refresh_required_after_pipelined_route():
     """Routing the next batch while the active slot's update is pending makes
     its gather skip K(t) (the refresh supplies those rows): a lookup of that
