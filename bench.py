@@ -444,8 +444,11 @@ def main():
         return ms, prof, h2d, d2h
 
     sched_cache = {}
+    # the route's host sync after the tower is queued (E+T) / after the
+    # backward is queued (E): DESIGN.md §1, Runner(route_end=...)
+    rend = {"et": "before_grad", "e": "after_grad"}
     runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
-                    sched_cache=sched_cache,
+                    sched_cache=sched_cache, route_end=rend[args.variant],
                     pooled_dtype=pooled_dtype(args.variant))
     timed(runner, args.warmup, 0)
     clocks = Clocks(local)
@@ -485,7 +488,7 @@ def main():
         # e2e: fresh device copies every step -- an offline partition is keyed
         # by the device batch, so this run clusters inside the step (conservative)
         r2 = Runner(ctx, N=N, schedule="clustered" if args.schedule == "clustered-offline" else args.schedule,
-                    pipelined=True, lr_over_B=lr, adagrad=adagrad,
+                    pipelined=True, lr_over_B=lr, adagrad=adagrad, route_end=rend[args.variant],
                     pooled_dtype=pooled_dtype(args.variant))
         r2.t = runner.t
         timed(r2, 2, runner.t, source="host")
@@ -500,7 +503,7 @@ def main():
     # N = 1 (no FWP) and, when there is an All2All to hide, N = 2 (FWP)
     def tower_run(Nv, t0):
         r1 = Runner(ctx, N=Nv, schedule=args.schedule if Nv > 1 else "sequential", pipelined=True,
-                    sched_cache=sched_cache,
+                    sched_cache=sched_cache, route_end=rend["et"],
                     lr_over_B=lr, adagrad=adagrad, pooled_dtype=pooled_dtype("et"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="et")
@@ -520,7 +523,7 @@ def main():
 
     def embedding_run(Nv, t0):
         r1 = Runner(ctx, N=Nv, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
-                    sched_cache=sched_cache,
+                    sched_cache=sched_cache, route_end=rend["e"],
                     pooled_dtype=pooled_dtype("e"))
         r1.t = t0
         timed(r1, 3, r1.t, variant="e")

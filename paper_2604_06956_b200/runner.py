@@ -15,6 +15,7 @@ order); all work runs in libnest.so.  The order follows the paper:
 """
 from __future__ import annotations
 
+import os
 from typing import Callable, List, Optional
 
 import torch
@@ -63,7 +64,7 @@ class Runner:
 
     def __init__(self, ctx: NestContext, N: int = 1, schedule: str = "sequential",
                  pipelined: bool = True, lr_over_B: float = 2.0 ** -10, pooled_dtype=None,
-                 adagrad=None, sched_cache: Optional[dict] = None):
+                 adagrad=None, sched_cache: Optional[dict] = None, route_end: Optional[str] = None):
         # schedule: "sequential", "clustered" (the GPU greedy inside every
         # route), or "clustered-offline" (clustering "can be performed
         # asynchronously on CPU or offline": the partition of a batch is
@@ -71,6 +72,14 @@ class Runner:
         # seen, and reused -- e.g. precomputed by the data pipeline)
         self.ctx, self.N, self.schedule, self.pipelined = ctx, N, schedule, pipelined
         self.sched_cache = sched_cache if sched_cache is not None else {}
+        # when the DBP route of the next batch does its host sync (nest_route_end):
+        # "after_grad" (default) once the window's backward is queued, so the
+        # compute lane has work while the host waits for the counts; or
+        # "before_grad" right after the dense lane's work (the stand-in tower)
+        # is queued -- that work covers the wait, and the gather / owner
+        # dedup then run beside the tower instead of beside the segment-sum
+        # (NEST_ROUTE_END overrides)
+        self.route_end_mode = os.environ.get("NEST_ROUTE_END") or route_end or "after_grad"
         self.lr = lr_over_B
         # row-wise AdaGrad contexts: (grad_scale, lr) of nest_grad_bwd_update_adagrad
         self.adagrad = adagrad
@@ -78,7 +87,6 @@ class Runner:
         self.pooled_dtype = pooled_dtype or torch.float32
         self._hold: List[torch.Tensor] = []
         dev = ctx.device
-        import os
         # block-scheduling priorities (lower = scheduled first as SMs free up):
         # dense tower > comm > embedding, so the overlapped sparse work takes
         # the SMs the GEMMs leave (NEST_LANE_PRIORITIES="dense,comm,emb")
@@ -203,8 +211,10 @@ class Runner:
                 dout = dout_fn(self.t, i, outs[i]) if dout_fn else outs[i]
             self._ev_dense[i].record(ds)
             cs.wait_event(self._ev_dense[i])
+            if route_next and self.route_end_mode == "before_grad":
+                ctx.route_end(p)      # host blocks for the counts; the dense lane is busy
             self._grad(a, i, dout, cs, ms)
-            if route_next:
+            if route_next and self.route_end_mode != "before_grad":
                 ctx.route_end(p)      # host blocks for the counts here, the window is queued
         if self.pipelined and next_batch is not None:
             ctx.dbp_refresh(a, p, cs)
