@@ -21,19 +21,23 @@
  *           shard plays the role of the host store written back to).
  * Memory    every device byte is owned by the caller: query sizes with
  *           nest_workspace_bytes, pass device pointers (e.g. torch tensors).
- *           The library owns only NCCL communicators, CUDA events and small
- *           pinned host mirrors.  Pointers are device pointers unless marked
- *           "host".  Inputs are read-only.
+ *           The library owns only its NCCL communicators (when given ids),
+ *           the exchange windows (W > 1: peer-mapped row / count / key areas
+ *           and flags), CUDA events, two internal streams (the occurrence
+ *           sorts, the tower's dW GEMMs; replaceable, nest_set_streams) and
+ *           small pinned host mirrors.  Pointers are device pointers unless
+ *           marked "host".  Inputs are read-only.
  * Streams   `void*` arguments named *stream / compute / comm are cudaStream_t
  *           (NULL = the legacy default stream).  All calls are
- *           stream-asynchronous except nest_route (one host sync for the
- *           All2All sizes), nest_create and nest_destroy.
+ *           stream-asynchronous except nest_route / nest_route_end (one host
+ *           sync for the All2All sizes), nest_create,
+ *           nest_destroy, nest_set_streams and the read-back helpers.
  * Slots     two pipeline slots (0/1) hold the per-batch state: routing
  *           results and one HBM buffer each; their roles (active/prefetch)
  *           alternate every step.
  * Errors    host-detectable errors return immediately and leave the context
  *           unchanged.  Device-detected errors (key out of range, foreign key
- *           at an owner) are raised at the next nest_route sync, become
+ *           at an owner) are raised at the next nest_route(_end) sync, become
  *           sticky, and every later call returns that code (CUDA-style).
  *           Calls never abort or throw.  nest_last_error gives a message.
  *           Collective consistency: the count exchange carries every rank's
