@@ -1037,10 +1037,18 @@ void route_sort(Ctx& c, Slot& s, cudaStream_t st) {
     passes = ub <= db ? 1 : (ub + db - 1) / db;
   } else {
     // LSD over the u digits, then the micro-batch digit at ubits (a u digit
-    // that also covers micro-batch bits only refines the order of the last pass)
+    // that also covers micro-batch bits only refines the order of the last
+    // pass) -- or, when fewer passes, plain 8-bit digits over the whole
+    // (mb << ubits | u) key: the bits between bits(U_s) and ubits are zero, so
+    // e.g. DLRM N=2 (u < 2^21, ubits 22) sorts in 3 passes instead of 4
     std::vector<int> shifts;
     for (int sh = 0; sh < ub; sh += kRadixMaxDigit) shifts.push_back(sh);
     shifts.push_back(s.ubits);
+    const int total = s.ubits + mbbits;
+    if ((total + kRadixMaxDigit - 1) / kRadixMaxDigit < int(shifts.size())) {
+      shifts.clear();
+      for (int sh = 0; sh < total; sh += kRadixMaxDigit) shifts.push_back(sh);
+    }
     radix_sort_pairs_shifts(s.rx, s.rx.tkey[0], s.rx.tval[0], s.skey, s.sval, nnz, shifts, st);
     passes = int(shifts.size());
   }
