@@ -620,7 +620,6 @@ nest_status_t nest_route_end(nest_ctx_t* ctx, int32_t slot) {
     route_phase_b(*c, s, st);
     // 12 K + 8 U_s (keys + inverse + uniq)
     prof_add_bytes(*c, c->route_pid, 12.0 * double(s.info.nnz) + 8.0 * double(s.info.uniq));
-    NEST_CUDA(cudaEventRecord(s.ev_gather, st));
     s.routed = true;
     s.updated = false;
     s.prefetched = 0;
@@ -656,6 +655,10 @@ nest_status_t nest_route_end(nest_ctx_t* ctx, int32_t slot) {
       s.early = true;
       s.prefetched = (1u << N) - 1u;
     }
+    // the positions last: the early push above does not need them, the
+    // lookups of this batch do (ev_gather: "route complete")
+    route_positions(*c, s, st);
+    NEST_CUDA(cudaEventRecord(s.ev_gather, st));
     NEST_CUDA(cudaEventRecord(c->ev_scratch, st));
   });
 }
@@ -740,7 +743,9 @@ static nest_status_t lookup_fwd_impl(Ctx* c, int32_t slot, int32_t mb, void* out
     NEST_CHECK(out != nullptr, NEST_ERR_INVALID, "null out");
     cudaStream_t cs = S(compute), ms = S(comm);
     if (c->W > 1 && s.early) {
-      // rows pushed at route time (+ the refresh's re-push) by every owner
+      // rows pushed at route time (+ the refresh's re-push) by every owner;
+      // ev_gather: the route is complete (the positions come after the push)
+      NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_early, 0));
       xfer_wait_emb(*c, s, mb, cs, XK_EMB);
       if (s.repushed) {
@@ -788,7 +793,10 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
     NEST_CHECK(dout != nullptr || s.info.mb_out_rows[mb] == 0, NEST_ERR_INVALID, "null dout");
     cudaStream_t cs = S(compute), ms = S(comm);
     const double row = double(c->D) * sizeof(float);
-    if (mb == 0) NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
+    if (mb == 0) {
+      NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_sorted, 0));   // segment-sum input
+      NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));   // ... and the key positions
+    }
     if (c->W == 1 && s.N == 1) {
       // one rank, one micro-batch: the segment-sum applies Eq. 2 itself (the
       // next slot's gather skipped this slot's rows: no ordering with it,

@@ -581,6 +581,7 @@ void route_phase_a(Ctx& c, Slot& s, const int64_t* keys, const int32_t* bag_offs
 void route_plan(Ctx& c, Slot& s);
 void route_phase_b(Ctx& c, Slot& s, cudaStream_t st);
 void route_sort(Ctx& c, Slot& s, cudaStream_t st);
+void route_positions(Ctx& c, Slot& s, cudaStream_t st);
 void exchange_plan(const Ctx& c, int N, const int32_t* all, nest_exchange_plan_t& p);
 void zero_f32(float* p, int64_t n, cudaStream_t st);
 void launch_init_tables(Ctx& c, cudaStream_t st);

@@ -913,19 +913,6 @@ void route_plan(Ctx& c, Slot& s) {
 void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
   const int W = c.W, N = s.N, Nc = c.Nmax + 2, D = c.D;
   const int64_t U = s.info.uniq, R = s.info.recv;
-  // ---- R1 tail: per micro-batch positions among its keys (the pool needs
-  // them); the occurrence sort runs on the sort stream (route_sort) ----
-  {
-    ProfScope ps(c, ST_ROUTE, SK_AUX, st);
-    for (int i = 0; i < N; ++i) {
-      const uint32_t* mk = s.mask;
-      int32_t* pos = s.pos + int64_t(i) * (c.Kcap + 1);
-      scan_exclusive<int32_t>([=] __device__(int64_t u) { return int32_t((mk[u] >> i) & 1u); }, U,
-                              [=] __device__(int64_t u, int32_t v) { pos[u] = v; }, c.scan_tmp, st);
-    }
-    ps.launches = 3 * N;
-    ps.bytes = double(U) * 4 * (1 + N);   // masks read + N positions written
-  }
 
   if (W == 1) {
     // owner == source: the owner-unique keys are the unique keys
@@ -1015,6 +1002,23 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     ps.bpc = 2.0 * c.D * sizeof(float);  // 2 U_o row
   }
   (void)D;
+}
+
+// R1 tail: per micro-batch positions of the keys among that micro-batch's
+// keys (the pool and the segment-sum of this batch need them; nothing in the
+// route does, so nest_route_end issues them after the gather and early push)
+void route_positions(Ctx& c, Slot& s, cudaStream_t st) {
+  const int N = s.N;
+  const int64_t U = s.info.uniq;
+  ProfScope ps(c, ST_ROUTE, SK_AUX, st);
+  for (int i = 0; i < N; ++i) {
+    const uint32_t* mk = s.mask;
+    int32_t* pos = s.pos + int64_t(i) * (c.Kcap + 1);
+    scan_exclusive<int32_t>([=] __device__(int64_t u) { return int32_t((mk[u] >> i) & 1u); }, U,
+                            [=] __device__(int64_t u, int32_t v) { pos[u] = v; }, c.scan_tmp, st);
+  }
+  ps.launches = 3 * N;
+  ps.bytes = double(U) * 4 * (1 + N);   // masks read + N positions written
 }
 
 // R1 tail: occurrences sorted by (micro-batch, key) -- the grouping of the
