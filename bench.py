@@ -49,7 +49,7 @@ def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=10)   # >= 10 warm-up, >= 50 timed
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="dlrm", choices=["dlrm", "tiny", "dbp_stress", "genrec"])
     ap.add_argument("--zipf", type=float, default=0.0, help="override the config's Zipf skew (FWP sweep)")
@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--tower-train", action="store_true",
                     help="train the stand-in tower: dense dW AllReduce + SGD on the dW stream (SURVEY NEXT-4)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--seeds", type=int, default=1,
+                    help="SURVEY §8(d) protocol: time the step on the batches of seeds seed..seed+n-1 "
+                         "(one context, re-routed per seed) and report the median step time")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fwp-compare", action="store_true",
@@ -324,11 +327,13 @@ def main():
     N = args.micro_batches
     B, F, d = cfg.batch_local, cfg.num_features, cfg.dim
     batches = rank_batches(cfg, args.seed, rank, args.batches, args)
-    K = max(len(k) for k, _ in batches)
+    # --seeds n: the other seeds' batches too (capacities cover all of them)
+    extra = [rank_batches(cfg, args.seed + i, rank, args.batches, args) for i in range(1, max(1, args.seeds))]
+    K = max(len(k) for k, _ in batches + [b for bs in extra for b in bs])
     # capacities from the actual batches: unique keys per batch bound the
     # received keys per owner (balanced by the row mod W rule) and the rows
     # exchanged per micro-batch (sum_i U_{s,i} <= min(K, N * U_s))
-    U = max(len(np.unique(k)) for k, _ in batches)
+    U = max(len(np.unique(k)) for k, _ in batches + [b for bs in extra for b in bs])
     if world > 1:
         # one configuration on every rank (the exchange windows and the
         # capacity decisions of the count exchange must agree)
@@ -398,7 +403,7 @@ def main():
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    def timed(runner, steps, t0, source=None, profile=False, variant=None):
+    def timed(runner, steps, t0, source=None, profile=False, variant=None, dev_b=dev_b):
         """Runs `steps` steps; returns device ms (max over ranks)."""
         dout_fn = make_dout_fn(variant or args.variant, runner.N)
         barrier()
@@ -477,6 +482,26 @@ def main():
                  "sum_mb_uniq": int(sum(info.mb_uniq[i] for i in range(N))),
                  "alpha": (sum(info.mb_uniq[i] for i in range(N)) / info.uniq) if info.uniq else None}
 
+    seed_ms, seed_median_ms = None, None
+    if extra:
+        # the same timed loop on every seed's batches, median
+        # reported (the profiled statistics stay those of the first seed)
+        seed_ms = [ms / args.steps]
+        for i, bs in enumerate(extra):
+            db = [(torch.from_numpy(k).to(dev), torch.from_numpy(o).to(dev), B) for k, o in bs]
+            rs = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
+                        sched_cache={}, route_end=rend[args.variant], pooled_dtype=pooled_dtype(args.variant))
+            rs.t = runner.t + 16 * (i + 1)
+            timed(rs, args.warmup, rs.t, dev_b=db)
+            ms_i, _, _, _ = timed(rs, args.steps, rs.t, dev_b=db)
+            seed_ms.append(ms_i / args.steps)
+            rs._hold, rs.outs = [], []
+            runner.t = rs.t          # later runners continue from the last routed slot
+            del db
+        seed_median_ms = statistics.median(seed_ms)
+    if seed_median_ms is not None:
+        ms = seed_median_ms * args.steps
+        value = B * world * args.steps / (ms / 1e3)
     # e2e through the public API with host inputs (copies inside the timed region)
     e2e = None
     # release the timed runner's held outputs (gen-rec: 17 GB per step) before
@@ -653,6 +678,8 @@ def main():
                         "intersection_ratio": (rs["units"] / (st["gather"]["units"] + rs["units"])
                                                if st["gather"]["units"] + rs["units"] else None)},
                 "fwp": dict(fwp_stats, with_tower=with_tower_runs),
+                "seeds": None if seed_ms is None else {"first": args.seed, "n": len(seed_ms),
+                                                       "ms_per_step": seed_ms, "value_is": "median"},
                 "embedding_only": embedding_only}
         if host_tier is not None:
             line["host_tier"] = host_tier
