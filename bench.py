@@ -537,6 +537,7 @@ def main():
         sm, st1 = prof1["summary"], prof1["stages"]
         tw = st1["tower"]
         out = {"N": Nv, "steps": k2, "ms_per_step": ms1 / k2, "samples_per_s": B * world * k2 / (ms1 / 1e3),
+               "roofline": roofline_from(st1, f"{cfg.name}/W{world}/N{Nv}"),
                "tower_ms_per_step": tw["ms"] / k2,
                "tower_tflops": (tw["bytes"] + st1["tower_dw"]["bytes"]) / ((tw["ms"] + st1["tower_dw"]["ms"]) * 1e9)
                if tw["ms"] else None}
@@ -559,7 +560,7 @@ def main():
                 # the same roofline kernel without the tower's GEMMs beside it
                 "roofline": roofline_from(st1, f"{cfg.name}/W{world}/N{Nv}"),
                 "whole_step_hbm": whole_step_hbm(st1, args.steps, ms1 / args.steps),
-                "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in st1.items() if v["records"]}}
+                "stage_ms_per_step": {k: v["ms"] / args.steps for k, v in st1.items() if v["records"]}}, r1.t
 
     # host-DRAM tier (NEXT-3): the retrieval's PCIe rate against the measured
     # pinned H2D copy, and the step with DBP off (route + retrieval inline)
@@ -596,7 +597,7 @@ def main():
                      "ms_per_step_dbp": ms / args.steps,
                      "ms_per_step_sequential": ms_seq / max(5, args.steps // 2)}
 
-    with_tower_runs, embedding_only = None, None
+    with_tower_runs, embedding_only, zero_copy = None, None, None
     if not args.no_fwp_compare:
         tnext = runner.t + args.steps + 8
         if args.variant == "et":
@@ -609,7 +610,19 @@ def main():
                 if N2 <= ctx.cfg.max_micro_batches:
                     res, tnext = tower_run(N2, tnext)
                     with_tower_runs[f"N{N2}"] = res
-            embedding_only = embedding_run(N, tnext + 8)
+            embedding_only, tnext = embedding_run(N, tnext + 8)
+            if world == 1 and N == 1 and args.tables == "hbm" and cfg.pooling == "sum":
+                # zero-copy retrieval: the same steps without the
+                # DBP retrieval copy and refresh -- the shard read in place
+                ctx.set_zero_copy(True)
+                zc_et, tnext = tower_run(1, tnext + 8)
+                zc_e, tnext = embedding_run(1, tnext + 8)
+                ctx.set_zero_copy(False)
+                zero_copy = {"note": "W=1 HBM tables: no retrieval copy (R4) / refresh (R5); pool and fused "
+                                     "update read the shard in place; same results (parity tests)",
+                             "et": {k: zc_et[k] for k in ("ms_per_step", "samples_per_s", "roofline")},
+                             "e": {k: zc_e[k] for k in ("ms_per_step", "samples_per_s", "roofline",
+                                                        "whole_step_hbm")}}
         elif with_tower:
             with_tower_runs = {}
             for Nv in ([1, 2] if world > 1 and ctx.cfg.max_micro_batches >= 2 else [1]):
@@ -680,7 +693,7 @@ def main():
                 "fwp": dict(fwp_stats, with_tower=with_tower_runs),
                 "seeds": None if seed_ms is None else {"first": args.seed, "n": len(seed_ms),
                                                        "ms_per_step": seed_ms, "value_is": "median"},
-                "embedding_only": embedding_only}
+                "embedding_only": embedding_only, "zero_copy": zero_copy}
         if host_tier is not None:
             line["host_tier"] = host_tier
         if args.trace:

@@ -373,6 +373,16 @@ NEST_API nest_status_t nest_tower_fwd_bwd_bf16(nest_ctx_t* ctx, const void* pool
 enum { NEST_TOWER_WEIGHTS = 0, NEST_TOWER_TOP_GRAD = 1 };
 NEST_API nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, float* out, void* stream);
 
+/* Zero-copy retrieval (also NEST_ZERO_COPY=1 at creation): batches routed
+ * from now on with world == 1, one micro-batch and HBM tables skip the
+ * retrieval copy (R4) -- the pool and the fused update read and update the
+ * shard rows in place -- and so need no dual-buffer refresh (R5): the lookup
+ * of such a batch is ordered after the previous window's update (reading
+ * Q8), which is the synchronous result the refresh restores otherwise
+ * (P:370-378).  Other batches keep the buffered DBP path.  Host-side only;
+ * takes effect at the next nest_route_begin. */
+NEST_API nest_status_t nest_set_zero_copy(nest_ctx_t* ctx, int32_t on);
+
 /* Replace the library's internal streams with the caller's (NULL keeps
  * one): the occurrence sorts of nest_route_end and the tower's deferred dW
  * GEMMs -- e.g. streams of green contexts that split the SMs between the

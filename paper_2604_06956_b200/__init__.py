@@ -193,6 +193,11 @@ class NestContext:
         fn = self.lib.nest_tower_fwd_bwd_bf16 if str(pooled.dtype) == "torch.bfloat16" else self.lib.nest_tower_fwd_bwd
         self._check(fn(self.ctx, _ptr(pooled), int(pooled.shape[0]), _ptr(dout), _stream(stream)))
 
+    def set_zero_copy(self, on: bool) -> None:
+        """Zero-copy retrieval for W=1 / N=1 / HBM batches routed from now on
+        (nest_set_zero_copy)."""
+        self._check(self.lib.nest_set_zero_copy(self.ctx, 1 if on else 0))
+
     def set_streams(self, sort_stream=None, tower_dw_stream=None) -> None:
         """The library's internal streams -> the caller's (nest_set_streams)."""
         self._check(self.lib.nest_set_streams(self.ctx, sort_stream.cuda_stream if sort_stream is not None else None,

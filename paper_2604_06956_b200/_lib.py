@@ -28,7 +28,7 @@ SYMBOLS = ["nest_version", "nest_get_unique_id", "nest_workspace_bytes", "nest_s
            "nest_create", "nest_destroy", "nest_window_export", "nest_window_connect", "nest_check_guards", "nest_init_tables", "nest_fwp_schedule", "nest_route", "nest_route_begin", "nest_route_end",
            "nest_dbp_refresh", "nest_lookup_prefetch", "nest_lookup_fwd", "nest_lookup_fwd_bf16",
            "nest_grad_bwd_update", "nest_grad_bwd_update_adagrad", "nest_tower_fwd_bwd",
-           "nest_tower_fwd_bwd_bf16", "nest_tower_step", "nest_set_streams", "nest_join", "nest_read_state", "nest_tower_read",
+           "nest_tower_fwd_bwd_bf16", "nest_tower_step", "nest_set_streams", "nest_set_zero_copy", "nest_join", "nest_read_state", "nest_tower_read",
            "nest_slot_info", "nest_route_view", "nest_read_rows", "nest_exchange_plan", "nest_profile_enable",
            "nest_profile_read", "nest_profile_records", "nest_last_error"]
 PROFILE_STAGES = 16
@@ -142,6 +142,7 @@ def load() -> C.CDLL:
         "nest_tower_read": ([vp, i32, i32, vp, vp], i32),
         "nest_tower_step": ([vp, vp], i32),
         "nest_set_streams": ([vp, vp, vp], i32),
+        "nest_set_zero_copy": ([vp, i32], i32),
         "nest_join": ([vp, vp], i32),
         "nest_slot_info": ([vp, i32, C.POINTER(SlotInfo)], i32),
         "nest_route_view": ([vp, i32, C.POINTER(RouteView)], i32),

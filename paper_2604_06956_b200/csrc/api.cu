@@ -382,6 +382,7 @@ nest_status_t nest_create(const nest_config_t* cfg, const void* nccl_uids, void*
       }
     }
     if (const char* e = std::getenv("NEST_GATHER_SKIP")) c->gather_skip = std::atoi(e) != 0;
+    if (const char* e = std::getenv("NEST_ZERO_COPY")) c->zero_copy = std::atoi(e) != 0;
     if (c->cfg.optimizer == NEST_OPT_ROWWISE_ADAGRAD) {
       c->opt_state = c->shard + std::max<int64_t>(c->Vo, 1) * c->D;
       zero_f32(c->opt_state, std::max<int64_t>(c->Vo, 1), S(stream));
@@ -581,6 +582,7 @@ nest_status_t nest_route_begin(nest_ctx_t* ctx, int32_t slot, const int64_t* key
     (void)mb_offsets;  // micro-batches are equal: mb_offsets[i] = i * B / N
     cudaStream_t st = S(stream);
     s.routed = false;
+    s.zero_copy = c->zero_copy && c->W == 1 && N == 1 && c->cfg.table_location == NEST_TABLE_HBM;
     // the pipelined call order (route(t+1) inside window t, before update(t)
     // is issued): the gather will skip K(t) and the refresh supplies it
     {
@@ -683,7 +685,9 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
     cudaStream_t st = S(stream);
     NEST_CUDA(cudaStreamWaitEvent(st, a.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, p.ev_gather, 0));
-    if (p.early) {
+    if (p.zero_copy) {
+      // zero-copy batch: it reads the written-back shard itself, nothing to copy
+    } else if (p.early) {
       // the requesters' early copies of the intersection are stale too: the
       // refresh re-pushes exactly those rows (after the early push landed)
       NEST_CUDA(cudaStreamWaitEvent(st, p.ev_early, 0));
@@ -758,6 +762,14 @@ static nest_status_t lookup_fwd_impl(Ctx* c, int32_t slot, int32_t mb, void* out
       if (c->xfer_ce) xfer_wait_emb(*c, s, mb, cs);   // every owner's rows have landed
     } else if (mb == 0) {
       NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_gather, 0));
+      if (s.zero_copy) {
+        // the shard is read in place: after the other slot's update (DBP's
+        // staleness-freedom without a buffer, reading Q8)
+        Slot& o = c->slot[1 - slot];
+        NEST_CHECK(!o.routed || o.updated, NEST_ERR_ORDER,
+                   "zero-copy lookup before the previous window's update was issued");
+        if (o.routed) NEST_CUDA(cudaStreamWaitEvent(cs, o.ev_update, 0));
+      }
     }
     ProfScope ps(*c, ST_POOL, SK_COMPUTE, cs);
     launch_pool(*c, s, mb, out, bf16, cs);
@@ -942,6 +954,12 @@ nest_status_t nest_tower_read(nest_ctx_t* ctx, int32_t what, int32_t layer, floa
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return NEST_ERR_INVALID;
   return guard(c, [&] { tower_read(*c, what, layer, out, S(stream)); });
+}
+
+nest_status_t nest_set_zero_copy(nest_ctx_t* ctx, int32_t on) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return NEST_ERR_INVALID;
+  return guard(c, [&] { c->zero_copy = on != 0; });
 }
 
 nest_status_t nest_set_streams(nest_ctx_t* ctx, void* sort_stream, void* tower_dw_stream) {

@@ -123,6 +123,7 @@ struct Slot {
   // writes (K(t) cap K(t+1)); nest_dbp_refresh supplies them
   bool refresh_pending = false;
   bool skip_planned = false;       // nest_route_begin: the other slot's update was not yet issued
+  bool zero_copy = false;          // this batch reads / updates the shard in place (no buffer, no refresh)
   cudaEvent_t ev_early = nullptr, ev_repush = nullptr;
   cudaEvent_t ev_sorted = nullptr;  // occurrences sorted (the segment-sum's input)
   cudaEvent_t ev_gather = nullptr, ev_update = nullptr, ev_free = nullptr, ev_emb[NEST_MAX_MICRO_BATCHES] = {},
@@ -270,6 +271,9 @@ struct Ctx {
   // the prefetch gather skips the pending update's keys (default); 0: the r01
   // ordering, update(t) waits for gather(t+1) (NEST_GATHER_SKIP=0)
   bool gather_skip = true;
+  // NEST_ZERO_COPY=1 (W = 1, N = 1, HBM tables): no retrieval copy -- the pool
+  // and the fused update read the shard rows in place
+  bool zero_copy = false;
   int64_t src_slot_stride = 0;     // floats between the two slots' receive windows (0: shared)
   std::vector<void*> peer_win;
   std::vector<float*> peer_src, peer_own;
@@ -635,6 +639,10 @@ struct PeerRows {
   int32_t ada;
   float ada_gscale, ada_eps;
   float* ada_state;
+  // zero-copy retrieval (W = 1, HBM tables): the frozen row of key k is read
+  // from the shard itself (row sgd_rows[k], updated in place) instead of the
+  // slot buffer
+  int32_t sgd_inplace;
 };
 enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
 // the update's sparse optimizer step: Eq. 2 SGD (e = fma(-lr, G, e), lr =

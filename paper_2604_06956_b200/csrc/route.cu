@@ -993,6 +993,13 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     // this gather never waits for -- nor races -- that update; otherwise the
     // gather follows the other slot's update and reads its written-back rows
     Slot& o = c.slot[&s == &c.slot[0] ? 1 : 0];
+    if (s.zero_copy) {
+      // no retrieval copy: the window reads the shard in place after the
+      // other slot's update (stream order on the compute lane, checked by
+      // the lookup), so there is nothing stale to refresh either
+      s.refresh_pending = false;
+      return;
+    }
     const bool skip = s.skip_planned && o.routed;   // decided at nest_route_begin
     if (!skip && o.routed) NEST_CUDA(cudaStreamWaitEvent(st, o.ev_update, 0));
     s.refresh_pending = skip;

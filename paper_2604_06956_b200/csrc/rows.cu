@@ -445,9 +445,11 @@ static bool pool_by_bag() {
 void launch_pool(Ctx& c, Slot& s, int mb, void* out_v, bool bf16, cudaStream_t st) {
   float* out = reinterpret_cast<float*>(out_v);
   __nv_bfloat16* out_h = reinterpret_cast<__nv_bfloat16*>(out_v);
-  const bool w1 = c.W == 1;
-  const float* src = w1 ? s.buffer : src_rows_of(c, s) + s.src_base[mb] * c.D;
-  const int32_t* pos = s.pos + int64_t(mb) * (c.Kcap + 1);
+  // zero-copy (W = 1): the rows come straight from the shard, key u at shard
+  // row owner_rows[u] (the non-W1 kernels' indirection)
+  const bool w1 = c.W == 1 && !s.zero_copy;
+  const float* src = s.zero_copy ? c.shard : w1 ? s.buffer : src_rows_of(c, s) + s.src_base[mb] * c.D;
+  const int32_t* pos = s.zero_copy ? s.owner_rows : s.pos + int64_t(mb) * (c.Kcap + 1);
   const int32_t* perm_mb = s.perm + int64_t(mb) * s.cap;
   const int pf = (pf_mask() >> 1) & 1;
   NEST_DISPATCH_D(c.D, {
@@ -572,12 +574,13 @@ __device__ __forceinline__ float* map_row(const PeerRows& m, int64_t p, int D) {
 // shard[owner_rows[k]] = fma(-lr, g, frozen buffer row k)  (Eq. 2)
 __device__ __forceinline__ void put_grad(const PeerRows& m, int64_t k, int D, int col, float4 g) {
   if (m.sgd_shard) {
-    float4 e = ldg_f4(m.sgd_buffer + k * D + col);
+    const int64_t srow = __ldg(m.sgd_rows + k);
+    float4 e = ldg_f4((m.sgd_inplace ? m.sgd_shard + srow * D : m.sgd_buffer + k * D) + col);
     e.x = __fmaf_rn(-m.sgd_lr, g.x, e.x);
     e.y = __fmaf_rn(-m.sgd_lr, g.y, e.y);
     e.z = __fmaf_rn(-m.sgd_lr, g.z, e.z);
     e.w = __fmaf_rn(-m.sgd_lr, g.w, e.w);
-    st_f4_cs(m.sgd_shard + int64_t(__ldg(m.sgd_rows + k)) * D + col, e);
+    st_f4_cs(m.sgd_shard + srow * D + col, e);
   } else {
     st_f4(map_row(m, k, D) + col, g);
   }
@@ -617,7 +620,7 @@ __device__ __forceinline__ void put_row_adagrad(const PeerRows& m, int64_t k, bo
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int col = (v * L + l) * 4;
-    float4 e = ldg_f4(m.sgd_buffer + k * D + col);
+    float4 e = ldg_f4((m.sgd_inplace ? m.sgd_shard + srow * D : m.sgd_buffer + k * D) + col);
     e.x = __fmaf_rn(-step, acc[v].x, e.x);
     e.y = __fmaf_rn(-step, acc[v].y, e.y);
     e.z = __fmaf_rn(-step, acc[v].z, e.z);
@@ -861,7 +864,9 @@ __global__ void __launch_bounds__(kRowThreads, NEST_SEGSUM_RANGE_MINB) k_segsum_
         k_l = __ldg(pos + u_l);
         if (PRE) {
           s_l = __ldg(out.sgd_rows + k_l);
-          if (pf) prefetch_l2(out.sgd_buffer + int64_t(k_l) * D, D * sizeof(float));
+          if (pf)
+            prefetch_l2(out.sgd_inplace ? out.sgd_shard + int64_t(s_l) * D : out.sgd_buffer + int64_t(k_l) * D,
+                        D * sizeof(float));
         }
       }
       const uint32_t heads = __ballot_sync(gm, head) >> (lane_id() - gp.l);
@@ -880,11 +885,13 @@ __global__ void __launch_bounds__(kRowThreads, NEST_SEGSUM_RANGE_MINB) k_segsum_
             for (int v = 0; v < VPL; ++v)
               x[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_hint(dout + int64_t(r) * D + gp.col(v), pol_el)
                                            : ldg_f4(dout + int64_t(r) * D + gp.col(v));
-            if (PRE && ((heads >> t) & 1u))
+            if (PRE && ((heads >> t) & 1u)) {
+              const float* fr = out.sgd_inplace ? out.sgd_shard + int64_t(ss[k]) * D
+                                                : out.sgd_buffer + int64_t(kk[k]) * D;
 #pragma unroll
               for (int v = 0; v < VPL; ++v)
-                ex[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_hint(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v), pol_ef)
-                                              : ldg_f4(out.sgd_buffer + int64_t(kk[k]) * D + gp.col(v));
+                ex[k][v] = NEST_SEGSUM_L2HINT ? ldg_f4_hint(fr + gp.col(v), pol_ef) : ldg_f4(fr + gp.col(v));
+            }
           }
         }
 #pragma unroll
@@ -1070,6 +1077,7 @@ void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, c
   out.off[1] = int32_t(s.info.mb_uniq[0]);
   out.n = 1;
   out.sgd_buffer = s.buffer;
+  out.sgd_inplace = s.zero_copy ? 1 : 0;
   out.sgd_rows = s.owner_rows;
   out.sgd_shard = c.shard;
   out.sgd_lr = opt.lr;

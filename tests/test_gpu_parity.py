@@ -458,6 +458,45 @@ def test_edge_many_features_per_sample(d, N):
     _p1_check(cfg, batches, N=N)
 
 
+# --------------------------------------------------------------------------- zero-copy retrieval
+@pytest.mark.parametrize("N,d", [(1, 128), (1, 16), (2, 64)])
+def test_zero_copy_retrieval_p1_bit_exact(monkeypatch, N, d):
+    """NEST_ZERO_COPY=1 (W=1, N=1, HBM tables): no retrieval copy and no
+    refresh -- the pool and the fused update read the shard in place -- and the
+    pipelined steps still reach the synchronous result bit for bit (P1), hot
+    segments and empty bags included; with N > 1 the buffered path runs."""
+    monkeypatch.setenv("NEST_ZERO_COPY", "1")
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(4000, 50, 9, 2000), zipf=1.3, bag_len=(0, 6), bag_repeats=True,
+                                   dim=d)
+    batches = [WL.gen_batch(cfg, 60 + t, t, 0, batch=128) for t in range(5)]
+    _p1_check(cfg, batches, N=N)
+
+
+def test_zero_copy_adagrad_matches_oracle(monkeypatch):
+    """Zero-copy with the fused row-wise AdaGrad update (P2 tolerance)."""
+    monkeypatch.setenv("NEST_ZERO_COPY", "1")
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(3000, 700, 90, 20), zipf=1.2, bag_repeats=True, dim=32)
+    B, F, d, T = 64, cfg.num_features, cfg.dim, 4
+    batches = [WL.gen_batch(cfg, 70 + t, t, 0, batch=B) for t in range(T)]
+    douts = [WL.gen_dout(70, t, 0, B * F, d, "realistic") for t in range(T)]
+    gs, lr, eps = 1.0 / 64, 0.05, 1e-8
+    ctx = make_ctx(cfg, B, K=max(len(k) for k, _ in batches), init="uniform", seed=4,
+                   optimizer="rowwise_adagrad", adagrad_eps=eps)
+    run = Runner(ctx, N=1, pipelined=True, adagrad=(gs, lr))
+    db = [(to_dev(k, torch.int64), to_dev(o, torch.int32), B) for k, o in batches]
+    for t in range(T):
+        dd = to_dev(douts[t], torch.float32)
+        run.step(db[t], db[t + 1] if t + 1 < T else None, lambda tt, i, p, dd=dd: dd)
+    run.join()
+    torch.cuda.synchronize()
+    tab = OS.LazyTable(4, d, "uniform")
+    opt = OS.RowwiseAdagrad(lr=lr, grad_scale=gs, eps=eps)
+    for t in range(T):
+        OS.sync_step(tab, [batches[t]], [douts[t]], 0.0, optimizer=opt)
+    allk = np.unique(np.concatenate([k for k, _ in batches]))
+    assert rel_rowwise_ok(ctx.read_rows(to_dev(allk, torch.int64)).cpu().numpy(), tab.get(allk))
+
+
 # --------------------------------------------------------------------------- checked mode
 @pytest.mark.parametrize("N", [1, 2])
 def test_checked_mode_guard_bands(monkeypatch, N):
