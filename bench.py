@@ -611,15 +611,17 @@ def main():
                     res, tnext = tower_run(N2, tnext)
                     with_tower_runs[f"N{N2}"] = res
             embedding_only, tnext = embedding_run(N, tnext + 8)
-            if world == 1 and N == 1 and args.tables == "hbm" and cfg.pooling == "sum":
+            if N == 1 and args.tables == "hbm" and cfg.pooling == "sum" and \
+                    (world == 1 or os.environ.get("NEST_A2A", "fused") == "fused"):
                 # zero-copy retrieval: the same steps without the
                 # DBP retrieval copy and refresh -- the shard read in place
                 ctx.set_zero_copy(True)
                 zc_et, tnext = tower_run(1, tnext + 8)
                 zc_e, tnext = embedding_run(1, tnext + 8)
                 ctx.set_zero_copy(False)
-                zero_copy = {"note": "W=1 HBM tables: no retrieval copy (R4) / refresh (R5); pool and fused "
-                                     "update read the shard in place; same results (parity tests)",
+                zero_copy = {"note": "HBM tables: no retrieval copy (R4); W=1: no refresh (R5), pool and fused "
+                                     "update read the shard in place; W>1: owners push and update their shard "
+                                     "rows in place (re-push kept); same results (parity tests)",
                              "et": {k: zc_et[k] for k in ("ms_per_step", "samples_per_s", "roofline")},
                              "e": {k: zc_e[k] for k in ("ms_per_step", "samples_per_s", "roofline",
                                                         "whole_step_hbm")}}

@@ -582,7 +582,10 @@ nest_status_t nest_route_begin(nest_ctx_t* ctx, int32_t slot, const int64_t* key
     (void)mb_offsets;  // micro-batches are equal: mb_offsets[i] = i * B / N
     cudaStream_t st = S(stream);
     s.routed = false;
-    s.zero_copy = c->zero_copy && c->W == 1 && N == 1 && c->cfg.table_location == NEST_TABLE_HBM;
+    // zero-copy retrieval: HBM tables; at W > 1 only with the fused early push
+    // (the owner's rows then leave from the shard, refreshed by the re-push)
+    s.zero_copy = c->zero_copy && c->cfg.table_location == NEST_TABLE_HBM &&
+                  (c->W == 1 || (c->a2a_mode == A2A_FUSED && c->early_push == EP_SM));
     // the pipelined call order (route(t+1) inside window t, before update(t)
     // is issued): the gather will skip K(t) and the refresh supplies it
     {
@@ -685,7 +688,7 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
     cudaStream_t st = S(stream);
     NEST_CUDA(cudaStreamWaitEvent(st, a.ev_update, 0));
     NEST_CUDA(cudaStreamWaitEvent(st, p.ev_gather, 0));
-    if (p.zero_copy) {
+    if (p.zero_copy && c->W == 1) {
       // zero-copy batch: it reads the written-back shard itself, nothing to copy
     } else if (p.early) {
       // the requesters' early copies of the intersection are stale too: the

@@ -994,10 +994,12 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
     // gather follows the other slot's update and reads its written-back rows
     Slot& o = c.slot[&s == &c.slot[0] ? 1 : 0];
     if (s.zero_copy) {
-      // no retrieval copy: the window reads the shard in place after the
-      // other slot's update (stream order on the compute lane, checked by
-      // the lookup), so there is nothing stale to refresh either
-      s.refresh_pending = false;
+      // no retrieval copy: at W = 1 the window reads the shard in place after
+      // the other slot's update (stream order on the compute lane, checked by
+      // the lookup), so there is nothing stale to refresh; at W > 1 the
+      // owner's rows leave from the shard (early push) and the requesters'
+      // copies of the pending update's keys still need the re-push
+      s.refresh_pending = c.W > 1 && s.skip_planned && o.routed;
       return;
     }
     const bool skip = s.skip_planned && o.routed;   // decided at nest_route_begin

@@ -446,10 +446,12 @@ void launch_pool(Ctx& c, Slot& s, int mb, void* out_v, bool bf16, cudaStream_t s
   float* out = reinterpret_cast<float*>(out_v);
   __nv_bfloat16* out_h = reinterpret_cast<__nv_bfloat16*>(out_v);
   // zero-copy (W = 1): the rows come straight from the shard, key u at shard
-  // row owner_rows[u] (the non-W1 kernels' indirection)
-  const bool w1 = c.W == 1 && !s.zero_copy;
-  const float* src = s.zero_copy ? c.shard : w1 ? s.buffer : src_rows_of(c, s) + s.src_base[mb] * c.D;
-  const int32_t* pos = s.zero_copy ? s.owner_rows : s.pos + int64_t(mb) * (c.Kcap + 1);
+  // row owner_rows[u] (the non-W1 kernels' indirection); at W > 1 the rows
+  // are the received ones either way
+  const bool zc = s.zero_copy && c.W == 1;
+  const bool w1 = c.W == 1 && !zc;
+  const float* src = zc ? c.shard : w1 ? s.buffer : src_rows_of(c, s) + s.src_base[mb] * c.D;
+  const int32_t* pos = zc ? s.owner_rows : s.pos + int64_t(mb) * (c.Kcap + 1);
   const int32_t* perm_mb = s.perm + int64_t(mb) * s.cap;
   const int pf = (pf_mask() >> 1) & 1;
   NEST_DISPATCH_D(c.D, {
@@ -1094,12 +1096,15 @@ template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, const int64_t* __restrict__ recv,
                                                            const int32_t* __restrict__ owner_inv,
                                                            const int32_t* __restrict__ sendpos,
-                                                           const float* __restrict__ buffer, const PeerRows out) {
+                                                           const float* __restrict__ buffer,
+                                                           const int32_t* __restrict__ rowmap, const PeerRows out) {
   Grp<D> gp;
   for (int64_t r = gp.g; r < R; r += gp.ng) {
     if (!((uint64_t(__ldg(recv + r)) >> (56 + mb)) & 1u)) continue;
     float* dst = map_row(out, __ldg(sendpos + r), D);
-    const float* src = buffer + int64_t(__ldg(owner_inv + r)) * D;
+    // the owner's frozen row: its buffer row, or (zero-copy) its shard row
+    const int32_t k = __ldg(owner_inv + r);
+    const float* src = buffer + int64_t(rowmap ? __ldg(rowmap + k) : k) * D;
 #pragma unroll
     for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(dst + gp.col(v), ldg_f4(src + gp.col(v)));
   }
@@ -1128,8 +1133,9 @@ __global__ void __launch_bounds__(kRowThreads) k_refresh_push(
 #pragma unroll
     for (int q = 0; q < VPL; ++q) v[q] = ldg_f4(shard + int64_t(ld) * D + gp.col(q));
     if (mb == 0) {
+      if (buf_p)   // zero-copy: the owner has no buffer to refresh, only the requesters' copies
 #pragma unroll
-      for (int q = 0; q < VPL; ++q) st_f4(buf_p + u * D + gp.col(q), v[q]);
+        for (int q = 0; q < VPL; ++q) st_f4(buf_p + u * D + gp.col(q), v[q]);
       if (gp.l == 0) ++local;
     }
     for (int s = 0; s < W; ++s) {
@@ -1170,7 +1176,9 @@ void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
   const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
-    k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp, s.buffer, out);
+    k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
+                                                                s.zero_copy ? c.shard : s.buffer,
+                                                                s.zero_copy ? s.owner_rows : nullptr, out);
   });
   NEST_LAUNCH_CHECK();
 }
@@ -1183,7 +1191,8 @@ void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st) {
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
     k_refresh_push<D><<<blocks_for_rows(c.Uocap, rpb, 148 * 16), kRowThreads, 0, st>>>(
-        p.n_owner, p.owner_rows, a.obm, c.shard, p.buffer, p.src_tab, c.W, mb, p.recv, sp, out, c.n_refreshed);
+        p.n_owner, p.owner_rows, a.obm, c.shard, p.zero_copy ? nullptr : p.buffer, p.src_tab, c.W, mb, p.recv,
+        sp, out, c.n_refreshed);
   });
   NEST_LAUNCH_CHECK();
 }
@@ -1346,9 +1355,12 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
       step = opt.lr / (sqrtf(m) + opt.eps);
     }
     if (!act) continue;
+    // the frozen row: the slot buffer, or (zero-copy, buffer == nullptr) the
+    // shard row itself, read and written once by this lane group
+    const float* frozen = buffer ? buffer + u * D : shard + srow * D;
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
-      float4 e = ld_f4(buffer + u * D + gp.col(v));
+      float4 e = ld_f4(frozen + gp.col(v));
       e.x = __fmaf_rn(-step, acc[v].x, e.x);
       e.y = __fmaf_rn(-step, acc[v].y, e.y);
       e.z = __fmaf_rn(-step, acc[v].z, e.z);
@@ -1368,11 +1380,11 @@ void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& lr, cudaStream_t st) {
     if (w1)
       k_reduce_sgd<D, true><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, 1, lr, b, s.mask, s.pos, c.Kcap + 1, nullptr, nullptr, nullptr, 0,
-          src_rows_of(c, s), s.owner_rows, s.buffer, c.shard);
+          src_rows_of(c, s), s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard);
     else
       k_reduce_sgd<D, false><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, c.W, lr, b, nullptr, nullptr, 0, s.src_tab, s.recv, s.sendpos, c.Rcap + 1,
-          c.own_rows, s.owner_rows, s.buffer, c.shard);
+          c.own_rows, s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard);
   });
   NEST_LAUNCH_CHECK();
 }

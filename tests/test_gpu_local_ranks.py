@@ -28,7 +28,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TRANSPORTS = {"fused-early": {}, "ce": {"NEST_A2A": "ce"}, "fused-range": {"NEST_SEGSUM": "range"},
               "fused-window": {"NEST_EARLY_PUSH": "0"}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
               # checked mode: guard bands after every workspace buffer verified after each case
-              "fused-early-guard": {"NEST_GUARD": "1"}}
+              "fused-early-guard": {"NEST_GUARD": "1"},
+              # zero-copy retrieval: owners push / update their shard rows in place
+              "fused-early-zerocopy": {"NEST_ZERO_COPY": "1"}}
 
 
 def _port():
@@ -42,7 +44,8 @@ def _port():
 @pytest.mark.parametrize("world,transport,big", [(2, "fused-early", True), (4, "fused-early", False),
                                                  (8, "fused-early", False), (2, "ce", False),
                                                  (4, "fused-range", False), (2, "fused-window", False),
-                                                 (2, "fused-early-ce", False), (4, "fused-early-guard", False)])
+                                                 (2, "fused-early-ce", False), (4, "fused-early-guard", False),
+                                                 (2, "fused-early-zerocopy", True), (4, "fused-early-zerocopy", False)])
 def test_local_ranks_parity(world, transport, big):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
