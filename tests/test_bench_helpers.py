@@ -1,0 +1,51 @@
+"""Host-side bench.py arithmetic (no GPU): the roofline and whole-step HBM
+fractions are algorithmic bytes over event time against the peak, the CPU
+model string is read, and the tiny oracle baseline runs 10 steps."""
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def _stages(**kw):
+    names = ["schedule", "route", "sort", "key_a2a", "owner_dedup", "gather", "refresh", "send_gather",
+             "emb_a2a", "pool", "tower", "segsum", "grad_a2a", "update", "tower_dw", "emb_repush"]
+    st = {n: {"records": 0, "ms": 0.0, "bytes": 0.0, "units": 0.0, "launches": 0} for n in names}
+    for n, (ms, by) in kw.items():
+        st[n] = {"records": 10, "ms": ms, "bytes": by, "units": 0.0, "launches": 10}
+    return st
+
+
+def test_roofline_picks_the_longest_hbm_stage(monkeypatch):
+    monkeypatch.setattr(bench, "peaks", lambda: (6000.0, 1400.0, "measured"))
+    st = _stages(pool=(3.0, 12e9), segsum=(6.0, 24e9), tower=(20.0, 1e12))   # the tower is not an HBM stage
+    r = bench.roofline_from(st, "x/W1/N1")
+    assert r["kernel"] == "segsum"
+    assert r["achieved"] == pytest.approx(24e9 / (6.0 * 1e6))            # bytes / (ms * 1e6) = GB/s
+    assert r["frac"] == pytest.approx(r["achieved"] / 6000.0)
+    assert r["bytes_per_launch"] == pytest.approx(24e9 / 10)
+    assert r["ms_per_launch"] == pytest.approx(0.6)
+
+
+def test_whole_step_hbm_sums_every_hbm_stage(monkeypatch):
+    monkeypatch.setattr(bench, "peaks", lambda: (5000.0, 1400.0, "measured"))
+    st = _stages(route=(1.0, 1e9), sort=(1.0, 2e9), gather=(1.0, 3e9), pool=(1.0, 4e9), segsum=(1.0, 5e9),
+                 emb_a2a=(1.0, 9e9))                                        # NVLink bytes are not counted
+    w = bench.whole_step_hbm(st, steps=10, ms_step=2.0)
+    assert w["bytes_per_step"] == pytest.approx(15e9 / 10)
+    assert w["gbs"] == pytest.approx(1.5e9 / 2e6)
+    assert w["frac"] == pytest.approx(w["gbs"] / 5000.0)
+    assert "emb_a2a" not in w["stages"]
+
+
+def test_cpu_model_and_tiny_oracle_baseline():
+    assert isinstance(bench.cpu_model(), str) and bench.cpu_model()
+    t = bench.tiny_oracle_baseline(0, steps=2)
+    assert t["steps"] == 2 and t["value"] > 0 and "tiny" in t["sample"]
+    json.dumps(t)
