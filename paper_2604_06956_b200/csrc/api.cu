@@ -599,7 +599,10 @@ nest_status_t nest_route_begin(nest_ctx_t* ctx, int32_t slot, const int64_t* key
     NEST_CUDA(cudaStreamWaitEvent(st, c->ev_scratch, 0));
     c->route_pid = prof_begin(*c, ST_ROUTE, SK_AUX, st);
     route_phase_a(*c, s, keys, bag_offsets, nnz, B, perm, N, st);
-    prof_end(*c, c->route_pid, st, 0.0, nullptr, 0.0, c->cfg.pooling == NEST_POOL_SUM ? 11 : 15);   // phase A kernels (unpooled: + sample-base scan + k_unpooled_base)
+    // phase A kernels (unpooled: + sample-base scan + k_unpooled_base; the
+    // window count exchange: + k_push_counts; NCCL kernels are not counted)
+    prof_end(*c, c->route_pid, st, 0.0, nullptr, 0.0,
+             (c->cfg.pooling == NEST_POOL_SUM ? 11 : 15) + (c->W > 1 && c->route_window ? 1 : 0));
     c->route_open = slot;
     c->route_stream = st;
   });
