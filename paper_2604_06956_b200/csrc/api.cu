@@ -700,7 +700,7 @@ nest_status_t nest_dbp_refresh(nest_ctx_t* ctx, int32_t active_slot, int32_t pre
       {
         ProfScope ps(*c, ST_EMB_REPUSH, SK_COMPUTE, st);
         for (int mb = 0; mb < p.N; ++mb) launch_refresh_push(*c, a, p, mb, st);
-        ps.launches = p.N + 1;
+        ps.launches = p.N;   // one k_refresh_push per micro-batch
         // N4 (8 U_o' keys + 2 I rows) + the re-pushed rows (not counted: the
         // requester fan-out of I is known on the device only)
         ps.bytes = 8.0 * double(std::min(p.info.recv, c->Uocap));
