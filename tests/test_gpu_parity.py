@@ -458,6 +458,23 @@ def test_edge_many_features_per_sample(d, N):
     _p1_check(cfg, batches, N=N)
 
 
+# --------------------------------------------------------------------------- DBP stress
+@pytest.mark.parametrize("p_reuse,zero_copy", [(0.7, "0"), (0.3, "0"), (0.7, "1")])
+def test_dbp_stress_high_overlap_p1(monkeypatch, p_reuse, zero_copy):
+    """BASELINE configs[3] structure at test size: one table feeding all 26
+    features, batch t+1 reusing batch t's keys with probability p (the
+    intersection I/U_o the refresh copies grows with p), 5 pipelined steps:
+    pooled rows and final rows bit-exact (P1), the measured intersection
+    matching the oracle's |K(t) cap K(t+1)|."""
+    monkeypatch.setenv("NEST_ZERO_COPY", zero_copy)
+    cfg = WL.CONFIGS["dbp_stress"].with_(table_rows=(200_000,), dim=32, batch_local=256)
+    batches = WL.gen_overlap_batches(cfg, 11, 5, 0, p_reuse)
+    inter = [len(np.intersect1d(batches[t][0], batches[t + 1][0])) / len(np.unique(batches[t + 1][0]))
+             for t in range(4)]
+    assert min(inter) > (0.6 if p_reuse > 0.5 else 0.3)
+    _p1_check(cfg, batches, N=1, lr=2.0 ** -12)
+
+
 # --------------------------------------------------------------------------- zero-copy retrieval
 @pytest.mark.parametrize("N,d", [(1, 128), (1, 16), (2, 64)])
 def test_zero_copy_retrieval_p1_bit_exact(monkeypatch, N, d):
