@@ -47,11 +47,15 @@ def _port():
                                                  (2, "fused-early-ce", False), (4, "fused-early-guard", False),
                                                  (2, "fused-early-zerocopy", True), (4, "fused-early-zerocopy", False)])
 def test_local_ranks_parity(world, transport, big):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    def cmd():
+        return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                os.path.join(ROOT, "tests", "mgpu_worker.py")]
     env = dict(os.environ, NEST_MGPU_SAME_DEVICE="1", NEST_MGPU_BIG="1" if big else "0",
                **TRANSPORTS[transport])
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    for _ in range(3):   # a free port can be taken between probing and torchrun binding it
+        r = subprocess.run(cmd(), cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+        if "EADDRINUSE" not in r.stderr:
+            break
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "MGPU ALL OK" in r.stdout

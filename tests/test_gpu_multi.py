@@ -42,10 +42,14 @@ TRANSPORTS = {"fused-early": {}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
 def test_multi_rank_parity(world, transport):
     if _ndev() < world:
         pytest.skip(f"needs >= {world} CUDA devices")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    def cmd():
+        return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                os.path.join(ROOT, "tests", "mgpu_worker.py")]
     env = dict(os.environ, **TRANSPORTS[transport])
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    for _ in range(3):   # a free port can be taken between probing and torchrun binding it
+        r = subprocess.run(cmd(), cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+        if "EADDRINUSE" not in r.stderr:
+            break
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "MGPU ALL OK" in r.stdout
