@@ -77,6 +77,9 @@ def cases(big=True):
         Case("adagrad-P2-N2", WL.CONFIGS["tiny"].with_(table_rows=(3000, 700, 90, 20), zipf=1.2,
                                                        bag_repeats=True, dim=32),
              128, 2, 4, "uniform", "realistic", 0.0, adagrad=(1.0 / 256, 0.05, 1e-8)),
+        # soak: many pipelined steps (slot reuse, epoch flags, window reuse)
+        Case("soak-P1-N2-40steps", WL.CONFIGS["tiny"].with_(table_rows=(500, 300, 200, 100), bag_repeats=True),
+             64, 2, 40, "dyadic", "dyadic", 2.0 ** -12),
         # host-DRAM tier (NEXT-3): every owner's shard in pinned host memory
         Case("host-tier-P1-N2", WL.CONFIGS["tiny"].with_(table_rows=(3000, 40, 7, 999), zipf=1.3,
                                                          bag_repeats=True, dim=128),

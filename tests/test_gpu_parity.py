@@ -458,6 +458,18 @@ def test_edge_many_features_per_sample(d, N):
     _p1_check(cfg, batches, N=N)
 
 
+# --------------------------------------------------------------------------- soak
+@pytest.mark.parametrize("N", [1, 2])
+def test_long_run_soak_p1(N):
+    """120 pipelined steps over 3 cycled batches of a small hot table (every
+    key updated many times, slots and events reused 60 times each): pooled
+    rows of every step and the final table bit-exact against the oracle (P1)."""
+    cfg = WL.CONFIGS["tiny"].with_(table_rows=(400, 300, 200, 100), zipf=1.2, bag_repeats=True, dim=32)
+    base = [WL.gen_batch(cfg, 90 + t, t, 0, batch=64) for t in range(3)]
+    batches = [base[t % 3] for t in range(120)]
+    _p1_check(cfg, batches, N=N, lr=2.0 ** -14)
+
+
 # --------------------------------------------------------------------------- DBP stress
 @pytest.mark.parametrize("p_reuse,zero_copy", [(0.7, "0"), (0.3, "0"), (0.7, "1")])
 def test_dbp_stress_high_overlap_p1(monkeypatch, p_reuse, zero_copy):
