@@ -92,17 +92,24 @@ def peaks():
     return 6650.0, 1400.0, "fallback"
 
 
-HBM_STAGES = ["route", "sort", "owner_dedup", "gather", "refresh", "send_gather", "pool", "segsum", "update"]
+HBM_STAGES = ["route", "sort", "owner_dedup", "gather", "refresh", "send_gather", "pool", "segsum", "update",
+              "emb_repush"]
+# fused transport stages (W > 1, or W = 1 with micro-batches): their `bytes` are
+# off-GPU bytes; their local-HBM bytes (rows gathered / the segment-sum's reads
+# + rows stored locally) come in `hbm_bytes`
+XFER_STAGES = ["key_a2a", "emb_a2a", "grad_a2a"]
 
 
 def whole_step_hbm(st, steps, ms_step):
     """Algorithmic HBM bytes of every stage of the step (SURVEY §8(d) per-kernel
     formulas, summed) over the step time, against the measured copy peak."""
     hbm_peak, _, src = peaks()
-    b = sum(st[n]["bytes"] for n in HBM_STAGES if n in st and st[n]["records"]) / steps
+    used = [n for n in HBM_STAGES + XFER_STAGES if n in st and st[n]["records"]
+            and (n in HBM_STAGES or st[n].get("hbm_bytes", 0.0) > 0)]
+    b = sum(st[n]["bytes"] if n in HBM_STAGES else st[n]["hbm_bytes"] for n in used) / steps
     gbs = b / (ms_step * 1e6)
     return {"bytes_per_step": b, "gbs": gbs, "peak": hbm_peak, "frac": gbs / hbm_peak, "peak_source": src,
-            "stages": [n for n in HBM_STAGES if n in st and st[n]["records"]]}
+            "stages": used}
 
 
 def roofline_from(st, key_prefix):

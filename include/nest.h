@@ -455,6 +455,10 @@ typedef struct {
                            off-GPU bytes for the All2All stages */
   double units;         /* summed device-side counts: refreshed rows I (refresh),
                            owner-unique keys U_o (gather, update, owner_dedup) */
+  double hbm_bytes;     /* local-HBM algorithmic bytes of the fused transport stages
+                           (emb_a2a: rows gathered + rows stored locally; grad_a2a:
+                           the segment-sum's reads + rows stored locally); equal to
+                           `bytes` for the HBM stages, 0 for tower / tower_dw */
 } nest_profile_stage_t;
 
 typedef struct {

@@ -256,7 +256,7 @@ class NestContext:
         for s in stages:
             out["stages"][s.name.decode()] = {"stream": s.stream, "records": s.records,
                                               "launches": s.launches, "ms": s.ms, "bytes": s.bytes,
-                                              "units": s.units}
+                                              "units": s.units, "hbm_bytes": s.hbm_bytes}
         return out
 
     def profile_records(self) -> list:

@@ -82,7 +82,7 @@ class ExchangePlan(C.Structure):
 class ProfileStage(C.Structure):
     _fields_ = [("name", C.c_char * 24), ("stream", C.c_int32), ("records", C.c_int32),
                 ("launches", C.c_int32), ("pad", C.c_int32), ("ms", C.c_double), ("bytes", C.c_double),
-                ("units", C.c_double)]
+                ("units", C.c_double), ("hbm_bytes", C.c_double)]
 
 
 class ProfileRecord(C.Structure):

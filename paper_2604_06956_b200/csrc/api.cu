@@ -282,6 +282,7 @@ static void lookup_comm(Ctx& c, Slot& s, int mb, cudaStream_t cs, cudaStream_t m
       launch_send_push(c, s, mb, ms);
       int64_t self = s.all[(size_t(c.rank) * c.W + c.rank) * (c.Nmax + 2) + 1 + mb];
       ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+      ps.hbm = row * double(s.info.mb_recv[mb] + self);    // rows gathered + rows stored locally
     }
     NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
     xfer_signal(c, s, 0, mb, ms);
@@ -652,10 +653,12 @@ nest_status_t nest_route_end(nest_ctx_t* ctx, int32_t slot) {
           xfer_push_emb(*c, s, mb, st, s.ev_emb[mb], c->send_stage);   // signals XK_EMB
           ps.launches = 0;
           ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+          ps.hbm = row * double(s.info.mb_recv[mb] + self);    // staged rows read + self rows stored
         } else {
           ProfScope ps(*c, ST_EMB_A2A, SK_AUX, st);
           launch_send_push(*c, s, mb, st);
           ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+          ps.hbm = row * double(s.info.mb_recv[mb] + self);    // rows gathered + rows stored locally
           xfer_signal(*c, s, XK_EMB, mb, st);
         }
       }
@@ -863,6 +866,8 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
         // accounted as the gradient All2All: rows stored off-GPU
         const int64_t self = s.all[(size_t(c->rank) * c->W + c->rank) * (c->Nmax + 2) + 1 + mb];
         ps.bytes = row * double(s.info.mb_uniq[mb] - self);
+        // local HBM: the segment-sum's reads (N7: gradient rows + 4 K_i) + rows stored locally
+        ps.hbm = row * double(s.info.mb_out_rows[mb]) + 4.0 * double(s.info.mb_nnz[mb]) + row * double(self);
       } else {
         // gradient rows read + 4 K_i + U_{s,i} rows written
         ps.bytes = row * double(s.info.mb_out_rows[mb]) + 4.0 * double(s.info.mb_nnz[mb]) +
@@ -891,6 +896,7 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
           a2a_rows(*c, c->src_rows + s.src_base[mb] * c->D, scnt, c->own_rows + s.own_base[mb] * c->D, rcnt, ms);
         ps.launches = 0;
         ps.bytes = row * double(s.info.mb_uniq[mb] - scnt[c->rank]);  // rows sent off-GPU
+        ps.hbm = row * double(s.info.mb_uniq[mb] + scnt[c->rank]);    // rows read + self rows stored
       }
       if (mb == s.N - 1) {
         if (c->xfer_ce) xfer_wait_grads(*c, s, ms);  // every requester's gradients have landed

@@ -145,6 +145,7 @@ struct ProfRec {
   int stage, kind;
   cudaEvent_t e0, e1;
   double bytes;          // fixed part of the algorithmic bytes
+  double hbm = -1;       // local-HBM bytes of a transport stage (< 0: same as bytes)
   int cidx;              // index into the pinned device-count ring (-1: none)
   double bytes_per_cnt;  // bytes per unit of that device count
   int launches;
@@ -607,6 +608,7 @@ int prof_begin(Ctx& c, int stage, int kind, cudaStream_t st);
 void prof_end(Ctx& c, int id, cudaStream_t st, double bytes, const int32_t* dcount = nullptr,
               double bytes_per_cnt = 0.0, int launches = 1) noexcept;
 void prof_add_bytes(Ctx& c, int id, double bytes) noexcept;
+void prof_set_hbm(Ctx& c, int id, double hbm) noexcept;
 void profile_enable(Ctx& c, bool on);
 void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* sum);
 void profile_destroy(Ctx& c);
@@ -618,10 +620,14 @@ struct ProfScope {
   int id;
   cudaStream_t st;
   double bytes = 0, bpc = 0;
+  double hbm = -1;   // transport stages: local-HBM bytes (bytes = off-GPU bytes)
   const int32_t* dcount = nullptr;
   int launches = 1;
   ProfScope(Ctx& cc, int stage, int kind, cudaStream_t s) : c(cc), id(prof_begin(cc, stage, kind, s)), st(s) {}
-  ~ProfScope() { prof_end(c, id, st, bytes, dcount, bpc, launches); }
+  ~ProfScope() {
+    prof_end(c, id, st, bytes, dcount, bpc, launches);
+    prof_set_hbm(c, id, hbm);
+  }
 };
 // output maps of the fused gather->NVLink-put kernels (rows.cu): position p of
 // a micro-batch's (owner- or source-major) row list goes to row

@@ -59,6 +59,10 @@ void prof_add_bytes(Ctx& c, int id, double bytes) noexcept {
   if (id >= 0 && id < int(c.prof.recs.size())) c.prof.recs[id].bytes += bytes;
 }
 
+void prof_set_hbm(Ctx& c, int id, double hbm) noexcept {
+  if (id >= 0 && id < int(c.prof.recs.size()) && hbm >= 0) c.prof.recs[id].hbm = hbm;
+}
+
 void profile_enable(Ctx& c, bool on) {
   Profiler& p = c.prof;
   if (on) {
@@ -129,6 +133,13 @@ void profile_read(Ctx& c, nest_profile_stage_t* stages, nest_profile_summary_t* 
       g.units += double(p.hcnt[r.cidx]);
     }
     g.bytes += bytes;
+    if (r.stage == ST_TOWER || r.stage == ST_TOWER_DW) {
+      // FLOPs, not bytes
+    } else if (r.stage == ST_EMB_A2A || r.stage == ST_GRAD_A2A || r.stage == ST_KEY_A2A) {
+      g.hbm_bytes += r.hbm >= 0 ? r.hbm : 0.0;   // transport stages: `bytes` are off-GPU bytes
+    } else {
+      g.hbm_bytes += bytes;
+    }
     t_min = std::min(t_min, double(t0));
     t_max = std::max(t_max, double(t1));
     if (r.stage == ST_EMB_A2A || r.stage == ST_GRAD_A2A || r.stage == ST_EMB_REPUSH) {

@@ -16,9 +16,11 @@ import bench  # noqa: E402
 def _stages(**kw):
     names = ["schedule", "route", "sort", "key_a2a", "owner_dedup", "gather", "refresh", "send_gather",
              "emb_a2a", "pool", "tower", "segsum", "grad_a2a", "update", "tower_dw", "emb_repush"]
-    st = {n: {"records": 0, "ms": 0.0, "bytes": 0.0, "units": 0.0, "launches": 0} for n in names}
-    for n, (ms, by) in kw.items():
-        st[n] = {"records": 10, "ms": ms, "bytes": by, "units": 0.0, "launches": 10}
+    st = {n: {"records": 0, "ms": 0.0, "bytes": 0.0, "units": 0.0, "launches": 0, "hbm_bytes": 0.0} for n in names}
+    for n, v in kw.items():
+        ms, by = v[:2]
+        st[n] = {"records": 10, "ms": ms, "bytes": by, "units": 0.0, "launches": 10,
+                 "hbm_bytes": v[2] if len(v) > 2 else by}
     return st
 
 
@@ -36,12 +38,24 @@ def test_roofline_picks_the_longest_hbm_stage(monkeypatch):
 def test_whole_step_hbm_sums_every_hbm_stage(monkeypatch):
     monkeypatch.setattr(bench, "peaks", lambda: (5000.0, 1400.0, "measured"))
     st = _stages(route=(1.0, 1e9), sort=(1.0, 2e9), gather=(1.0, 3e9), pool=(1.0, 4e9), segsum=(1.0, 5e9),
-                 emb_a2a=(1.0, 9e9))                                        # NVLink bytes are not counted
+                 emb_a2a=(1.0, 9e9, 0.0))                                   # NVLink bytes are not counted
     w = bench.whole_step_hbm(st, steps=10, ms_step=2.0)
     assert w["bytes_per_step"] == pytest.approx(15e9 / 10)
     assert w["gbs"] == pytest.approx(1.5e9 / 2e6)
     assert w["frac"] == pytest.approx(w["gbs"] / 5000.0)
     assert "emb_a2a" not in w["stages"]
+
+
+def test_whole_step_hbm_counts_the_local_side_of_fused_transports(monkeypatch):
+    # W > 1: the fused segment-sum -> peer-store stage (grad_a2a) and the send
+    # push (emb_a2a) move NVLink bytes (`bytes`) and local HBM bytes
+    # (`hbm_bytes`); only the latter count towards the HBM fraction
+    monkeypatch.setattr(bench, "peaks", lambda: (5000.0, 1400.0, "measured"))
+    st = _stages(pool=(1.0, 4e9), update=(1.0, 2e9), grad_a2a=(1.0, 7e9, 3e9), emb_a2a=(1.0, 9e9, 1e9),
+                 key_a2a=(1.0, 5e8, 0.0))
+    w = bench.whole_step_hbm(st, steps=10, ms_step=2.0)
+    assert w["bytes_per_step"] == pytest.approx((4e9 + 2e9 + 3e9 + 1e9) / 10)
+    assert set(w["stages"]) == {"pool", "update", "grad_a2a", "emb_a2a"}
 
 
 def test_cpu_model_and_tiny_oracle_baseline():
