@@ -215,6 +215,15 @@ typedef struct {
   uint8_t ipc[64];               /* cudaIpcMemHandle_t (other processes) */
   uint64_t bytes, off_own, off_cnt, off_key, off_twr, off_flags;
   uint64_t src_stride, cnt_stride, key_stride;
+  /* direct write-back (W > 1, fused transport, SGD, HBM tables): the owner
+   * marks every row it pushes with the row's shard index when the requester is
+   * the key's only contributor (one source, one micro-batch), and that
+   * requester applies Eq. 2 to its received copy and stores the updated row
+   * straight into the owner's shard -- so the shard is mapped too */
+  uint64_t off_dwb, dwb_stride;  /* int32 marks, per slot, indexed like the receive rows */
+  uint64_t shard_ptr, shard_off; /* shard device address; its offset in the IPC-mapped allocation */
+  uint8_t shard_ipc[64];         /* cudaIpcMemHandle_t of the allocation holding the shard */
+  int32_t dwb_ok, dwb_pad;       /* 1: this rank can take part (the feature runs iff every rank can) */
 } nest_window_rec_t;
 
 /* This rank's window record (context created with nccl_uids == NULL and

@@ -100,7 +100,10 @@ class WindowRec(C.Structure):
                 ("device", C.c_int32), ("ptr", C.c_uint64), ("ipc", C.c_uint8 * 64),
                 ("bytes", C.c_uint64), ("off_own", C.c_uint64), ("off_cnt", C.c_uint64),
                 ("off_key", C.c_uint64), ("off_twr", C.c_uint64), ("off_flags", C.c_uint64),
-                ("src_stride", C.c_uint64), ("cnt_stride", C.c_uint64), ("key_stride", C.c_uint64)]
+                ("src_stride", C.c_uint64), ("cnt_stride", C.c_uint64), ("key_stride", C.c_uint64),
+                ("off_dwb", C.c_uint64), ("dwb_stride", C.c_uint64), ("shard_ptr", C.c_uint64),
+                ("shard_off", C.c_uint64), ("shard_ipc", C.c_uint8 * 64), ("dwb_ok", C.c_int32),
+                ("dwb_pad", C.c_int32)]
 
 
 _lib = None

@@ -856,6 +856,13 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
         out.off[W] = int32_t(acc);
         out.n = W;
         out.fence = 1;
+        if (dwb_active(*c, s, opt)) {
+          // direct write-back: the owners marked the sole-contributor rows
+          out.dwb_rows = dwb_of(*c, s) + s.src_base[mb];
+          out.sgd_buffer = src_rows_of(*c, s) + s.src_base[mb] * c->D;
+          out.sgd_lr = opt.lr;
+          for (int o = 0; o < W; ++o) out.dwb_shard[o] = c->peer_shard[o];
+        }
         launch_segsum_to(*c, s, mb, dout, out, cs);
         xfer_signal(*c, s, 1, mb, cs);
       } else {
@@ -874,11 +881,10 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
                    row * double(s.info.mb_uniq[mb]);
       }
     }
-    // sum_i R_{o,i} gradient rows + U_o buffer rows read + U_o rows
-    // written back (the survey's third U_o row, the buffer rewrite, is not needed:
-    // the refresh copies written-back rows)
-    double upd_fixed = 0;
-    for (int i = 0; i < s.N; ++i) upd_fixed += row * double(c->W > 1 ? s.info.mb_recv[i] : s.info.mb_uniq[i]);
+    // SURVEY §8(d) N8 (the update below): sum_i R_{o,i} gradient rows + U_o
+    // buffer rows read + U_o rows written back (the survey's third U_o row, the
+    // buffer rewrite, is not needed: the refresh copies written-back rows,
+    // DESIGN.md §7) -- counted on the device as moved
     if (c->W > 1) {
       NEST_CUDA(cudaEventRecord(s.ev_grad[mb], cs));
       NEST_CUDA(cudaStreamWaitEvent(ms, s.ev_grad[mb], 0));
@@ -904,9 +910,12 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
         {
           ProfScope ps(*c, ST_UPDATE, SK_COMM, ms);
           launch_reduce_sgd(*c, s, opt, ms);
-          ps.bytes = upd_fixed;
-          ps.dcount = s.n_owner;
-          ps.bpc = 2.0 * row + (opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 : 0.0);  // + accumulator r/w
+          // N8 as moved: contributions read + frozen row read + row written
+          // (counted on the device; under direct write-back the sole
+          // contributors' keys are not touched here), + AdaGrad's accumulator
+          ps.bytes = opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 * double(std::min(s.info.recv, c->Uocap)) : 0.0;
+          ps.dcount = c->n_refreshed + 3;
+          ps.bpc = row;
         }
         NEST_CUDA(cudaEventRecord(s.ev_update, ms));
         NEST_CUDA(cudaStreamWaitEvent(cs, s.ev_update, 0));
@@ -916,9 +925,9 @@ static nest_status_t grad_impl(Ctx* c, int32_t slot, int32_t mb, const float* do
       {
         ProfScope ps(*c, ST_UPDATE, SK_COMPUTE, cs);
         launch_reduce_sgd(*c, s, opt, cs);
-        ps.bytes = upd_fixed;
-        ps.dcount = s.n_owner;
-        ps.bpc = 2.0 * row + (opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 : 0.0);  // + accumulator r/w
+        ps.bytes = opt.kind == NEST_OPT_ROWWISE_ADAGRAD ? 8.0 * double(std::min(s.info.recv, c->Uocap)) : 0.0;
+        ps.dcount = c->n_refreshed + 3;   // rows moved (N8), counted on the device
+        ps.bpc = row;
       }
       NEST_CUDA(cudaEventRecord(s.ev_update, cs));
     }

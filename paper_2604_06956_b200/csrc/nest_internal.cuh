@@ -276,6 +276,16 @@ struct Ctx {
   // and the fused update read the shard rows in place
   bool zero_copy = false;
   int64_t src_slot_stride = 0;     // floats between the two slots' receive windows (0: shared)
+  // direct write-back of sole-contributor keys (W > 1): marks
+  // region of the window (int32 per receive row, per slot), every peer's marks
+  // and shard; dwb = on for this world (every rank able, NEST_DIRECT_WB != 0)
+  bool dwb_wanted = false, dwb = false;
+  size_t xoff_dwb = 0;
+  int64_t dwb_slot_stride = 0;     // int32s between the two slots' mark areas (0: shared)
+  int32_t* dwb_marks = nullptr;
+  std::vector<int32_t*> peer_dwb_slot[2];
+  std::vector<float*> peer_shard;
+  std::vector<void*> peer_shard_map;   // IPC mappings of peers' shard allocations (closed at destroy)
   std::vector<void*> peer_win;
   std::vector<float*> peer_src, peer_own;
   std::vector<float*> peer_src_slot[2];  // each peer's receive rows of slot 0 / 1
@@ -293,6 +303,9 @@ inline float* src_rows_of(const Ctx& c, const Slot& s) {
   return c.src_rows + slot_index(c, s) * c.src_slot_stride;
 }
 inline float* peer_src_of(const Ctx& c, const Slot& s, int p) { return c.peer_src_slot[slot_index(c, s)][p]; }
+// direct write-back marks of a slot (this rank / peer p's window)
+inline int32_t* dwb_of(const Ctx& c, const Slot& s) { return c.dwb_marks + slot_index(c, s) * c.dwb_slot_stride; }
+inline int32_t* peer_dwb_of(const Ctx& c, const Slot& s, int p) { return c.peer_dwb_slot[slot_index(c, s)][p]; }
 
 // GPU clustering (cluster.cu): histogram bins of the radix select, ids per
 // block of the ordered passes
@@ -652,6 +665,15 @@ struct PeerRows {
   // from the shard itself (row sgd_rows[k], updated in place) instead of the
   // slot buffer
   int32_t sgd_inplace;
+  // direct write-back (W > 1, SGD): dwb_rows[k] >= 0 marks a key whose only
+  // contribution is this row -- it is applied to the received frozen copy
+  // (sgd_buffer + k*D, lr sgd_lr) and stored at row dwb_rows[k] of the owner's
+  // shard (dwb_shard[segment of k]) instead of sent as a gradient row.
+  // Owner side (k_send_push): dwb_dst[p] = requester p's mark area, indexed
+  // like base[p]
+  const int32_t* dwb_rows;
+  float* dwb_shard[NEST_MAX_WORLD];
+  int32_t* dwb_dst[NEST_MAX_WORLD];
 };
 enum A2AMode : int { A2A_NCCL = 0, A2A_CE = 1, A2A_FUSED = 2 };
 // the update's sparse optimizer step: Eq. 2 SGD (e = fma(-lr, G, e), lr =
@@ -665,6 +687,7 @@ struct OptStep {
   float* state;
 };
 void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& opt, cudaStream_t st);
+bool dwb_active(const Ctx& c, const Slot& s, const OptStep& opt);
 void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, cudaStream_t st);
 void launch_read_state(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 enum EarlyPush : int { EP_OFF = 0, EP_CE = 1, EP_SM = 2 };

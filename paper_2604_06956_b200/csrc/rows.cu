@@ -565,11 +565,28 @@ __device__ __forceinline__ void sum_rows(const int32_t* __restrict__ sval, int64
   }
 }
 
-// destination row of position p under a PeerRows map (local or a peer's window)
-__device__ __forceinline__ float* map_row(const PeerRows& m, int64_t p, int D) {
+// segment of position p under a PeerRows map, and its destination row
+__device__ __forceinline__ int map_seg(const PeerRows& m, int64_t p) {
   int s = 0;
   while (s + 1 < m.n && m.off[s + 1] <= p) ++s;
+  return s;
+}
+__device__ __forceinline__ float* map_row(const PeerRows& m, int64_t p, int D) {
+  const int s = map_seg(m, p);
   return m.base[s] + (p - m.off[s]) * D;
+}
+
+// owner side of the direct write-back: owner-unique key u is marked iff one
+// requester asked for it, in one micro-batch (its gradient is then that
+// requester's segment-sum row alone)
+__device__ __forceinline__ bool sole_contributor(const int32_t* __restrict__ src_tab, int64_t u, int W,
+                                                 const int64_t* __restrict__ recv) {
+  int n = 0, r1 = -1;
+  for (int s = 0; s < W; ++s) {
+    const int32_t r = __ldg(src_tab + u * W + s);
+    if (r >= 0) { ++n; r1 = r; }
+  }
+  return n == 1 && __popc(uint32_t(uint64_t(__ldg(recv + r1)) >> 56)) == 1;
 }
 
 // store gradient row k (one float4 per call) or, in fused-SGD mode, apply it:
@@ -583,6 +600,22 @@ __device__ __forceinline__ void put_grad(const PeerRows& m, int64_t k, int D, in
     e.z = __fmaf_rn(-m.sgd_lr, g.z, e.z);
     e.w = __fmaf_rn(-m.sgd_lr, g.w, e.w);
     st_f4_cs(m.sgd_shard + srow * D + col, e);
+  } else if (m.dwb_rows) {
+    // W > 1: a sole-contributor key is applied here (Eq. 2 on the received
+    // frozen copy) and written back into its owner's shard; any other key's
+    // gradient row goes to its owner's receive rows
+    const int32_t srow = __ldg(m.dwb_rows + k);
+    const int s = map_seg(m, k);
+    if (srow >= 0) {
+      float4 e = ldg_f4(m.sgd_buffer + k * D + col);
+      e.x = __fmaf_rn(-m.sgd_lr, g.x, e.x);
+      e.y = __fmaf_rn(-m.sgd_lr, g.y, e.y);
+      e.z = __fmaf_rn(-m.sgd_lr, g.z, e.z);
+      e.w = __fmaf_rn(-m.sgd_lr, g.w, e.w);
+      st_f4(m.dwb_shard[s] + int64_t(srow) * D + col, e);
+    } else {
+      st_f4(m.base[s] + (k - m.off[s]) * D + col, g);
+    }
   } else {
     st_f4(map_row(m, k, D) + col, g);
   }
@@ -1092,19 +1125,29 @@ void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, c
 
 // R6 + R7 fused: the owner's gather writes every requested row straight into
 // the requester's receive rows (peer memory over NVLink; own rows locally)
+// (direct write-back: src_tab != nullptr -- each row's mark, its shard row
+// if the requester is the key's sole contributor else -1, is stored into the
+// requester's mark area at the row's index)
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, const int64_t* __restrict__ recv,
                                                            const int32_t* __restrict__ owner_inv,
                                                            const int32_t* __restrict__ sendpos,
                                                            const float* __restrict__ buffer,
-                                                           const int32_t* __restrict__ rowmap, const PeerRows out) {
+                                                           const int32_t* __restrict__ rowmap,
+                                                           const int32_t* __restrict__ src_tab, int W,
+                                                           const int32_t* __restrict__ owner_rows,
+                                                           const PeerRows out) {
   Grp<D> gp;
   for (int64_t r = gp.g; r < R; r += gp.ng) {
     if (!((uint64_t(__ldg(recv + r)) >> (56 + mb)) & 1u)) continue;
-    float* dst = map_row(out, __ldg(sendpos + r), D);
+    const int32_t p = __ldg(sendpos + r);
+    const int s = map_seg(out, p);
+    float* dst = out.base[s] + (p - out.off[s]) * D;
     // the owner's frozen row: its buffer row, or (zero-copy) its shard row
     const int32_t k = __ldg(owner_inv + r);
     const float* src = buffer + int64_t(rowmap ? __ldg(rowmap + k) : k) * D;
+    if (src_tab && gp.l == 0)
+      out.dwb_dst[s][p - out.off[s]] = sole_contributor(src_tab, k, W, recv) ? __ldg(owner_rows + k) : -1;
 #pragma unroll
     for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(dst + gp.col(v), ldg_f4(src + gp.col(v)));
   }
@@ -1166,6 +1209,12 @@ static PeerRows send_map(Ctx& c, Slot& s, int mb) {
   out.off[W] = int32_t(acc);
   out.n = W;
   out.fence = 1;
+  if (c.dwb && !s.zero_copy)
+    for (int p = 0; p < W; ++p) {
+      int64_t dst = src_base_at(s, c, p, mb);
+      for (int o = 0; o < c.rank; ++o) dst += s.all[(size_t(p) * W + o) * Nc + 1 + mb];
+      out.dwb_dst[p] = peer_dwb_of(c, s, p) + dst;
+    }
   return out;
 }
 
@@ -1176,9 +1225,11 @@ void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
   const int32_t* sp = s.sendpos + int64_t(mb) * (c.Rcap + 1);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
+    const bool marks = c.dwb && !s.zero_copy;
     k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
                                                                 s.zero_copy ? c.shard : s.buffer,
-                                                                s.zero_copy ? s.owner_rows : nullptr, out);
+                                                                s.zero_copy ? s.owner_rows : nullptr,
+                                                                marks ? s.src_tab : nullptr, c.W, s.owner_rows, out);
   });
   NEST_LAUNCH_CHECK();
 }
@@ -1289,20 +1340,25 @@ struct MbBases {
 };
 
 // (the loop trip count is warp-uniform: row-wise AdaGrad reduces sum g^2
-// across the row's lane group with shuffles)
+// across the row's lane group with shuffles).  n_done (optional) counts the
+// rows moved: contributions read + the frozen row read + the row written.
 template <int D, bool W1>
 __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
     const int32_t* __restrict__ n_dev, int N, int W, const OptStep opt, MbBases base,
     const uint32_t* __restrict__ mask, const int32_t* __restrict__ pos, int64_t pos_stride,
     const int32_t* __restrict__ src_tab, const int64_t* __restrict__ recv,
     const int32_t* __restrict__ sendpos, int64_t sp_stride, const float* __restrict__ rows,
-    const int32_t* __restrict__ owner_rows, float* __restrict__ buffer, float* __restrict__ shard) {
+    const int32_t* __restrict__ owner_rows, float* __restrict__ buffer, float* __restrict__ shard,
+    int dwb_skip, int32_t* __restrict__ n_done) {
   Grp<D> gp;
   constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
   const int64_t n = *n_dev;
   const bool ada = opt.kind == NEST_OPT_ROWWISE_ADAGRAD;
+  int32_t done = 0;
   for (int64_t u = gp.g; __any_sync(0xffffffffu, u < n); u += gp.ng) {
-    const bool act = u < n;
+    // direct write-back (SGD only): the sole contributor wrote this key back
+    const bool act = u < n && !(dwb_skip && sole_contributor(src_tab, u, W, recv));
+    if (act && gp.l == 0) done += 2;
     float4 acc[VPL];
 #pragma unroll
     for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1314,6 +1370,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
         const int64_t r = base.v[i] + __ldg(pos + i * pos_stride + u);
 #pragma unroll
         for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(rows + r * D + gp.col(v)));
+        if (gp.l == 0) ++done;
       }
     } else {
       for (int i = 0; i < N; ++i) {
@@ -1323,6 +1380,7 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
           const int64_t row = base.v[i] + __ldg(sendpos + i * sp_stride + r);
 #pragma unroll
           for (int v = 0; v < VPL; ++v) acc[v] = f4add(acc[v], ldg_f4(rows + row * D + gp.col(v)));
+          if (gp.l == 0) ++done;
         }
       }
     }
@@ -1368,23 +1426,32 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
       st_f4_cs(shard + srow * D + gp.col(v), e);
     }
   }
+  if (n_done && done) atomicAdd(n_done, done);
 }
 
+bool dwb_active(const Ctx& c, const Slot& s, const OptStep& opt) {
+  return c.dwb && c.W > 1 && !s.zero_copy && opt.kind == NEST_OPT_SGD;
+}
+
+// rows moved by the update are counted on the device (c.n_refreshed[3])
 void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& lr, cudaStream_t st) {
   MbBases b{};
   const bool w1 = c.W == 1;
   for (int i = 0; i < s.N; ++i) b.v[i] = w1 ? s.src_base[i] : s.own_base[i];
+  int32_t* cnt = c.n_refreshed + 3;
+  NEST_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
     const int grid = blocks_for_rows(c.Uocap, rpb, 148 * 16);
     if (w1)
       k_reduce_sgd<D, true><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, 1, lr, b, s.mask, s.pos, c.Kcap + 1, nullptr, nullptr, nullptr, 0,
-          src_rows_of(c, s), s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard);
+          src_rows_of(c, s), s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard, 0, cnt);
     else
       k_reduce_sgd<D, false><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, c.W, lr, b, nullptr, nullptr, 0, s.src_tab, s.recv, s.sendpos, c.Rcap + 1,
-          c.own_rows, s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard);
+          c.own_rows, s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard, dwb_active(c, s, lr) ? 1 : 0,
+          cnt);
   });
   NEST_LAUNCH_CHECK();
 }

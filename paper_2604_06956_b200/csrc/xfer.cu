@@ -37,8 +37,11 @@ namespace nest {
 using PFN_wait = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using PFN_write = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
+using PFN_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
 static PFN_wait g_wait = nullptr;
 static PFN_write g_write = nullptr;
+static PFN_range g_range = nullptr;
 
 static void load_driver_ops() {
   if (g_wait && g_write) return;
@@ -50,6 +53,11 @@ static void load_driver_ops() {
   NEST_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q));
   NEST_CHECK(q == cudaDriverEntryPointSuccess && fn, NEST_ERR_CUDA, "cuStreamWriteValue32 unavailable");
   g_write = reinterpret_cast<PFN_write>(fn);
+  // (optional: without it the shard is not exported and direct write-back stays off)
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_range = reinterpret_cast<PFN_range>(fn);
+  (void)cudaGetLastError();
 }
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -77,7 +85,20 @@ static int early_push_wanted() {
 //                 route counts [2 slots][W*W*Nc + Nmax + 1] i32 (route_window) |
 //                 received keys [2 slots][Rcap] i64 (route_window) |
 //                 tower dW exchange [2][n] f32 (trained tower without NCCL) |
+//                 direct write-back marks [slot 0 (| slot 1)][MBcap] i32 |
 //                 flags [2][XK_COUNT][Nmax][W] u32]
+//
+// Direct write-back (NEST_DIRECT_WB, default on; fused transport with SM
+// pushes, SGD, HBM tables): most keys of a batch have one contributor
+// (DLRM at W = 2: 87% of the owner-unique keys come from one source and one
+// micro-batch).  For those the owner's reduce would read one gradient row and
+// the frozen row and write the shard row; instead the owner's push marks the
+// row (its shard index), the requester applies Eq. 2 to its received frozen
+// copy -- the same fma on the same operands, so the same bits -- and stores
+// the updated row into the owner's shard over NVLink (or locally), and the
+// owner's reduce skips the key.  Ordering is unchanged: the owner's update
+// (and the refresh / re-push after it) waits for every requester's gradient
+// flag, which each requester raises after its segment-sum's stores.
 void xfer_alloc(Ctx& c, cudaStream_t st) {
   load_driver_ops();
   c.a2a_mode = a2a_mode_wanted(c.W);
@@ -101,12 +122,22 @@ void xfer_alloc(Ctx& c, cudaStream_t st) {
   const size_t key_b = c.route_window ? align_up(2 * key1, 4096) : 0;
   const size_t twr_b = align_up(sizeof(float) * 2 * size_t(c.twr_elems), 4096);
   const size_t flg_b = align_up(size_t(2) * XK_COUNT * c.Nmax * c.W * sizeof(uint32_t), 4096);
+  {
+    const char* e = std::getenv("NEST_DIRECT_WB");
+    c.dwb_wanted = !(e && std::strcmp(e, "0") == 0) && c.a2a_mode == A2A_FUSED && !c.grad_ce &&
+                   c.early_push != EP_CE && c.cfg.table_location == NEST_TABLE_HBM &&
+                   c.cfg.optimizer == NEST_OPT_SGD;
+  }
+  const size_t dwb1 = align_up(sizeof(int32_t) * size_t(c.MBcap), 4096);
+  const size_t dwb_b = c.dwb_wanted ? (c.early_push ? 2 * dwb1 : dwb1) : 0;
+  c.dwb_slot_stride = c.early_push ? int64_t(dwb1 / sizeof(int32_t)) : 0;
   c.src_slot_stride = c.early_push ? int64_t(src1 / sizeof(float)) : 0;
   c.xoff_own = src_b;
   c.xoff_cnt = src_b + own_b;
   c.xoff_key = c.xoff_cnt + cnt_b;
   c.xoff_twr = c.xoff_key + key_b;
-  c.xoff_flags = c.xoff_twr + twr_b;
+  c.xoff_dwb = c.xoff_twr + twr_b;
+  c.xoff_flags = c.xoff_dwb + dwb_b;
   c.xcnt_stride = cnt1;
   c.xkey_stride = key1;
   c.xwin_bytes = c.xoff_flags + flg_b;
@@ -125,6 +156,7 @@ void xfer_alloc(Ctx& c, cudaStream_t st) {
     }
   }
   c.twr = c.twr_elems ? reinterpret_cast<float*>(base + c.xoff_twr) : nullptr;
+  c.dwb_marks = c.dwb_wanted ? reinterpret_cast<int32_t*>(base + c.xoff_dwb) : nullptr;
 }
 
 void xfer_export(const Ctx& c, nest_window_rec_t* r) {
@@ -151,6 +183,23 @@ void xfer_export(const Ctx& c, nest_window_rec_t* r) {
   r->src_stride = uint64_t(c.src_slot_stride);
   r->cnt_stride = c.xcnt_stride;
   r->key_stride = c.xkey_stride;
+  r->off_dwb = c.xoff_dwb;
+  r->dwb_stride = uint64_t(c.dwb_slot_stride);
+  r->shard_ptr = reinterpret_cast<uint64_t>(c.shard);
+  if (c.dwb_wanted && g_range) {
+    // the shard is caller memory (e.g. a block of PyTorch's allocator): export
+    // the allocation that holds it, plus the offset
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    cudaIpcMemHandle_t sh;
+    if (g_range(&b, &sz, reinterpret_cast<CUdeviceptr>(c.shard)) == CUDA_SUCCESS &&
+        cudaIpcGetMemHandle(&sh, reinterpret_cast<void*>(b)) == cudaSuccess) {
+      std::memcpy(r->shard_ipc, &sh, sizeof(sh));
+      r->shard_off = reinterpret_cast<uint64_t>(c.shard) - uint64_t(b);
+      r->dwb_ok = 1;
+    }
+    (void)cudaGetLastError();
+  }
 }
 
 // map every peer's window: the same process (in-process ranks sharing one
@@ -207,6 +256,32 @@ void xfer_connect(Ctx& c, const nest_window_rec_t* all) {
   // (no barrier needed: the first push happens after the first route's count
   // exchange, which every rank enters after connecting)
   c.xfer_ce = true;
+  // direct write-back runs iff every rank can take part
+  bool dwb = c.dwb_wanted;
+  for (int p = 0; p < c.W; ++p) dwb = dwb && all[p].dwb_ok == 1 && all[p].off_dwb == c.xoff_dwb;
+  c.dwb = dwb;
+  if (dwb) {
+    c.peer_shard.assign(c.W, nullptr);
+    for (int si = 0; si < 2; ++si) c.peer_dwb_slot[si].assign(c.W, nullptr);
+    for (int p = 0; p < c.W; ++p) {
+      const nest_window_rec_t& r = all[p];
+      char* base = reinterpret_cast<char*>(c.peer_src[p]);   // window base
+      for (int si = 0; si < 2; ++si)
+        c.peer_dwb_slot[si][p] = reinterpret_cast<int32_t*>(base + r.off_dwb) + si * int64_t(r.dwb_stride);
+      if (p == c.rank) {
+        c.peer_shard[p] = c.shard;
+      } else if (r.pid == me_pid) {
+        c.peer_shard[p] = reinterpret_cast<float*>(r.shard_ptr);
+      } else {
+        void* ptr = nullptr;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, r.shard_ipc, sizeof(h));
+        NEST_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        c.peer_shard_map.push_back(ptr);
+        c.peer_shard[p] = reinterpret_cast<float*>(reinterpret_cast<char*>(ptr) + r.shard_off);
+      }
+    }
+  }
   c.connected = true;
 }
 
@@ -231,6 +306,8 @@ void xfer_destroy(Ctx& c) {
   for (void* p : c.peer_win)
     if (p) cudaIpcCloseMemHandle(p);
   c.peer_win.clear();
+  for (void* p : c.peer_shard_map) cudaIpcCloseMemHandle(p);
+  c.peer_shard_map.clear();
   if (c.xwin) cudaFree(c.xwin);
   c.xwin = nullptr;
   if (c.send_stage) cudaFree(c.send_stage);

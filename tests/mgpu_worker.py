@@ -23,6 +23,7 @@ import torch.distributed as dist  # noqa: E402
 
 import multirank as MR  # noqa: E402
 from paper_2604_06956_b200 import unique_ids  # noqa: E402
+from paper_2604_06956_b200._lib import WindowRec  # noqa: E402
 
 SAME_DEVICE = os.environ.get("NEST_MGPU_SAME_DEVICE", "0") == "1"
 NO_NCCL = SAME_DEVICE or os.environ.get("NEST_MGPU_NO_NCCL", "0") == "1"
@@ -43,8 +44,13 @@ def ctx_kw(rank):
 def connect(ctx, world):
     if NO_NCCL:
         recs = [None] * world
-        dist.all_gather_object(recs, ctx.window_export())
+        mine = ctx.window_export()
+        dist.all_gather_object(recs, mine)
         ctx.window_connect(recs)
+        # direct write-back of sole-contributor keys (fused transport, SGD, HBM):
+        # this rank exported its shard for the peers' write-backs
+        rec = WindowRec.from_buffer_copy(mine)
+        print(f"[window] rank {dist.get_rank()}: direct write-back {'on' if rec.dwb_ok else 'off'}", flush=True)
 
 
 def run_case(case, rank, world, dev):

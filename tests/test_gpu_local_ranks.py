@@ -30,7 +30,9 @@ TRANSPORTS = {"fused-early": {}, "ce": {"NEST_A2A": "ce"}, "fused-range": {"NEST
               # checked mode: guard bands after every workspace buffer verified after each case
               "fused-early-guard": {"NEST_GUARD": "1"},
               # zero-copy retrieval: owners push / update their shard rows in place
-              "fused-early-zerocopy": {"NEST_ZERO_COPY": "1"}}
+              "fused-early-zerocopy": {"NEST_ZERO_COPY": "1"},
+              # every key's gradient row goes to its owner (no direct write-back)
+              "fused-early-nodwb": {"NEST_DIRECT_WB": "0"}}
 
 
 def _port():
@@ -45,7 +47,8 @@ def _port():
                                                  (8, "fused-early", False), (2, "ce", False),
                                                  (4, "fused-range", False), (2, "fused-window", False),
                                                  (2, "fused-early-ce", False), (4, "fused-early-guard", False),
-                                                 (2, "fused-early-zerocopy", True), (4, "fused-early-zerocopy", False)])
+                                                 (2, "fused-early-zerocopy", True), (4, "fused-early-zerocopy", False),
+                                                 (2, "fused-early-nodwb", True)])
 def test_local_ranks_parity(world, transport, big):
     def cmd():
         return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
@@ -59,3 +62,6 @@ def test_local_ranks_parity(world, transport, big):
             break
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0 and "MGPU ALL OK" in r.stdout
+    # the direct write-back runs wherever it applies (fused SM pushes, SGD, HBM)
+    dwb = "direct write-back on" in r.stdout
+    assert dwb == (transport not in ("ce", "fused-early-ce", "fused-early-nodwb")), "direct write-back state"

@@ -34,7 +34,9 @@ TRANSPORTS = {"fused-early": {}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
               # count exchange + key All2All over the windows too (no NCCL on the route)
               "fused-early-routewin": {"NEST_ROUTE_XCHG": "window"},
               # no NCCL at all: windows connected through torch.distributed
-              "no-nccl": {"NEST_MGPU_NO_NCCL": "1"}}
+              "no-nccl": {"NEST_MGPU_NO_NCCL": "1"},
+              # every key's gradient row to its owner (no direct write-back)
+              "fused-early-nodwb": {"NEST_DIRECT_WB": "0"}}
 
 
 @pytest.mark.parametrize("world,transport", [(2, t) for t in TRANSPORTS] +
