@@ -133,7 +133,11 @@ def roofline_from(st, key_prefix):
 
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
-    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
+    """nvidia-smi samples (every 50 ms) of SM clocks and throttle reasons.  The
+    sampler starts before the warm-up; the timed region is marked with host
+    wall-clock times and only the samples inside it are used (the nearest one
+    when the region is shorter than the sampling period)."""
+    FIELDS = "timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active," \
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
 
@@ -141,6 +145,7 @@ class Clocks:
         self.gpu = gpu_index
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_gpu{gpu_index}.csv")
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -152,6 +157,20 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    @staticmethod
+    def _ts(x):
+        import datetime
+        try:
+            return datetime.datetime.strptime(x, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
     def stop(self):
         if not self.proc:
             return None
@@ -162,23 +181,30 @@ class Clocks:
         except Exception:
             self.proc.kill()
         self.f.close()
-        sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
+                smv, mxv = float(parts[2]), float(parts[3])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
+            rs = {n for n, v in zip(names, parts[6:10]) if v.lower().startswith("active")}
+            rows.append((self._ts(parts[0]), smv, mxv, rs))
+        if not rows:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+        sel = rows
+        if self.t0 is not None and self.t1 is not None and all(r[0] is not None for r in rows):
+            inside = [r for r in rows if self.t0 <= r[0] <= self.t1]
+            mid = 0.5 * (self.t0 + self.t1)
+            sel = inside or [min(rows, key=lambda r: abs(r[0] - mid))]
+        reasons = set().union(*(r[3] for r in sel))
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": max(r[2] for r in sel),
+                "samples": len(sel), "samples_in_timed_region": len([r for r in sel if self.t0 is not None
+                                                                     and r[0] is not None
+                                                                     and self.t0 <= r[0] <= self.t1]),
                 "reasons": sorted(reasons)}
 
 
@@ -462,10 +488,12 @@ def main():
     runner = Runner(ctx, N=N, schedule=args.schedule, pipelined=True, lr_over_B=lr, adagrad=adagrad,
                     sched_cache=sched_cache, route_end=rend[args.variant],
                     pooled_dtype=pooled_dtype(args.variant))
-    timed(runner, args.warmup, 0)
     clocks = Clocks(local)
-    clocks.start()
+    clocks.start()   # before the warm-up: nvidia-smi's first sample takes ~0.1-0.3 s
+    timed(runner, args.warmup, 0)
+    clocks.mark_start()
     ms, prof, _, _ = timed(runner, args.steps, args.warmup, profile=True)
+    clocks.mark_end()
     clk = clocks.stop()
     trace_records = prof.get("records")
     value = B * world * args.steps / (ms / 1e3)

@@ -15,7 +15,7 @@ for f in sys.argv[1:]:
           f"({d['roofline']['kernel']}) | pool {st.get('pool',{}).get('ms_per_step',0):.3f} "
           f"segsum {st.get('segsum',{}).get('ms_per_step',0):.3f} | E {eo.get('ms_per_step',0):.3f}ms "
           f"frac {eo.get('roofline',{}).get('frac',0):.3f} pool {es.get('pool',0):.3f} seg {es.get('segsum',0):.3f} "
-          f"sort {es.get('sort',0):.3f} route {es.get('route',0):.3f} | clk {d.get('clocks',{}).get('sm_mhz')}")
+          f"sort {es.get('sort',0):.3f} route {es.get('route',0):.3f} | clk {(d.get('clocks') or {}).get('sm_mhz')}")
     zc = d.get("zero_copy")
     if zc:
         print(f"    zero-copy: ET {zc['et']['samples_per_s']/1e6:.2f}M {zc['et']['ms_per_step']:.3f}ms "

@@ -63,3 +63,41 @@ def test_cpu_model_and_tiny_oracle_baseline():
     t = bench.tiny_oracle_baseline(0, steps=2)
     assert t["steps"] == 2 and t["value"] > 0 and "tiny" in t["sample"]
     json.dumps(t)
+
+
+def test_clock_samples_are_taken_inside_the_timed_region(tmp_path):
+    """bench.Clocks keeps the nvidia-smi samples whose timestamps fall inside
+    the marked timed region (the nearest one if none does) and reports the
+    throttle reasons seen there."""
+    import datetime
+
+    def line(t, sm, reasons=("Not Active",) * 4):
+        ts = datetime.datetime.fromtimestamp(t).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        return ", ".join([ts, "0", str(sm), "1965", "900.0", "0x0"] + list(reasons)) + "\n"
+
+    c = bench.Clocks(0)
+    c.path = str(tmp_path / "clk.csv")
+    t = 1_700_000_000.0
+    with open(c.path, "w") as f:
+        f.write(line(t - 1.0, 1200, ("Active", "Not Active", "Not Active", "Not Active")))   # warm-up
+        f.write(line(t + 0.10, 1900))
+        f.write(line(t + 0.15, 1950, ("Not Active", "Not Active", "Not Active", "Active")))
+        f.write(line(t + 5.0, 1000))                                                           # after
+
+    class _P:
+        def terminate(self):
+            pass
+
+        def wait(self, timeout=None):
+            return 0
+
+    c.proc, c.f = _P(), open(str(tmp_path / "sink"), "w")
+    c.t0, c.t1 = t, t + 0.2
+    r = c.stop()
+    assert r["samples"] == 2 and r["samples_in_timed_region"] == 2
+    assert r["sm_mhz"] == pytest.approx(1925.0) and r["reasons"] == ["sw_power_cap"]
+    # a region between two samples: the nearest sample stands in
+    c.proc, c.f = _P(), open(str(tmp_path / "sink2"), "w")
+    c.t0, c.t1 = t + 0.16, t + 0.17
+    r = c.stop()
+    assert r["samples"] == 1 and r["samples_in_timed_region"] == 0 and r["sm_mhz"] == 1950.0
