@@ -207,6 +207,8 @@ static size_t layout(Ctx& c, char* base) {
       s.owner_inv = w.take<int32_t>(R);
       s.src_tab = w.take<int32_t>(Uo * W);
       s.sendpos = w.take<int32_t>(Nm * (R + 1));
+      s.upd_list = w.take<int32_t>(Uo);
+      s.n_upd = w.take<int32_t>(1);
     }
     s.buffer = w.take<float>(Uo * D);
   }

@@ -103,6 +103,10 @@ struct Slot {
   int32_t* src_tab = nullptr;      // [Uocap][W] received position per source, -1 if none
   int32_t* sendpos = nullptr;      // [Nmax][Rcap+1]
   int32_t* n_owner = nullptr;      // [1] U_o
+  // direct write-back (W > 1): the owner keys with >= 2 contributions, the
+  // only ones the owner's update touches (any order: keys are independent)
+  int32_t* upd_list = nullptr;     // [Uocap]
+  int32_t* n_upd = nullptr;        // [1]
   float* buffer = nullptr;         // [Uocap][d] HBM buffer (active / prefetch)
   // host-known plan
   nest_slot_info_t info{};
@@ -688,6 +692,7 @@ struct OptStep {
 };
 void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& opt, cudaStream_t st);
 bool dwb_active(const Ctx& c, const Slot& s, const OptStep& opt);
+void launch_upd_list(Ctx& c, Slot& s, cudaStream_t st);
 void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, cudaStream_t st);
 void launch_read_state(Ctx& c, const int64_t* keys, int64_t n, float* out, cudaStream_t st);
 enum EarlyPush : int { EP_OFF = 0, EP_CE = 1, EP_SM = 2 };

@@ -980,6 +980,10 @@ void route_phase_b(Ctx& c, Slot& s, cudaStream_t st) {
             [=] __device__(int64_t r, int32_t v) { sp[r] = v; }, c.scan_tmp, st);
       }
       ps.launches = 2 * (R > 0) + 3 + 1 + 3 * N;
+      if (c.dwb && !s.zero_copy) {
+        launch_upd_list(c, s, st);   // the keys the owner's update will touch
+        ps.launches += 1;
+      }
       ps.bytes = 12.0 * double(R);  // 12 R_o + 8 U_o
       ps.dcount = s.n_owner;
       ps.bpc = 8.0;

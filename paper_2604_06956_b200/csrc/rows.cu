@@ -1349,15 +1349,16 @@ __global__ void __launch_bounds__(kRowThreads) k_reduce_sgd(
     const int32_t* __restrict__ src_tab, const int64_t* __restrict__ recv,
     const int32_t* __restrict__ sendpos, int64_t sp_stride, const float* __restrict__ rows,
     const int32_t* __restrict__ owner_rows, float* __restrict__ buffer, float* __restrict__ shard,
-    int dwb_skip, int32_t* __restrict__ n_done) {
+    const int32_t* __restrict__ list, int32_t* __restrict__ n_done) {
   Grp<D> gp;
   constexpr int VPL = RowGeom<D>::VPL, L = RowGeom<D>::L;
   const int64_t n = *n_dev;
   const bool ada = opt.kind == NEST_OPT_ROWWISE_ADAGRAD;
   int32_t done = 0;
-  for (int64_t u = gp.g; __any_sync(0xffffffffu, u < n); u += gp.ng) {
-    // direct write-back (SGD only): the sole contributor wrote this key back
-    const bool act = u < n && !(dwb_skip && sole_contributor(src_tab, u, W, recv));
+  for (int64_t q = gp.g; __any_sync(0xffffffffu, q < n); q += gp.ng) {
+    // direct write-back (SGD only): only the listed keys (>= 2 contributions)
+    const bool act = q < n;
+    const int64_t u = list && act ? int64_t(__ldg(list + q)) : q;
     if (act && gp.l == 0) done += 2;
     float4 acc[VPL];
 #pragma unroll
@@ -1433,6 +1434,31 @@ bool dwb_active(const Ctx& c, const Slot& s, const OptStep& opt) {
   return c.dwb && c.W > 1 && !s.zero_copy && opt.kind == NEST_OPT_SGD;
 }
 
+// the owner keys with >= 2 contributions (warp-aggregated append; the order
+// is irrelevant: every key's update is independent and fixed-order inside)
+__global__ void __launch_bounds__(256) k_upd_list(const int32_t* __restrict__ n_owner,
+                                                  const int32_t* __restrict__ src_tab, int W,
+                                                  const int64_t* __restrict__ recv, int32_t* __restrict__ list,
+                                                  int32_t* __restrict__ cnt) {
+  const int64_t n = *n_owner;
+  const int lane = lane_id();
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; __any_sync(0xffffffffu, u < n);
+       u += int64_t(gridDim.x) * blockDim.x) {
+    const bool keep = u < n && !sole_contributor(src_tab, u, W, recv);
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    int32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(cnt, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) list[base + __popc(m & ((1u << lane) - 1u))] = int32_t(u);
+  }
+}
+
+void launch_upd_list(Ctx& c, Slot& s, cudaStream_t st) {
+  NEST_CUDA(cudaMemsetAsync(s.n_upd, 0, sizeof(int32_t), st));
+  k_upd_list<<<148 * 8, 256, 0, st>>>(s.n_owner, s.src_tab, c.W, s.recv, s.upd_list, s.n_upd);
+  NEST_LAUNCH_CHECK();
+}
+
 // rows moved by the update are counted on the device (c.n_refreshed[3])
 void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& lr, cudaStream_t st) {
   MbBases b{};
@@ -1440,18 +1466,20 @@ void launch_reduce_sgd(Ctx& c, Slot& s, const OptStep& lr, cudaStream_t st) {
   for (int i = 0; i < s.N; ++i) b.v[i] = w1 ? s.src_base[i] : s.own_base[i];
   int32_t* cnt = c.n_refreshed + 3;
   NEST_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
+  // direct write-back: only the keys with >= 2 contributions (listed by the route)
+  const bool dwb = !w1 && dwb_active(c, s, lr);
   NEST_DISPATCH_D(c.D, {
     const int rpb = (kRowThreads / 32) * RowGeom<D>::GPW;
     const int grid = blocks_for_rows(c.Uocap, rpb, 148 * 16);
     if (w1)
       k_reduce_sgd<D, true><<<grid, kRowThreads, 0, st>>>(
           s.n_owner, s.N, 1, lr, b, s.mask, s.pos, c.Kcap + 1, nullptr, nullptr, nullptr, 0,
-          src_rows_of(c, s), s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard, 0, cnt);
+          src_rows_of(c, s), s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard, nullptr, cnt);
     else
       k_reduce_sgd<D, false><<<grid, kRowThreads, 0, st>>>(
-          s.n_owner, s.N, c.W, lr, b, nullptr, nullptr, 0, s.src_tab, s.recv, s.sendpos, c.Rcap + 1,
-          c.own_rows, s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard, dwb_active(c, s, lr) ? 1 : 0,
-          cnt);
+          dwb ? s.n_upd : s.n_owner, s.N, c.W, lr, b, nullptr, nullptr, 0, s.src_tab, s.recv, s.sendpos,
+          c.Rcap + 1, c.own_rows, s.owner_rows, s.zero_copy ? nullptr : s.buffer, c.shard,
+          dwb ? s.upd_list : nullptr, cnt);
   });
   NEST_LAUNCH_CHECK();
 }
