@@ -283,7 +283,8 @@ static void lookup_comm(Ctx& c, Slot& s, int mb, cudaStream_t cs, cudaStream_t m
       ProfScope ps(c, ST_EMB_A2A, SK_COMM, ms);
       launch_send_push(c, s, mb, ms);
       int64_t self = s.all[(size_t(c.rank) * c.W + c.rank) * (c.Nmax + 2) + 1 + mb];
-      ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+      ps.dcount = c.n_refreshed + 1;   // rows sent off-GPU (counted on the device)
+      ps.bpc = row;
       ps.hbm = row * double(s.info.mb_recv[mb] + self);    // rows gathered + rows stored locally
     }
     NEST_CUDA(cudaEventRecord(s.ev_emb[mb], ms));
@@ -658,8 +659,10 @@ nest_status_t nest_route_end(nest_ctx_t* ctx, int32_t slot) {
           ps.hbm = row * double(s.info.mb_recv[mb] + self);    // staged rows read + self rows stored
         } else {
           ProfScope ps(*c, ST_EMB_A2A, SK_AUX, st);
-          launch_send_push(*c, s, mb, st);
-          ps.bytes = row * double(s.info.mb_recv[mb] - self);  // rows sent off-GPU
+          // the rows of the pending update's keys are left to the re-push
+          launch_send_push(*c, s, mb, st, s.refresh_pending ? c->slot[1 - slot].obm : nullptr);
+          ps.dcount = c->n_refreshed + 1;   // rows sent off-GPU (counted on the device)
+          ps.bpc = row;
           ps.hbm = row * double(s.info.mb_recv[mb] + self);    // rows gathered + rows stored locally
           xfer_signal(*c, s, XK_EMB, mb, st);
         }

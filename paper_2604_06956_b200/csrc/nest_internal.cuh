@@ -699,7 +699,7 @@ enum EarlyPush : int { EP_OFF = 0, EP_CE = 1, EP_SM = 2 };
 int a2a_mode_wanted(int W);
 int64_t src_base_at(const Slot& s, const Ctx& c, int p, int mb);
 int64_t own_base_at(const Slot& s, const Ctx& c, int p, int mb);
-void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st);
+void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st, const uint32_t* stale_bm = nullptr);
 // dual-buffer refresh a -> p fused with the re-push of the refreshed rows to
 // every requester of micro-batch mb of slot p (early push)
 void launch_refresh_push(Ctx& c, Slot& a, Slot& p, int mb, cudaStream_t st);

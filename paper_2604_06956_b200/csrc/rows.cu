@@ -1127,7 +1127,10 @@ void launch_segsum_sgd(Ctx& c, Slot& s, const float* dout, const OptStep& opt, c
 // the requester's receive rows (peer memory over NVLink; own rows locally)
 // (direct write-back: src_tab != nullptr -- each row's mark, its shard row
 // if the requester is the key's sole contributor else -1, is stored into the
-// requester's mark area at the row's index)
+// requester's mark area at the row's index.  stale_bm: the early push skips
+// the rows of the pending update's keys -- the skipping gather left them
+// stale in the buffer and the re-push after that update sends them anyway.
+// Rows stored off-GPU are counted into *sent.)
 template <int D>
 __global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, const int64_t* __restrict__ recv,
                                                            const int32_t* __restrict__ owner_inv,
@@ -1136,8 +1139,10 @@ __global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, co
                                                            const int32_t* __restrict__ rowmap,
                                                            const int32_t* __restrict__ src_tab, int W,
                                                            const int32_t* __restrict__ owner_rows,
-                                                           const PeerRows out) {
+                                                           const uint32_t* __restrict__ stale_bm, int self,
+                                                           int32_t* __restrict__ sent, const PeerRows out) {
   Grp<D> gp;
+  int32_t nsent = 0;
   for (int64_t r = gp.g; r < R; r += gp.ng) {
     if (!((uint64_t(__ldg(recv + r)) >> (56 + mb)) & 1u)) continue;
     const int32_t p = __ldg(sendpos + r);
@@ -1148,9 +1153,12 @@ __global__ void __launch_bounds__(kRowThreads) k_send_push(int64_t R, int mb, co
     const float* src = buffer + int64_t(rowmap ? __ldg(rowmap + k) : k) * D;
     if (src_tab && gp.l == 0)
       out.dwb_dst[s][p - out.off[s]] = sole_contributor(src_tab, k, W, recv) ? __ldg(owner_rows + k) : -1;
+    if (stale_bm && bit_test(stale_bm, uint32_t(__ldg(owner_rows + k)))) continue;
+    if (gp.l == 0 && s != self) ++nsent;
 #pragma unroll
     for (int v = 0; v < RowGeom<D>::VPL; ++v) st_f4(dst + gp.col(v), ldg_f4(src + gp.col(v)));
   }
+  if (sent && nsent) atomicAdd(sent, nsent);
   __threadfence_system();
 }
 
@@ -1218,7 +1226,8 @@ static PeerRows send_map(Ctx& c, Slot& s, int mb) {
   return out;
 }
 
-void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
+void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st, const uint32_t* stale_bm) {
+  NEST_CUDA(cudaMemsetAsync(c.n_refreshed + 1, 0, sizeof(int32_t), st));
   const int64_t R = s.info.recv;
   if (R == 0) return;
   const PeerRows out = send_map(c, s, mb);
@@ -1229,7 +1238,9 @@ void launch_send_push(Ctx& c, Slot& s, int mb, cudaStream_t st) {
     k_send_push<D><<<emb_blocks(R, rpb), kRowThreads, 0, st>>>(R, mb, s.recv, s.owner_inv, sp,
                                                                 s.zero_copy ? c.shard : s.buffer,
                                                                 s.zero_copy ? s.owner_rows : nullptr,
-                                                                marks ? s.src_tab : nullptr, c.W, s.owner_rows, out);
+                                                                marks ? s.src_tab : nullptr, c.W, s.owner_rows,
+                                                                s.zero_copy ? nullptr : stale_bm, c.rank,
+                                                                c.n_refreshed + 1, out);
   });
   NEST_LAUNCH_CHECK();
 }
