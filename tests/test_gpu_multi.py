@@ -32,7 +32,8 @@ TRANSPORTS = {"fused-early": {}, "fused-early-ce": {"NEST_EARLY_PUSH": "ce"},
               "fused-window": {"NEST_EARLY_PUSH": "0"}, "ce": {"NEST_A2A": "ce"},
               "nccl": {"NEST_A2A": "nccl"},
               # count exchange + key All2All over the windows too (no NCCL on the route)
-              "fused-early-routewin": {"NEST_ROUTE_XCHG": "window"},
+              # count exchange + key All2All over NCCL (the default puts them on the windows)
+              "fused-early-routenccl": {"NEST_ROUTE_XCHG": "nccl"},
               # no NCCL at all: windows connected through torch.distributed
               "no-nccl": {"NEST_MGPU_NO_NCCL": "1"},
               # every key's gradient row to its owner (no direct write-back)
