@@ -68,3 +68,39 @@ def test_sm100a_cubin_present():
     B.build()
     out = subprocess.run(["cuobjdump", "--list-elf", B.LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+# every struct of include/nest.h and its ctypes mirror in _lib.py
+_STRUCTS = {"nest_config_t": "Config", "nest_slot_info_t": "SlotInfo", "nest_route_view_t": "RouteView",
+            "nest_window_rec_t": "WindowRec", "nest_exchange_plan_t": "ExchangePlan",
+            "nest_profile_stage_t": "ProfileStage", "nest_profile_summary_t": "ProfileSummary",
+            "nest_profile_record_t": "ProfileRecord"}
+
+
+def test_ctypes_mirrors_match_the_header(tmp_path):
+    """sizeof and every field offset of the header's structs, compiled by gcc,
+    equal the ctypes mirrors the binding passes through the ABI."""
+    import shutil
+    import subprocess
+    from paper_2604_06956_b200 import _lib as L
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "nest.h"', "int main(void) {"]
+    for cname, pyname in _STRUCTS.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f in getattr(L, pyname)._fields_:
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        s, f, v = ln.split()
+        got[(s, f)] = int(v)
+    for cname, pyname in _STRUCTS.items():
+        py = getattr(L, pyname)
+        assert got[(cname, "sizeof")] == C.sizeof(py), cname
+        for f in py._fields_:
+            assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
