@@ -318,6 +318,11 @@ def config_json(args, cfg, world):
             "pipelined": "DBP (route t+1 on the aux stream)" + (
                 f" + FWP ({args.micro_batches} micro-batches, comm/compute streams)" if args.micro_batches > 1
                 else "; FWP off (1 micro-batch; FWP at N=2 measured alongside when W > 1)"),
+            "exchanges": None if world == 1 else (
+                f"rows: {os.environ.get('NEST_A2A', 'fused')} (fused = SM peer stores into IPC-mapped windows), "
+                f"counts/keys: {os.environ.get('NEST_ROUTE_XCHG', 'window')}, early push: "
+                f"{os.environ.get('NEST_EARLY_PUSH', 'sm')}, direct write-back: "
+                f"{'off' if os.environ.get('NEST_DIRECT_WB') == '0' else 'on'}"),
             "tower_trained": bool(getattr(args, "tower_train", False)),
             "tables_in": "HBM" if getattr(args, "tables", "hbm") == "hbm" else
                          "pinned host DRAM (retrieval / refresh / write-back over PCIe)"}
