@@ -29,6 +29,7 @@ struct Tower {
   cublasHandle_t h = nullptr;
   cublasLtHandle_t lt = nullptr;
   int32_t sm_target = 0;
+  int32_t sm_target_dw = 0;   // the weight-gradient GEMMs (the only transposed-A ones)
   std::map<std::string, struct GemmPlan> plans;
   int L = 0, H = 0, in0 = 0;
   int64_t bmax = 0;
@@ -196,6 +197,11 @@ void tower_create(Ctx& c) {
       NEST_CUBLAS(cublasSetSmCountTarget(t->h, sms - reserve));
       t->sm_target = sms - reserve;
     }
+    // the deferred dW GEMMs run beside the segment-sum, refresh and the next
+    // pool: NEST_TOWER_DW_SM_RESERVE (default: the same reserve)
+    const char* rd = std::getenv("NEST_TOWER_DW_SM_RESERVE");
+    const int reserve_dw = rd ? std::atoi(rd) : reserve;
+    t->sm_target_dw = reserve_dw > 0 && reserve_dw < sms ? sms - reserve_dw : 0;
   }
   NEST_CUBLAS(cublasLtCreate(&t->lt));
   for (int l = 0; l < L; ++l) {
@@ -248,9 +254,11 @@ static GemmPlan& plan_for(Tower* t, bool ta, bool tb, int M, int N, int K, int l
   const cublasOperation_t oa = tb ? CUBLAS_OP_T : CUBLAS_OP_N, ob = ta ? CUBLAS_OP_T : CUBLAS_OP_N;
   NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSA, &oa, sizeof(oa)));
   NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_TRANSB, &ob, sizeof(ob)));
-  if (t->sm_target > 0)
-    NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_SM_COUNT_TARGET, &t->sm_target,
-                                               sizeof(t->sm_target)));
+  // (ta: the dW GEMMs dY^T X are the only ones with a transposed A)
+  const int32_t target = ta ? t->sm_target_dw : t->sm_target;
+  if (target > 0)
+    NEST_CUBLAS(cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_SM_COUNT_TARGET, &target,
+                                               sizeof(target)));
   NEST_CUBLAS(cublasLtMatrixLayoutCreate(&p.a, CUDA_R_16BF, oa == CUBLAS_OP_N ? N : K, oa == CUBLAS_OP_N ? K : N, ldb));
   NEST_CUBLAS(cublasLtMatrixLayoutCreate(&p.b, CUDA_R_16BF, ob == CUBLAS_OP_N ? K : M, ob == CUBLAS_OP_N ? M : K, lda));
   NEST_CUBLAS(cublasLtMatrixLayoutCreate(&p.c, ctype, N, M, ldc));
