@@ -64,6 +64,16 @@ class Case:
         return batches, douts
 
 
+def overlap_batches(cfg, B, T, world, p_reuse=0.7, seed=41):
+    """DBP stress at W > 1: each rank's batch t+1 reuses batch t's key at the
+    same slot with probability p_reuse (BASELINE configs[3]), so the refresh /
+    re-push (and the early push leaving the pending update's rows to it) carry
+    a large intersection."""
+    c = cfg.with_(batch_local=B)
+    per = [WL.gen_overlap_batches(c, seed, T, r, p_reuse) for r in range(world)]
+    return [[per[r][t] for r in range(world)] for t in range(T)]
+
+
 def cases(big=True):
     out = [
         Case("tiny-P1-N2", WL.CONFIGS["tiny"], 32, 2, 6, "dyadic", "dyadic", 2.0 ** -10),
@@ -92,6 +102,9 @@ def cases(big=True):
             Case("mid-P2-N4", WL.CONFIGS["tiny"].with_(table_rows=(20000, 5000, 333, 100000), zipf=1.1,
                                                        bag_repeats=True, dim=64), 2048, 4, 4, "uniform",
                  "realistic", 0.02),
+            Case("dbp-overlap-P1-N1", WL.CONFIGS["tiny"].with_(table_rows=(20000, 5000, 3000, 10000), zipf=1.1,
+                                                               bag_repeats=True, dim=64),
+                 512, 1, 5, "dyadic", "dyadic", 2.0 ** -12, gen=overlap_batches),
         ]
     return out
 
