@@ -101,3 +101,18 @@ def test_clock_samples_are_taken_inside_the_timed_region(tmp_path):
     c.t0, c.t1 = t + 0.16, t + 0.17
     r = c.stop()
     assert r["samples"] == 1 and r["samples_in_timed_region"] == 0 and r["sm_mhz"] == 1950.0
+
+
+def test_config_json_names_the_workload_and_exchanges(monkeypatch):
+    import argparse
+    import workload as WL
+    monkeypatch.delenv("NEST_A2A", raising=False)
+    monkeypatch.setenv("NEST_DIRECT_WB", "0")
+    args = argparse.Namespace(micro_batches=1, schedule="sequential", optimizer="sgd", variant="et")
+    cfg = WL.CONFIGS["dlrm"]
+    one = bench.config_json(args, cfg, 1)
+    two = bench.config_json(args, cfg, 2)
+    assert one["workload"] == "dlrm" and one["exchanges"] is None and one["global_batch"] == cfg.batch_local
+    assert two["global_batch"] == 2 * cfg.batch_local
+    assert "fused" in two["exchanges"] and "direct write-back: off" in two["exchanges"]
+    json.dumps(two)
